@@ -1,0 +1,75 @@
+"""ctypes binding of the C-ABI kernel library (include/netfuse_b200.h).
+
+The library is built in-tree by :mod:`paper_2009_13062_b200.build`. There is
+no fallback: if the shared object is missing or a CUDA device is absent, any
+compute call raises. :func:`load` only opens the library (no device work), so
+symbol checks run on CPU-only machines.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from .errors import ExecutionError, ShapeError, UnsupportedOpError
+
+LIB_PATH = Path(__file__).resolve().parent / "libnetfuse_b200.so"
+HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "netfuse_b200.h"
+
+NF_OK, NF_ERR_SHAPE, NF_ERR_UNSUPPORTED, NF_ERR_LAUNCH = 0, 1, 2, 3
+NF_F32, NF_BF16 = 0, 1
+NF_ACT_NONE, NF_ACT_RELU, NF_ACT_GELU, NF_ACT_TANH = 0, 1, 2, 3
+NF_MODE_FAST, NF_MODE_EXACT = 0, 1
+NF_W_NK, NF_W_KN = 0, 1
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i = ctypes.c_int
+_f = ctypes.c_float
+
+# name -> argtypes; must mirror include/netfuse_b200.h exactly.
+SIGNATURES: dict[str, list] = {
+    "nf_abi_version": [],
+    "nf_status_string": [_i],
+    "nf_grouped_linear": [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _i, _i, _i, _p],
+}
+
+_RESTYPES = {"nf_status_string": ctypes.c_char_p}
+
+_lib: ctypes.CDLL | None = None
+
+
+def load() -> ctypes.CDLL:
+    """Open the kernel library, building nothing; raise if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH.name} is not built; run `python -m paper_2009_13062_b200.build` "
+            "(there is no CPU fallback for the merged operators)")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if status == NF_OK:
+        return
+    lib = load()
+    msg = f"{what}: {lib.nf_status_string(status).decode()}"
+    if status == NF_ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == NF_ERR_UNSUPPORTED:
+        raise UnsupportedOpError(msg)
+    raise ExecutionError(what, RuntimeError(msg))
+
+
+def call(name: str, *args) -> None:
+    """Invoke one C-ABI entry point and raise on a non-OK status."""
+    check(getattr(load(), name)(*args), name)
