@@ -51,6 +51,20 @@ extern "C" {
 #define NF_MODE_FAST 0
 #define NF_MODE_EXACT 1
 
+/* elementwise ops (nf_elementwise) */
+#define NF_EW_ADD 0
+#define NF_EW_MUL 1
+#define NF_EW_RELU 2
+#define NF_EW_TANH 3
+#define NF_EW_GELU 4
+
+/* pooling kinds (nf_pool2d) */
+#define NF_POOL_MAX 0
+#define NF_POOL_MEAN 1
+
+/* max rank handled by nf_copy_strided */
+#define NF_MAX_RANK 8
+
 /* weight layouts for nf_grouped_linear */
 #define NF_W_NK 0 /* (G, N, K): K-major, the kernel-native merged layout   */
 #define NF_W_KN 1 /* (G, K, N): the reference layout (rules.py:180-184)    */
@@ -74,6 +88,84 @@ const char* nf_status_string(int status);
 int nf_grouped_linear(const void* x, const void* w, const void* bias, const void* residual,
                       void* y, int64_t groups, int64_t rows, int64_t k, int64_t n, int dtype,
                       int w_layout, int act, int mode, void* stream);
+
+/*
+ * Merged Conv2d == reference `grouped_conv2d` (engine.py:155-191), and with
+ * groups=1 `conv2d` (engine.py:122-152). NCHW x (N, Cin, H, W), w
+ * (Cout, Cin/groups, k, k), y (N, Cout, Ho, Wo). Epilogue (FAST, for the
+ * BN-folded CNN plans): y = relu?((acc * scale[c]) + bias[c] + residual);
+ * scale/bias fp32 or NULL, residual like y or NULL. EXACT f32 follows the
+ * reference accumulation order (ci, kh, kw; rounded mul then add; bias after).
+ */
+int nf_grouped_conv2d(const void* x, const void* w, const float* bias, const float* scale,
+                      const void* residual, void* y, int64_t N, int64_t Cin, int64_t H,
+                      int64_t W, int64_t Cout, int kernel, int stride, int pad, int groups,
+                      int relu, int dtype, int mode, void* stream);
+
+/*
+ * Pointwise ops == reference `add`/`mul`/`relu`/`tanh` (engine.py:305-331)
+ * plus GELU (extension). Dense over `n` elements; pointers 16-byte aligned.
+ * add/mul are IEEE-rounded with no contraction: bit-exact vs numpy.
+ */
+int nf_elementwise(int op, const void* a, const void* b, void* y, int64_t n, int dtype,
+                   void* stream);
+
+/*
+ * Layout glue: y[i0..] = x[i0..] over an up-to-8-D index space with
+ * arbitrary element strides on both sides. Realises the merger's
+ * Transpose/Reshape junctions (merger.py:237-301) and Pack/Unpack
+ * (engine.py:380-420) when they cannot be zero-copy views.
+ */
+int nf_copy_strided(const void* x, void* y, int rank, const int64_t* dims,
+                    const int64_t* x_strides, const int64_t* y_strides, int elem_bytes,
+                    void* stream);
+
+/*
+ * Merged LayerNorm == reference `group_norm` (engine.py:263-284), and with
+ * groups=1 `layer_norm` (engine.py:246-260). y = GN(x [+ residual]).
+ * Row r = (r1, r2) at element offset r1*s1 + r2*s2 (r1 < R1, r2 < R2);
+ * channel (g, c) of a row at g*sg + c*sc (g < G, c < Cg). gamma/beta are fp32
+ * of length G*Cg, or (rows/rows_per_affine) blocks of G*Cg when
+ * rows_per_affine > 0 (per-instance affine on a model-major layout). The
+ * same geometry addresses y and residual. Covers the channel-packed layout
+ * (B, S, M*D) and the model-major layout (M, B, S, D) without glue.
+ */
+int nf_group_norm(const void* x, const void* residual, const float* gamma, const float* beta,
+                  void* y, int64_t R1, int64_t R2, int64_t s1, int64_t s2, int64_t G,
+                  int64_t Cg, int64_t sg, int64_t sc, int64_t rows_per_affine, float eps,
+                  int dtype, void* stream);
+
+/*
+ * Softmax along one axis == reference `softmax` (engine.py:313-319):
+ * element (o, l, i) at o*so + l*sl + i*si for o < outer, l < L, i < inner.
+ */
+int nf_softmax(const void* x, void* y, int64_t outer, int64_t L, int64_t inner, int64_t so,
+               int64_t sl, int64_t si, int dtype, void* stream);
+
+/*
+ * Merged attention (extension; the reference composes batch_matmul +
+ * softmax): qkv (Bt, S, 3*H*dh) fused projection rows [Q | K | V], out
+ * (Bt, S, H*dh) = softmax(Q K^T * scale) V per (sequence, head).
+ * bf16 FAST with dh == 64 and S <= 128 runs the tcgen05/TMEM kernel.
+ */
+int nf_attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
+                 float scale, int dtype, int mode, void* stream);
+
+/*
+ * Inference batch norm == reference `batch_norm_inference`
+ * (engine.py:287-302) on an NCHW tensor (N, C, inner); fp32 parameters.
+ * Same operation order as numpy: bit-exact for f32.
+ */
+int nf_batch_norm(const void* x, const float* gamma, const float* beta, const float* mean,
+                  const float* var, void* y, int64_t N, int64_t C, int64_t inner, float eps,
+                  int dtype, void* stream);
+
+/*
+ * 2-D pooling == reference `max_pool2d` / `mean_pool2d` (engine.py:334-365)
+ * on NCHW; extension: symmetric `pad` (-inf for max, zeros for mean).
+ */
+int nf_pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind, int kernel,
+              int stride, int pad, int dtype, void* stream);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,9 @@ NF_F32, NF_BF16 = 0, 1
 NF_ACT_NONE, NF_ACT_RELU, NF_ACT_GELU, NF_ACT_TANH = 0, 1, 2, 3
 NF_MODE_FAST, NF_MODE_EXACT = 0, 1
 NF_W_NK, NF_W_KN = 0, 1
+NF_EW_ADD, NF_EW_MUL, NF_EW_RELU, NF_EW_TANH, NF_EW_GELU = 0, 1, 2, 3, 4
+NF_POOL_MAX, NF_POOL_MEAN = 0, 1
+NF_MAX_RANK = 8
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -32,6 +35,14 @@ SIGNATURES: dict[str, list] = {
     "nf_abi_version": [],
     "nf_status_string": [_i],
     "nf_grouped_linear": [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _i, _i, _i, _p],
+    "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
+    "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
+    "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],
+    "nf_group_norm": [_p, _p, _p, _p, _p] + [_i64] * 9 + [_f, _i, _p],
+    "nf_softmax": [_p, _p] + [_i64] * 6 + [_i, _p],
+    "nf_attention": [_p, _p, _i64, _i64, _i64, _i64, _f, _i, _i, _p],
+    "nf_batch_norm": [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _f, _i, _p],
+    "nf_pool2d": [_p, _p, _i64, _i64, _i, _i, _i, _i, _i, _i, _i, _p],
 }
 
 _RESTYPES = {"nf_status_string": ctypes.c_char_p}

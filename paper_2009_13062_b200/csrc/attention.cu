@@ -1,0 +1,338 @@
+// Merged attention: softmax(Q K^T * scale) V per (instance*batch, head) over
+// a fused QKV activation (..., S, 3*H*dh). Batched over instances: the merged
+// graph packs instances on the leading axis, so M instances x B sequences x H
+// heads are just independent CTAs.
+//
+// The reference IR cannot express attention; its oracle is the
+// reference contraction order + `softmax` (engine.py:313-319), see
+// oracle/kernels.py::attention.
+//
+// tcgen05 path (bf16, dh == 64, S <= 128): one CTA per (sequence, head).
+//   TMA loads Q, K, V tiles (128 x 64, SWIZZLE_128B) straight out of the
+//   fused QKV rows; S = Q K^T accumulates in TMEM (128 x 128 fp32); each
+//   thread owns one query row, does the max/exp2/sum in registers and writes
+//   unnormalised P (bf16) to smem in the K-major SWIZZLE_128B layout; V is
+//   transposed in smem; O = P V^T accumulates in TMEM (128 x 64) and is
+//   scaled by 1/rowsum in the epilogue. Scores never touch HBM.
+// SIMT path (any S, dh <= 128, f32 or bf16): one warp per query row with an
+//   online softmax, for shapes / dtypes the tensor-core path does not take.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nf {
+
+bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
+                   int box_inner, int box_rows);
+
+namespace {
+
+constexpr int kAttnS = 128;   // max keys / queries per CTA
+constexpr int kAttnD = 64;    // head dim on the tensor-core path
+constexpr int kTileBytes = kAttnS * kAttnD * 2;  // 16 KB
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn_attn() {
+  static EncodeTiledFn fn = []() -> EncodeTiledFn {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// qkv viewed as 4-D (dh, 3H, S, Bt); box (64, 1, 128, 1) = one 128 x 128 B
+// head tile in the K-major SWIZZLE_128B layout.
+bool make_qkv_map(CUtensorMap* map, const void* qkv, int64_t Bt, int64_t S, int64_t H) {
+  EncodeTiledFn fn = encode_fn_attn();
+  if (!fn) return false;
+  const int64_t D = H * kAttnD;
+  cuuint64_t dims[4] = {cuuint64_t(kAttnD), cuuint64_t(3 * H), cuuint64_t(S), cuuint64_t(Bt)};
+  cuuint64_t strides[3] = {cuuint64_t(kAttnD * 2), cuuint64_t(3 * D * 2),
+                           cuuint64_t(S * 3 * D * 2)};
+  cuuint32_t box[4] = {kAttnD, 1, kAttnS, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(qkv), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Byte offset of (row r, k) in a K-major SWIZZLE_128B operand whose K extent
+// is split into 64-element (128 B) blocks of `rows` rows each.
+__device__ __forceinline__ uint32_t kmajor_off(int r, int k, int rows) {
+  const int blk = k >> 6;
+  const int within = (k & 63) * 2;
+  return uint32_t(blk * rows * 128 + r * 128 + ((((within >> 4) ^ (r & 7)) << 4) | (within & 15)));
+}
+
+__global__ void __launch_bounds__(128, 2)
+    k_attention_tc(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
+                   int S, int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTileBytes;
+  uint8_t* sV = sK + kTileBytes;
+  uint8_t* sVt = sV + kTileBytes;          // 64 rows (dh) x 128 keys, 2 k-blocks
+  uint8_t* sP = sVt + kTileBytes;          // 128 rows x 128 keys, 2 k-blocks (32 KB)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTileBytes);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_s = bars + 1;
+  uint64_t* bar_o = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int bt = blockIdx.x / H;
+  const int h = blockIdx.x % H;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&map_qkv);
+    mbar_init(bar_load, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_o, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_s = tmem;        // columns [0, 128): scores
+  const uint32_t tmem_o = tmem + 128;  // columns [128, 192): context
+
+  if (tid == 0) {
+    grid_dependency_wait();
+    mbar_arrive_expect_tx(bar_load, 3 * kTileBytes);
+    tma_load_4d(sQ, &map_qkv, bar_load, 0, h, 0, bt, kEvictFirst);
+    tma_load_4d(sK, &map_qkv, bar_load, 0, H + h, 0, bt, kEvictFirst);
+    tma_load_4d(sV, &map_qkv, bar_load, 0, 2 * H + h, 0, bt, kEvictFirst);
+  }
+  mbar_wait(bar_load, 0);
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 128);
+    const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK);
+#pragma unroll
+    for (int kk = 0; kk < kAttnD / 16; ++kk)
+      umma_f16_ss(tmem_s, make_sw128_kmajor_desc(qa + kk * 32),
+                  make_sw128_kmajor_desc(ka + kk * 32), idesc, kk != 0);
+    umma_commit(bar_s);
+  }
+
+  // Transpose V (keys x dh) into Vt (dh x keys, K-major over keys) while the
+  // score MMA runs. Thread t handles key row t: 8 chunks of 8 dh values.
+  {
+    const int key = tid;
+    const uint32_t vrow = smem_u32(sV) + key * 128;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      uint4 u;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                   : "r"(vrow + (((ch ^ (key & 7)) << 4))));
+      const uint16_t* e = reinterpret_cast<const uint16_t*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) st_shared_u16(smem_u32(sVt) + kmajor_off(ch * 8 + j, key, 64), e[j]);
+    }
+  }
+  fence_proxy_async_smem();
+
+  // Softmax over this thread's query row (TMEM lane = tid).
+  mbar_wait(bar_s, 0);
+  tc_fence_after();
+  float mx = -INFINITY;
+  uint32_t r[4][32];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    tmem_ld_32x32b_x32(tmem_s + (uint32_t(warp * 32) << 16) + uint32_t(c * 32), r[c]);
+  tmem_ld_wait();
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (c * 32 + j < S) mx = fmaxf(mx, __uint_as_float(r[c][j]));
+  float sum = 0.f;
+  const uint32_t prow = smem_u32(sP);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float p[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float v = (c * 32 + j < S) ? exp2f((__uint_as_float(r[c][j]) - mx) * scale_log2) : 0.f;
+      // Round to the bf16 operand value before summing so the normaliser
+      // matches the probabilities the PV MMA actually consumes.
+      p[j] = __bfloat162float(__float2bfloat16_rn(v));
+      sum += p[j];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      st_shared_v4(prow + kmajor_off(tid, c * 32 + q * 8, 128), pack_bf16x2(p[8 * q], p[8 * q + 1]),
+                   pack_bf16x2(p[8 * q + 2], p[8 * q + 3]), pack_bf16x2(p[8 * q + 4], p[8 * q + 5]),
+                   pack_bf16x2(p[8 * q + 6], p[8 * q + 7]));
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64);
+    const uint32_t pa = smem_u32(sP), va = smem_u32(sVt);
+#pragma unroll
+    for (int kk = 0; kk < kAttnS / 16; ++kk) {
+      const int blk = kk >> 2, sub = kk & 3;
+      umma_f16_ss(tmem_o, make_sw128_kmajor_desc(pa + blk * 128 * 128 + sub * 32),
+                  make_sw128_kmajor_desc(va + blk * 64 * 128 + sub * 32), idesc, kk != 0);
+    }
+    umma_commit(bar_o);
+  }
+  mbar_wait(bar_o, 0);
+  tc_fence_after();
+  grid_dependents_launch();
+  {
+    uint32_t o[2][32];
+    tmem_ld_32x32b_x32(tmem_o + (uint32_t(warp * 32) << 16), o[0]);
+    tmem_ld_32x32b_x32(tmem_o + (uint32_t(warp * 32) << 16) + 32, o[1]);
+    tmem_ld_wait();
+    if (tid < S) {
+      const float inv = 1.0f / sum;
+      const int64_t D = int64_t(H) * kAttnD;
+      __nv_bfloat16* dst = out + (int64_t(bt) * S + tid) * D + int64_t(h) * kAttnD;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16x2(__uint_as_float(o[c][8 * q]) * inv, __uint_as_float(o[c][8 * q + 1]) * inv);
+          u.y = pack_bf16x2(__uint_as_float(o[c][8 * q + 2]) * inv, __uint_as_float(o[c][8 * q + 3]) * inv);
+          u.z = pack_bf16x2(__uint_as_float(o[c][8 * q + 4]) * inv, __uint_as_float(o[c][8 * q + 5]) * inv);
+          u.w = pack_bf16x2(__uint_as_float(o[c][8 * q + 6]) * inv, __uint_as_float(o[c][8 * q + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + q * 8) = u;
+        }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+constexpr size_t kAttnSmem = 1024 + 6 * kTileBytes + 64;
+
+// ---------------------------------------------------------------------------
+// SIMT fallback: one warp per (sequence, head, query), online softmax.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_attention_simt(const T* __restrict__ qkv, T* __restrict__ out, int64_t Bt,
+                                 int S, int H, int dh, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t D = int64_t(H) * dh;
+  const int64_t units = Bt * H * S;
+  for (int64_t u = w; u < units; u += nw) {
+    const int i = int(u % S);
+    const int h = int((u / S) % H);
+    const int64_t b = u / (int64_t(S) * H);
+    const T* base = qkv + b * S * 3 * D;
+    const T* q = base + int64_t(i) * 3 * D + int64_t(h) * dh;
+    float qv[4], acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int d = lane + 32 * e;
+      qv[e] = d < dh ? to_f32(q[d]) : 0.f;
+      acc[e] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < S; ++j) {
+      const T* k = base + int64_t(j) * 3 * D + D + int64_t(h) * dh;
+      const T* v = k + D;
+      float dot = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int d = lane + 32 * e;
+        if (d < dh) dot += qv[e] * to_f32(k[d]);
+      }
+      dot = warp_sum(dot) * scale;
+      const float mn = fmaxf(m, dot);
+      const float corr = expf(m - mn);
+      const float p = expf(dot - mn);
+      l = l * corr + p;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int d = lane + 32 * e;
+        acc[e] = acc[e] * corr + (d < dh ? p * to_f32(v[d]) : 0.f);
+      }
+      m = mn;
+    }
+    T* o = out + (b * S + i) * D + int64_t(h) * dh;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int d = lane + 32 * e;
+      if (d < dh) o[d] = from_f32<T>(acc[e] / l);
+    }
+  }
+}
+
+}  // namespace
+
+int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
+              float scale, int dtype, int mode, cudaStream_t stream) {
+  if (Bt < 1 || S < 1 || H < 1 || dh < 1) return NF_ERR_SHAPE;
+  if (dh > 128) return NF_ERR_UNSUPPORTED;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(out);
+  if (dtype == NF_BF16 && mode == NF_MODE_FAST && dh == kAttnD && S <= kAttnS && (al & 15) == 0 &&
+      Bt * H <= (int64_t(1) << 31) - 1) {
+    CUtensorMap map;
+    if (!make_qkv_map(&map, qkv, Bt, S, H)) return NF_ERR_LAUNCH;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kAttnSmem));
+      attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(Bt * H));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = kAttnSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const float scale_log2 = scale * 1.4426950408889634f;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_attention_tc, map,
+                                       static_cast<__nv_bfloat16*>(out), int(S), int(H),
+                                       scale_log2);
+    return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+  }
+  const int64_t warps = Bt * H * S;
+  int64_t blocks = (warps * 32 + 255) / 256;
+  if (blocks > int64_t(kNumSMs) * 32) blocks = int64_t(kNumSMs) * 32;
+  if (dtype == NF_F32)
+    k_attention_simt<float><<<unsigned(blocks), 256, 0, stream>>>(
+        static_cast<const float*>(qkv), static_cast<float*>(out), Bt, int(S), int(H), int(dh),
+        scale);
+  else if (dtype == NF_BF16)
+    k_attention_simt<__nv_bfloat16><<<unsigned(blocks), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(out), Bt, int(S),
+        int(H), int(dh), scale);
+  else
+    return NF_ERR_UNSUPPORTED;
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+}  // namespace nf

@@ -34,4 +34,68 @@ int nf_grouped_linear(const void* x, const void* w, const void* bias, const void
                                  mode == NF_MODE_EXACT, s);
 }
 
+int nf_grouped_conv2d(const void* x, const void* w, const float* bias, const float* scale,
+                      const void* residual, void* y, int64_t N, int64_t Cin, int64_t H,
+                      int64_t W, int64_t Cout, int kernel, int stride, int pad, int groups,
+                      int relu, int dtype, int mode, void* stream) {
+  if (!x || !w || !y || N < 1 || Cin < 1 || H < 1 || W < 1 || Cout < 1) return NF_ERR_SHAPE;
+  if (mode == NF_MODE_EXACT && (scale || residual || relu)) return NF_ERR_UNSUPPORTED;
+  return nf::conv2d_simt(x, w, bias, scale, residual, y, int(N), int(Cin), int(H), int(W),
+                         int(Cout), kernel, stride, pad, groups, relu, dtype,
+                         mode == NF_MODE_EXACT, static_cast<cudaStream_t>(stream));
+}
+
+int nf_elementwise(int op, const void* a, const void* b, void* y, int64_t n, int dtype,
+                   void* stream) {
+  if (!a || !y || n < 0) return NF_ERR_SHAPE;
+  if (n == 0) return NF_OK;
+  return nf::elementwise(op, a, b, y, n, dtype, static_cast<cudaStream_t>(stream));
+}
+
+int nf_copy_strided(const void* x, void* y, int rank, const int64_t* dims,
+                    const int64_t* x_strides, const int64_t* y_strides, int elem_bytes,
+                    void* stream) {
+  if (!x || !y || !dims || !x_strides || !y_strides) return NF_ERR_SHAPE;
+  return nf::copy_strided(x, y, rank, dims, x_strides, y_strides, elem_bytes,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int nf_group_norm(const void* x, const void* residual, const float* gamma, const float* beta,
+                  void* y, int64_t R1, int64_t R2, int64_t s1, int64_t s2, int64_t G,
+                  int64_t Cg, int64_t sg, int64_t sc, int64_t rows_per_affine, float eps,
+                  int dtype, void* stream) {
+  if (!x || !y || !gamma || !beta) return NF_ERR_SHAPE;
+  nf::NormGeomC g{R1, R2, s1, s2, G, Cg, sg, sc, rows_per_affine, eps};
+  return nf::group_norm(x, residual, gamma, beta, y, g, dtype, static_cast<cudaStream_t>(stream));
+}
+
+int nf_softmax(const void* x, void* y, int64_t outer, int64_t L, int64_t inner, int64_t so,
+               int64_t sl, int64_t si, int dtype, void* stream) {
+  if (!x || !y) return NF_ERR_SHAPE;
+  return nf::softmax(x, y, outer, L, inner, so, sl, si, dtype, static_cast<cudaStream_t>(stream));
+}
+
+int nf_attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
+                 float scale, int dtype, int mode, void* stream) {
+  if (!qkv || !out) return NF_ERR_SHAPE;
+  return nf::attention(qkv, out, Bt, S, H, dh, scale, dtype, mode,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int nf_batch_norm(const void* x, const float* gamma, const float* beta, const float* mean,
+                  const float* var, void* y, int64_t N, int64_t C, int64_t inner, float eps,
+                  int dtype, void* stream) {
+  if (!x || !y || !gamma || !beta || !mean || !var) return NF_ERR_SHAPE;
+  return nf::batch_norm(x, gamma, beta, mean, var, y, N, C, inner, eps, dtype,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int nf_pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind, int kernel,
+              int stride, int pad, int dtype, void* stream) {
+  if (!x || !y || N < 1 || C < 1 || H < 1 || W < 1) return NF_ERR_SHAPE;
+  if (kind != NF_POOL_MAX && kind != NF_POOL_MEAN) return NF_ERR_UNSUPPORTED;
+  return nf::pool2d(x, y, N, C, H, W, kind, kernel, stride, pad, dtype,
+                    static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

@@ -17,4 +17,34 @@ int grouped_linear_simt(const void* x, const void* w, const float* bias, const v
                         void* y, int64_t G, int64_t T, int64_t K, int64_t N, int dtype,
                         int w_layout, int act, int exact, cudaStream_t stream);
 
+// pointwise.cu
+struct NormGeomC {
+  int64_t R1, R2, s1, s2, G, Cg, sg, sc, rows_per_affine;
+  float eps;
+};
+int elementwise(int op, const void* a, const void* b, void* y, int64_t n, int dtype,
+                cudaStream_t s);
+int copy_strided(const void* src, void* dst, int rank, const int64_t* dims,
+                 const int64_t* src_strides, const int64_t* dst_strides, int elem_bytes,
+                 cudaStream_t s);
+int group_norm(const void* x, const void* residual, const float* gamma, const float* beta,
+               void* y, const NormGeomC& g, int dtype, cudaStream_t s);
+int softmax(const void* x, void* y, int64_t outer, int64_t L, int64_t inner, int64_t so,
+            int64_t sl, int64_t si, int dtype, cudaStream_t s);
+int batch_norm(const void* x, const float* gamma, const float* beta, const float* mean,
+               const float* var, void* y, int64_t N, int64_t C, int64_t inner, float eps,
+               int dtype, cudaStream_t s);
+int pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind, int k,
+           int stride, int pad, int dtype, cudaStream_t s);
+
+// conv_simt.cu
+int conv2d_simt(const void* x, const void* w, const float* bias, const float* scale,
+                const void* residual, void* y, int N, int Cin, int H, int W, int Cout, int k,
+                int stride, int pad, int groups, int relu, int dtype, int exact,
+                cudaStream_t s);
+
+// attention.cu
+int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
+              float scale, int dtype, int mode, cudaStream_t stream);
+
 }  // namespace nf

@@ -1,0 +1,442 @@
+// Memory-bound merged ops: elementwise, strided copy (layout glue), group /
+// layer norm, softmax, inference batch norm and 2-D pooling.
+//
+// Each kernel replaces one reference kernel of pkg/src/modelmerge/engine.py
+// (cited below). All are HBM-bound: 128-bit vector loads where the layout
+// allows, grids sized in multiples of the SM count, fp32 arithmetic.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nf {
+
+template <typename T> struct Vec8;  // 16 bytes of T
+template <> struct Vec8<__nv_bfloat16> { static constexpr int N = 8; };
+template <> struct Vec8<float> { static constexpr int N = 4; };
+
+static inline int grid_for(int64_t work, int threads, int per_sm = 8) {
+  int64_t blocks = (work + threads - 1) / threads;
+  int64_t cap = int64_t(kNumSMs) * per_sm * 4;
+  return int(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise (engine.py:305-331 relu/tanh/add/mul; GELU extension).
+// Binary ops use IEEE add/mul with no contraction: bit-exact vs numpy.
+// ---------------------------------------------------------------------------
+template <typename T, int OP>
+__global__ void k_elementwise(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
+                              int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  constexpr int V = Vec8<T>::N;
+  const int64_t nv = n / V;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 ua = reinterpret_cast<const uint4*>(a)[i];
+    uint4 ub = b ? reinterpret_cast<const uint4*>(b)[i] : ua;
+    const T* pa = reinterpret_cast<const T*>(&ua);
+    const T* pb = reinterpret_cast<const T*>(&ub);
+    uint4 uo;
+    T* po = reinterpret_cast<T*>(&uo);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      float x = to_f32(pa[e]);
+      float r;
+      if constexpr (OP == NF_EW_ADD) r = __fadd_rn(x, to_f32(pb[e]));
+      else if constexpr (OP == NF_EW_MUL) r = __fmul_rn(x, to_f32(pb[e]));
+      else if constexpr (OP == NF_EW_RELU) r = fmaxf(x, 0.0f);
+      else if constexpr (OP == NF_EW_TANH) r = tanhf(x);
+      else r = gelu_erf(x);
+      po[e] = from_f32<T>(r);
+    }
+    reinterpret_cast<uint4*>(y)[i] = uo;
+  }
+  for (int64_t i = nv * V + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float x = to_f32(a[i]);
+    float r;
+    if constexpr (OP == NF_EW_ADD) r = __fadd_rn(x, to_f32(b[i]));
+    else if constexpr (OP == NF_EW_MUL) r = __fmul_rn(x, to_f32(b[i]));
+    else if constexpr (OP == NF_EW_RELU) r = fmaxf(x, 0.0f);
+    else if constexpr (OP == NF_EW_TANH) r = tanhf(x);
+    else r = gelu_erf(x);
+    y[i] = from_f32<T>(r);
+  }
+}
+
+template <typename T>
+static int launch_ew(int op, const void* a, const void* b, void* y, int64_t n, cudaStream_t s) {
+  const T* pa = static_cast<const T*>(a);
+  const T* pb = static_cast<const T*>(b);
+  T* py = static_cast<T*>(y);
+  const int grid = grid_for(n / Vec8<T>::N + 1, 256);
+  switch (op) {
+    case NF_EW_ADD: k_elementwise<T, NF_EW_ADD><<<grid, 256, 0, s>>>(pa, pb, py, n); break;
+    case NF_EW_MUL: k_elementwise<T, NF_EW_MUL><<<grid, 256, 0, s>>>(pa, pb, py, n); break;
+    case NF_EW_RELU: k_elementwise<T, NF_EW_RELU><<<grid, 256, 0, s>>>(pa, nullptr, py, n); break;
+    case NF_EW_TANH: k_elementwise<T, NF_EW_TANH><<<grid, 256, 0, s>>>(pa, nullptr, py, n); break;
+    case NF_EW_GELU: k_elementwise<T, NF_EW_GELU><<<grid, 256, 0, s>>>(pa, nullptr, py, n); break;
+    default: return NF_ERR_UNSUPPORTED;
+  }
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+int elementwise(int op, const void* a, const void* b, void* y, int64_t n, int dtype,
+                cudaStream_t s) {
+  if ((op == NF_EW_ADD || op == NF_EW_MUL) && !b) return NF_ERR_SHAPE;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                       reinterpret_cast<uintptr_t>(y);
+  if (al & 15) return NF_ERR_UNSUPPORTED;  // caller allocates 16-byte aligned buffers
+  if (dtype == NF_F32) return launch_ew<float>(op, a, b, y, n, s);
+  if (dtype == NF_BF16) return launch_ew<__nv_bfloat16>(op, a, b, y, n, s);
+  return NF_ERR_UNSUPPORTED;
+}
+
+// ---------------------------------------------------------------------------
+// Strided copy (the merger's Transpose/Reshape glue, merger.py:237-301, and
+// Pack/Unpack, engine.py:380-420, when they cannot be views).
+// ---------------------------------------------------------------------------
+struct CopyGeom {
+  int rank;
+  int64_t dims[NF_MAX_RANK];
+  int64_t src_strides[NF_MAX_RANK];
+  int64_t dst_strides[NF_MAX_RANK];
+};
+
+template <int BYTES>
+__global__ void k_copy_strided(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                               CopyGeom g, int64_t n) {
+  using W = typename std::conditional<BYTES == 2, uint16_t,
+            typename std::conditional<BYTES == 4, uint32_t, uint64_t>::type>::type;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    int64_t rem = i, so = 0, dof = 0;
+#pragma unroll
+    for (int d = NF_MAX_RANK - 1; d >= 0; --d) {
+      if (d < g.rank) {
+        const int64_t idx = rem % g.dims[d];
+        rem /= g.dims[d];
+        so += idx * g.src_strides[d];
+        dof += idx * g.dst_strides[d];
+      }
+    }
+    reinterpret_cast<W*>(dst)[dof] = reinterpret_cast<const W*>(src)[so];
+  }
+}
+
+int copy_strided(const void* src, void* dst, int rank, const int64_t* dims,
+                 const int64_t* src_strides, const int64_t* dst_strides, int elem_bytes,
+                 cudaStream_t s) {
+  if (rank < 1 || rank > NF_MAX_RANK) return NF_ERR_UNSUPPORTED;
+  CopyGeom g{};
+  g.rank = rank;
+  int64_t n = 1;
+  for (int d = 0; d < rank; ++d) {
+    g.dims[d] = dims[d];
+    g.src_strides[d] = src_strides[d];
+    g.dst_strides[d] = dst_strides[d];
+    n *= dims[d];
+  }
+  if (n == 0) return NF_OK;
+  const int grid = grid_for(n, 256);
+  auto* ps = static_cast<const uint8_t*>(src);
+  auto* pd = static_cast<uint8_t*>(dst);
+  switch (elem_bytes) {
+    case 2: k_copy_strided<2><<<grid, 256, 0, s>>>(ps, pd, g, n); break;
+    case 4: k_copy_strided<4><<<grid, 256, 0, s>>>(ps, pd, g, n); break;
+    case 8: k_copy_strided<8><<<grid, 256, 0, s>>>(ps, pd, g, n); break;
+    default: return NF_ERR_UNSUPPORTED;
+  }
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+// ---------------------------------------------------------------------------
+// Group norm == merged LayerNorm (engine.py:246-284). One warp per
+// (row, group): mean, then population variance of (x - mean) over the
+// group's channels, y = gamma * (x - mean) / sqrt(var + eps) + beta, with an
+// optional fused residual (y = GN(x + r)). Geometry: row r = (r1, r2) at
+// offset r1*s1 + r2*s2; channel (g, c) at g*sg + c*sc; gamma index g*Cg + c
+// (+ (r1 * R2 + r2) / rows_per_affine * G*Cg for per-instance affine blocks).
+// ---------------------------------------------------------------------------
+struct NormGeom {
+  int64_t R1, R2, s1, s2;  // rows
+  int64_t G, Cg, sg, sc;   // groups x channels
+  int64_t rows_per_affine; // rows sharing one gamma/beta block (<=0: all)
+  float eps;
+};
+
+constexpr int kNormCache = 32;  // fp32 values cached per lane
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) k_group_norm(const T* __restrict__ x,
+                                                    const T* __restrict__ res,
+                                                    const float* __restrict__ gamma,
+                                                    const float* __restrict__ beta,
+                                                    T* __restrict__ y, NormGeom g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_id = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t rows = g.R1 * g.R2;
+  const int64_t units = rows * g.G;
+  for (int64_t u = warp_id; u < units; u += nwarps) {
+    const int64_t row = u / g.G, grp = u % g.G;
+    const int64_t base = (row / g.R2) * g.s1 + (row % g.R2) * g.s2 + grp * g.sg;
+    const int64_t aff = (g.rows_per_affine > 0 ? (row / g.rows_per_affine) : 0) * g.G * g.Cg +
+                        grp * g.Cg;
+    const int Cg = int(g.Cg);
+    float v[kNormCache];
+    float sum = 0.f;
+    if (VEC) {
+      // sc == 1, Cg % (8 * 32) handled by the cached vector path: each lane
+      // owns 16-byte chunks lane, lane+32, ...
+      constexpr int V = Vec8<T>::N;
+      const int nchunks = Cg / V;
+#pragma unroll
+      for (int q = 0; q < kNormCache / V; ++q) {
+        const int ch = lane + 32 * q;
+        if (ch < nchunks) {
+          uint4 ux = *reinterpret_cast<const uint4*>(x + base + int64_t(ch) * V);
+          const T* px = reinterpret_cast<const T*>(&ux);
+          uint4 ur;
+          const T* pr = reinterpret_cast<const T*>(&ur);
+          if (res) ur = *reinterpret_cast<const uint4*>(res + base + int64_t(ch) * V);
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            float t = to_f32(px[e]);
+            if (res) t = __fadd_rn(t, to_f32(pr[e]));
+            v[q * V + e] = t;
+            sum += t;
+          }
+        }
+      }
+      sum = warp_sum(sum);
+      const float mean = sum / float(Cg);
+      float sq = 0.f;
+#pragma unroll
+      for (int q = 0; q < kNormCache / V; ++q) {
+        if (lane + 32 * q < nchunks) {
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const float d = v[q * V + e] - mean;
+            sq += d * d;
+          }
+        }
+      }
+      sq = warp_sum(sq);
+      const float rstd = 1.0f / sqrtf(sq / float(Cg) + g.eps);
+#pragma unroll
+      for (int q = 0; q < kNormCache / V; ++q) {
+        const int ch = lane + 32 * q;
+        if (ch < nchunks) {
+          uint4 uo;
+          T* po = reinterpret_cast<T*>(&uo);
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            const int c = ch * V + e;
+            po[e] = from_f32<T>(gamma[aff + c] * ((v[q * V + e] - mean) * rstd) + beta[aff + c]);
+          }
+          *reinterpret_cast<uint4*>(y + base + int64_t(ch) * V) = uo;
+        }
+      }
+    } else {
+      // Generic strided path: three passes over memory.
+      for (int c = lane; c < Cg; c += 32) {
+        float t = to_f32(x[base + c * g.sc]);
+        if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
+        sum += t;
+      }
+      const float mean = warp_sum(sum) / float(Cg);
+      float sq = 0.f;
+      for (int c = lane; c < Cg; c += 32) {
+        float t = to_f32(x[base + c * g.sc]);
+        if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
+        const float d = t - mean;
+        sq += d * d;
+      }
+      const float rstd = 1.0f / sqrtf(warp_sum(sq) / float(Cg) + g.eps);
+      for (int c = lane; c < Cg; c += 32) {
+        float t = to_f32(x[base + c * g.sc]);
+        if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
+        y[base + c * g.sc] = from_f32<T>(gamma[aff + c] * ((t - mean) * rstd) + beta[aff + c]);
+      }
+    }
+  }
+}
+
+int group_norm(const void* x, const void* residual, const float* gamma, const float* beta,
+               void* y, const NormGeomC& gc, int dtype, cudaStream_t s) {
+  NormGeom g{gc.R1, gc.R2, gc.s1, gc.s2, gc.G, gc.Cg, gc.sg, gc.sc, gc.rows_per_affine, gc.eps};
+  if (g.R1 < 1 || g.R2 < 1 || g.G < 1 || g.Cg < 1) return NF_ERR_SHAPE;
+  const int64_t units = g.R1 * g.R2 * g.G;
+  const int grid = grid_for(units * 32, 256);
+  const uintptr_t al = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(residual) |
+                       reinterpret_cast<uintptr_t>(y);
+  if (dtype == NF_BF16) {
+    const bool vec = g.sc == 1 && g.Cg % 8 == 0 && g.Cg <= 8 * 32 * (kNormCache / 8) &&
+                     (al & 15) == 0 && g.s1 % 8 == 0 && g.s2 % 8 == 0 && g.sg % 8 == 0;
+    auto* px = static_cast<const __nv_bfloat16*>(x);
+    auto* pr = static_cast<const __nv_bfloat16*>(residual);
+    auto* py = static_cast<__nv_bfloat16*>(y);
+    if (vec) k_group_norm<__nv_bfloat16, true><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
+    else k_group_norm<__nv_bfloat16, false><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
+  } else if (dtype == NF_F32) {
+    const bool vec = g.sc == 1 && g.Cg % 4 == 0 && g.Cg <= 4 * 32 * (kNormCache / 4) &&
+                     (al & 15) == 0 && g.s1 % 4 == 0 && g.s2 % 4 == 0 && g.sg % 4 == 0;
+    auto* px = static_cast<const float*>(x);
+    auto* pr = static_cast<const float*>(residual);
+    auto* py = static_cast<float*>(y);
+    if (vec) k_group_norm<float, true><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
+    else k_group_norm<float, false><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
+  } else {
+    return NF_ERR_UNSUPPORTED;
+  }
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+// ---------------------------------------------------------------------------
+// Softmax along one axis (engine.py:313-319): (outer, L, inner) geometry with
+// element (o, l, i) at o*so + l*sl + i*si. Contiguous axis (sl == 1): one
+// warp per row; otherwise one thread per (o, i) column (coalesced over i).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_softmax_rows(const T* __restrict__ x, T* __restrict__ y, int64_t rows,
+                               int64_t L, int64_t so, int64_t inner, int64_t si) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w; r < rows; r += nw) {
+    const int64_t base = (r / inner) * so + (r % inner) * si;
+    float m = -INFINITY;
+    for (int64_t l = lane; l < L; l += 32) m = fmaxf(m, to_f32(x[base + l]));
+    m = warp_max(m);
+    float sum = 0.f;
+    for (int64_t l = lane; l < L; l += 32) sum += expf(to_f32(x[base + l]) - m);
+    sum = warp_sum(sum);
+    for (int64_t l = lane; l < L; l += 32) y[base + l] = from_f32<T>(expf(to_f32(x[base + l]) - m) / sum);
+  }
+}
+
+template <typename T>
+__global__ void k_softmax_cols(const T* __restrict__ x, T* __restrict__ y, int64_t outer,
+                               int64_t L, int64_t inner, int64_t so, int64_t sl, int64_t si) {
+  const int64_t n = outer * inner;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t base = (t / inner) * so + (t % inner) * si;
+    float m = -INFINITY;
+    for (int64_t l = 0; l < L; ++l) m = fmaxf(m, to_f32(x[base + l * sl]));
+    float sum = 0.f;
+    for (int64_t l = 0; l < L; ++l) sum += expf(to_f32(x[base + l * sl]) - m);
+    for (int64_t l = 0; l < L; ++l)
+      y[base + l * sl] = from_f32<T>(expf(to_f32(x[base + l * sl]) - m) / sum);
+  }
+}
+
+int softmax(const void* x, void* y, int64_t outer, int64_t L, int64_t inner, int64_t so,
+            int64_t sl, int64_t si, int dtype, cudaStream_t s) {
+  if (outer < 1 || L < 1 || inner < 1) return NF_ERR_SHAPE;
+#define NF_SM(T)                                                                              \
+  do {                                                                                        \
+    auto* px = static_cast<const T*>(x);                                                      \
+    auto* py = static_cast<T*>(y);                                                            \
+    if (sl == 1)                                                                              \
+      k_softmax_rows<T><<<grid_for(outer * inner * 32, 256), 256, 0, s>>>(px, py, outer * inner, \
+                                                                          L, so, inner, si);  \
+    else                                                                                      \
+      k_softmax_cols<T><<<grid_for(outer * inner, 256), 256, 0, s>>>(px, py, outer, L, inner, \
+                                                                     so, sl, si);             \
+  } while (0)
+  if (dtype == NF_F32) NF_SM(float);
+  else if (dtype == NF_BF16) NF_SM(__nv_bfloat16);
+  else return NF_ERR_UNSUPPORTED;
+#undef NF_SM
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+// ---------------------------------------------------------------------------
+// Inference batch norm (engine.py:287-302), NCHW: per-channel
+// gamma * ((x - mean) / sqrt(var + eps)) + beta, same op order as numpy.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_batch_norm(const T* __restrict__ x, const float* __restrict__ gamma,
+                             const float* __restrict__ beta, const float* __restrict__ mean,
+                             const float* __restrict__ var, T* __restrict__ y, int64_t n,
+                             int64_t C, int64_t inner, float eps) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = (i / inner) % C;
+    const float den = __fsqrt_rn(__fadd_rn(var[c], eps));
+    const float d = __fdiv_rn(__fsub_rn(to_f32(x[i]), mean[c]), den);
+    y[i] = from_f32<T>(__fadd_rn(__fmul_rn(gamma[c], d), beta[c]));
+  }
+}
+
+int batch_norm(const void* x, const float* gamma, const float* beta, const float* mean,
+               const float* var, void* y, int64_t N, int64_t C, int64_t inner, float eps,
+               int dtype, cudaStream_t s) {
+  const int64_t n = N * C * inner;
+  if (n < 1) return NF_ERR_SHAPE;
+  const int grid = grid_for(n, 256);
+  if (dtype == NF_F32)
+    k_batch_norm<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), gamma, beta, mean, var,
+                                            static_cast<float*>(y), n, C, inner, eps);
+  else if (dtype == NF_BF16)
+    k_batch_norm<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), gamma,
+                                                    beta, mean, var,
+                                                    static_cast<__nv_bfloat16*>(y), n, C, inner,
+                                                    eps);
+  else
+    return NF_ERR_UNSUPPORTED;
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+// ---------------------------------------------------------------------------
+// 2-D pooling, NCHW (engine.py:334-365): running max / row-major window sum
+// then divide by k^2. Extension: symmetric padding (-inf for max, zeros
+// counted in the k^2 divisor for mean, torch count_include_pad semantics).
+// ---------------------------------------------------------------------------
+template <typename T, bool MAXP>
+__global__ void k_pool2d(const T* __restrict__ x, T* __restrict__ y, int64_t NC, int H, int W,
+                         int Ho, int Wo, int k, int stride, int pad) {
+  const int64_t n = NC * Ho * Wo;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int wo = int(i % Wo);
+    const int ho = int((i / Wo) % Ho);
+    const int64_t nc = i / (int64_t(Ho) * Wo);
+    const T* xp = x + nc * H * W;
+    float acc = MAXP ? -INFINITY : 0.0f;
+    for (int r = 0; r < k; ++r) {
+      const int h = ho * stride - pad + r;
+      for (int c = 0; c < k; ++c) {
+        const int w = wo * stride - pad + c;
+        const bool in = h >= 0 && h < H && w >= 0 && w < W;
+        const float v = in ? to_f32(xp[h * W + w]) : (MAXP ? -INFINITY : 0.0f);
+        acc = MAXP ? fmaxf(acc, v) : __fadd_rn(acc, v);
+      }
+    }
+    y[i] = from_f32<T>(MAXP ? acc : __fdiv_rn(acc, float(k * k)));
+  }
+}
+
+int pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind, int k,
+           int stride, int pad, int dtype, cudaStream_t s) {
+  if (k < 1 || stride < 1 || pad < 0 || 2 * pad > k) return NF_ERR_SHAPE;
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  if (Ho < 1 || Wo < 1) return NF_ERR_SHAPE;
+  const int64_t n = N * C * Ho * Wo;
+  const int grid = grid_for(n, 256);
+#define NF_POOL(T)                                                                          \
+  do {                                                                                      \
+    auto* px = static_cast<const T*>(x);                                                    \
+    auto* py = static_cast<T*>(y);                                                          \
+    if (kind == NF_POOL_MAX)                                                                \
+      k_pool2d<T, true><<<grid, 256, 0, s>>>(px, py, N * C, H, W, Ho, Wo, k, stride, pad);  \
+    else                                                                                    \
+      k_pool2d<T, false><<<grid, 256, 0, s>>>(px, py, N * C, H, W, Ho, Wo, k, stride, pad); \
+  } while (0)
+  if (dtype == NF_F32) NF_POOL(float);
+  else if (dtype == NF_BF16) NF_POOL(__nv_bfloat16);
+  else return NF_ERR_UNSUPPORTED;
+#undef NF_POOL
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+}  // namespace nf

@@ -1,0 +1,679 @@
+"""GPU executor for (merged) graphs — the drop-in for the reference's
+``execute`` (pkg/src/modelmerge/engine.py:516-573) and its ``_run_node``
+dispatch seam (engine.py:456-510).
+
+A graph is compiled once into a :class:`Plan`: a list of launch closures
+over preallocated device buffers, each one C-ABI call into the sm_100a
+library, so a forward is replayable as a single CUDA graph (no host work per
+node). Compilation does three B200-specific things the reference cannot:
+
+* **kernel-native weights**: merged Linear weights are transposed once to
+  K-major (G, N, K) bf16 for the tcgen05 GEMM; biases / norm affines become
+  fp32; everything lives in HBM for the life of the plan;
+* **zero-copy glue**: the merger's Pack / Transpose / Reshape / Unpack
+  junctions (merger.py:237-301, 418-513) become tensor views. A reshape that
+  merges a model axis into the channel axis is kept *unmaterialised* (a
+  "split" value: logical (..., M*C), physical (M, ..., C) model-major) and
+  the grouped norm / pointwise kernels consume it directly, so the BERT
+  plan's per-LayerNorm transposes cost nothing;
+* **epilogue fusion**: an activation whose only consumer is a Linear's output
+  is folded into the GEMM epilogue.
+
+Arithmetic ``mode``: "fast" (tensor cores, FMA) or "exact" (reference
+accumulation order, f32).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable
+
+import torch
+
+from . import _lib
+from . import kernels as K
+from .errors import ExecutionError, ShapeError, UnsupportedOpError
+from .ir import (
+    Graph,
+    MergeDim,
+    OpKind,
+    OpNode,
+    TensorSpec,
+    channel_axis,
+    parse_ref,
+    topological_order,
+)
+from .tensors import TORCH_DTYPES, TensorValue, WeightStore
+
+_BOUNDARY = (OpKind.PACK, OpKind.UNPACK)
+_ACT_OF = {OpKind.RELU: _lib.NF_ACT_RELU, OpKind.GELU: _lib.NF_ACT_GELU,
+           OpKind.TANH: _lib.NF_ACT_TANH}
+_EW_OF = {OpKind.ADD: _lib.NF_EW_ADD, OpKind.MUL: _lib.NF_EW_MUL, OpKind.RELU: _lib.NF_EW_RELU,
+          OpKind.TANH: _lib.NF_EW_TANH, OpKind.GELU: _lib.NF_EW_GELU}
+_MODES = {"fast": _lib.NF_MODE_FAST, "exact": _lib.NF_MODE_EXACT}
+
+
+@dataclass
+class ExecTrace:
+    """What one execute() did (reference engine.py:428-443), plus the number
+    of sm_100a kernel launches the plan issued."""
+
+    node_outputs: dict[str, TensorValue] = field(default_factory=dict)
+    node_times_ns: dict[str, int] = field(default_factory=dict)
+    op_invocations: int = 0
+    dispatch_count: int = 0
+    kernel_launches: int = 0
+    total_ns: int = 0
+
+
+@dataclass
+class DVal:
+    """A device value. ``t`` is a (possibly strided) view; when ``split`` is
+    set, logical axis ``split`` is the merge of ``t``'s axes split, split+1
+    (model-major storage of a channel-packed tensor, never materialised)."""
+
+    t: torch.Tensor
+    dims: tuple[int, ...]
+    split: int | None = None
+
+    @property
+    def dtype(self):
+        return self.t.dtype
+
+
+def _dense_block(t: torch.Tensor) -> bool:
+    """True when ``t`` is a permutation of one contiguous storage block."""
+    if t.numel() == 0:
+        return False
+    pairs = sorted((s, d) for s, d in zip(t.stride(), t.shape) if d != 1)
+    expect = 1
+    for s, d in pairs:
+        if s != expect:
+            return False
+        expect *= d
+    return True
+
+
+def _same_physical(a: DVal, b: DVal) -> bool:
+    return (a.split == b.split and a.t.shape == b.t.shape and a.t.stride() == b.t.stride()
+            and a.dims == b.dims)
+
+
+def _flatten_rows(shape, strides) -> tuple[int, int] | None:
+    """Collapse dims into one (count, stride) if they are uniformly strided."""
+    dims = [(d, s) for d, s in zip(shape, strides) if d != 1]
+    if not dims:
+        return 1, 0
+    count = 1
+    for i in range(len(dims) - 1):
+        if dims[i][1] != dims[i + 1][0] * dims[i + 1][1]:
+            return None
+    for d, _ in dims:
+        count *= d
+    return count, dims[-1][1]
+
+
+class Plan:
+    """A compiled graph: preallocated buffers plus one launch closure per
+    kernel. ``run`` executes eagerly; ``capture`` records a CUDA graph."""
+
+    def __init__(self, graph: Graph, weights: WeightStore, *, mode: str = "fast",
+                 device: str | torch.device = "cuda", fuse: bool = True):
+        if mode not in _MODES:
+            raise ValueError(f"mode must be one of {sorted(_MODES)}")
+        if torch.device(device).type == "cuda" and not torch.cuda.is_available():
+            raise UnsupportedOpError("a CUDA (sm_100a) device is required; there is no CPU "
+                                     "fallback for the merged operators")
+        _lib.load()
+        self.graph = graph
+        self.mode = mode
+        self.mcode = _MODES[mode]
+        self.device = torch.device(device)
+        self.fuse = fuse
+        self.steps: list[tuple[str, Callable[[int], None], int]] = []  # (node, fn, launches)
+        self.vals: dict[str, DVal] = {}
+        self.input_views: dict[str, torch.Tensor] = {}
+        self.out_buffers: list[torch.Tensor] = []
+        self.out_sources: list[DVal] = []
+        self._wcache: dict[tuple, torch.Tensor] = {}
+        self._cuda_graph: torch.cuda.CUDAGraph | None = None
+        self.dispatch_count = 0
+        self.op_invocations = 0
+        self._build(weights)
+
+    # ----------------------------------------------------------------- weights
+    def _w(self, weights: WeightStore, name: str, kind: str, dtype: torch.dtype) -> torch.Tensor:
+        key = (name, kind, dtype)
+        if key in self._wcache:
+            return self._wcache[key]
+        src = weights[name].data
+        if kind == "linear_nk":  # (G, K, N) or (K, N) -> (G, N, K) K-major
+            w = src if src.dim() == 3 else src.unsqueeze(0)
+            out = w.to(self.device, dtype).transpose(1, 2).contiguous()
+        elif kind == "linear_kn":
+            w = src if src.dim() == 3 else src.unsqueeze(0)
+            out = w.to(self.device, dtype).contiguous()
+        elif kind == "vec_f32":
+            out = src.to(self.device, torch.float32).contiguous()
+        elif kind == "same":
+            out = src.to(self.device, dtype).contiguous()
+        else:  # pragma: no cover
+            raise AssertionError(kind)
+        self._wcache[key] = out
+        return out
+
+    # ---------------------------------------------------------------- helpers
+    def _alloc(self, dims, dtype) -> torch.Tensor:
+        return torch.empty(tuple(dims), dtype=dtype, device=self.device)
+
+    def _emit(self, node_id: str, fn: Callable[[int], None], launches: int = 1) -> None:
+        self.steps.append((node_id, fn, launches))
+
+    def _copy_step(self, node_id: str, src: torch.Tensor, dst: torch.Tensor) -> None:
+        import ctypes
+        rank = max(src.dim(), 1)
+        arr = ctypes.c_int64 * rank
+        dims = arr(*(src.shape or (1,)))
+        ss = arr(*(src.stride() or (1,)))
+        ds = arr(*(dst.stride() or (1,)))
+        sp, dp, es = src.data_ptr(), dst.data_ptr(), src.element_size()
+        self._emit(node_id, lambda st: _lib.call("nf_copy_strided", sp, dp, rank, dims, ss, ds,
+                                                 es, st))
+
+    def _materialize(self, node_id: str, v: DVal) -> torch.Tensor:
+        """Contiguous tensor with the logical dims of ``v`` (copy if needed)."""
+        if v.split is None and v.t.is_contiguous():
+            return v.t
+        out = self._alloc(v.dims, v.dtype)
+        if v.split is None:
+            self._copy_step(node_id, v.t, out)
+        else:
+            a = v.split
+            m, c = v.t.shape[a], v.t.shape[a + 1]
+            self._copy_step(node_id, v.t, out.view(v.dims[:a] + (m, c) + v.dims[a + 1:]))
+        return out
+
+    # ------------------------------------------------------------------ build
+    def _build(self, weights: WeightStore) -> None:
+        g = self.graph
+        order = topological_order(g)
+        users: dict[str, list[OpNode]] = {}
+        for n in order:
+            for r in n.inputs:
+                users.setdefault(parse_ref(r)[0], []).append(n)
+        outputs = {parse_ref(r)[0] for r in g.graph_outputs}
+
+        # Graph inputs: Pack-only inputs alias their slice of the packed buffer.
+        packs = [n for n in order if n.kind is OpKind.PACK]
+        for p in packs:
+            dt = TORCH_DTYPES[p.output_spec.dtype]
+            buf = self._alloc(p.output_spec.dims, dt)
+            count, dim = p.attrs["count"], MergeDim(p.attrs["dim"])
+            for j, ref in enumerate(p.inputs):
+                name = parse_ref(ref)[0]
+                per = g.graph_inputs.get(name)
+                if per is None:
+                    continue
+                if dim is MergeDim.CHANNEL:
+                    ca = channel_axis(len(per.dims))
+                    view = buf.narrow(ca, j * per.dims[ca], per.dims[ca])
+                elif p.attrs["stacked"]:
+                    view = buf[j]
+                else:
+                    view = buf.narrow(0, j * per.dims[0], per.dims[0])
+                only_pack = all(u.kind is OpKind.PACK for u in users.get(name, []))
+                if only_pack and name not in self.input_views:
+                    self.input_views[name] = view
+            self.vals[p.id] = DVal(buf, p.output_spec.dims)
+        for name, spec in g.graph_inputs.items():
+            if name not in self.input_views:
+                t = self._alloc(spec.dims, TORCH_DTYPES[spec.dtype])
+                self.input_views[name] = t
+            self.vals[name] = DVal(self.input_views[name], spec.dims)
+        # Packs whose inputs are not pure graph inputs copy at run time.
+        for p in packs:
+            count, dim = p.attrs["count"], MergeDim(p.attrs["dim"])
+            buf = self.vals[p.id].t
+            for j, ref in enumerate(p.inputs):
+                name = parse_ref(ref)[0]
+                if name in g.graph_inputs and self._aliases(buf, self.input_views[name]):
+                    continue
+                src = self.vals[name]
+                per = src.dims
+                if dim is MergeDim.CHANNEL:
+                    ca = channel_axis(len(per))
+                    view = buf.narrow(ca, j * per[ca], per[ca])
+                elif p.attrs["stacked"]:
+                    view = buf[j]
+                else:
+                    view = buf.narrow(0, j * per[0], per[0])
+                self._copy_step(p.id, self._materialize(p.id, src), view)
+
+        fused_into: dict[str, str] = {}
+        for node in order:
+            if node.kind is OpKind.PACK:
+                self.op_invocations += 1
+                continue
+            if node.id in fused_into:
+                self.vals[node.id] = self.vals[fused_into[node.id]]
+                self.op_invocations += 1
+                self.dispatch_count += 1
+                continue
+            ins = [self.vals[parse_ref(r)[0]] for r in node.inputs]
+            try:
+                act_user = None
+                if self.fuse and node.kind in (OpKind.MATMUL, OpKind.BATCH_MATMUL):
+                    us = users.get(node.id, [])
+                    exact_ok = self.mcode == _lib.NF_MODE_FAST or (
+                        us and us[0].kind is OpKind.RELU)
+                    if len(us) == 1 and us[0].kind in _ACT_OF and node.id not in outputs \
+                            and exact_ok:
+                        act_user = us[0]
+                        fused_into[act_user.id] = node.id
+                out = self._lower(node, ins, weights, act_user)
+            except (ShapeError, UnsupportedOpError) as exc:
+                raise ExecutionError(node.id, exc) from exc
+            if tuple(out.dims) != node.output_spec.dims:
+                raise ExecutionError(node.id, ShapeError(
+                    f"kernel produced {out.dims}, node declares {node.output_spec.dims}"))
+            self.vals[node.id] = out
+            self.op_invocations += 1
+            if node.kind not in _BOUNDARY:
+                self.dispatch_count += 1
+
+        for ref in g.graph_outputs:
+            v = self.vals[parse_ref(ref)[0]]
+            buf = self._alloc(v.dims, v.dtype)
+            if v.split is None:
+                self._copy_step("output", v.t, buf)
+            else:
+                a = v.split
+                m, c = v.t.shape[a], v.t.shape[a + 1]
+                self._copy_step("output", v.t, buf.view(v.dims[:a] + (m, c) + v.dims[a + 1:]))
+            self.out_buffers.append(buf)
+
+    @staticmethod
+    def _aliases(buf: torch.Tensor, view: torch.Tensor) -> bool:
+        lo = buf.data_ptr()
+        hi = lo + buf.numel() * buf.element_size()
+        return lo <= view.data_ptr() < hi
+
+    # ------------------------------------------------------------------ nodes
+    def _lower(self, node: OpNode, ins: list[DVal], weights: WeightStore,
+               act_user: OpNode | None) -> DVal:
+        k = node.kind
+        a = node.attrs
+        spec = node.output_spec
+        if k in (OpKind.MATMUL, OpKind.BATCH_MATMUL):
+            return self._linear(node, ins[0], weights, act_user)
+        if k is OpKind.ATTENTION:
+            return self._attention(node, ins[0])
+        if k in (OpKind.LAYER_NORM, OpKind.GROUP_NORM):
+            return self._norm(node, ins[0], weights)
+        if k in (OpKind.ADD, OpKind.MUL, OpKind.RELU, OpKind.TANH, OpKind.GELU):
+            return self._pointwise(node, ins)
+        if k is OpKind.RESHAPE:
+            return self._reshape(node, ins[0], tuple(a["dims"]))
+        if k is OpKind.TRANSPOSE:
+            v = ins[0]
+            if v.split is not None:
+                v = DVal(self._materialize(node.id, v), v.dims)
+            perm = tuple(a["perm"])
+            return DVal(v.t.permute(perm), tuple(v.dims[p] for p in perm))
+        if k is OpKind.UNPACK:
+            return self._unpack(node, ins[0])
+        if k is OpKind.SOFTMAX:
+            return self._softmax(node, ins[0])
+        if k is OpKind.BATCH_NORM:
+            return self._batch_norm(node, ins[0], weights)
+        if k in (OpKind.CONV2D, OpKind.GROUPED_CONV2D):
+            return self._conv(node, ins[0], weights)
+        if k in (OpKind.MAX_POOL2D, OpKind.MEAN_POOL2D):
+            return self._pool(node, ins[0])
+        if k is OpKind.SLICE:
+            v = ins[0]
+            x = v.t if v.split is None else self._materialize(node.id, v)
+            ax = a["axis"] % len(v.dims)
+            t = x.narrow(ax, a["start"], a["stop"] - a["start"])
+            if a.get("squeeze", False):
+                t = t.squeeze(ax)
+            return DVal(t, spec.dims)
+        if k is OpKind.CONCAT:
+            out = self._alloc(spec.dims, ins[0].dtype)
+            ax = a["axis"] % len(spec.dims)
+            off = 0
+            for v in ins:
+                x = v.t if v.split is None else self._materialize(node.id, v)
+                self._copy_step(node.id, x, out.narrow(ax, off, v.dims[ax]))
+                off += v.dims[ax]
+            return DVal(out, spec.dims)
+        raise UnsupportedOpError(f"no sm_100a lowering for kind {k.value}")
+
+    def _linear(self, node, v, weights, act_user):
+        x = self._materialize(node.id, v)
+        wname = node.weights[0]
+        wsrc = weights[wname]
+        dt = x.dtype
+        if wsrc.data.dtype != dt:
+            raise ShapeError(f"weight {wname!r} dtype {wsrc.spec.dtype} does not match input")
+        if node.kind is OpKind.BATCH_MATMUL:
+            groups, k_in, n_out = wsrc.spec.dims
+            if groups != node.attrs["batch_count"] or x.shape[0] != groups:
+                raise ShapeError(f"weight batch {groups} != batch_count "
+                                 f"{node.attrs['batch_count']}")
+        else:
+            groups = 1
+            k_in, n_out = wsrc.spec.dims
+        if x.shape[-1] != k_in:
+            raise ShapeError(f"operands incompatible: {tuple(x.shape)} vs {wsrc.spec.dims}")
+        rows = x.numel() // (groups * k_in)
+        fast_tc = self.mcode == _lib.NF_MODE_FAST and dt == torch.bfloat16
+        layout = _lib.NF_W_NK if fast_tc else _lib.NF_W_KN
+        w = self._w(weights, wname, "linear_nk" if fast_tc else "linear_kn", dt)
+        bias = self._w(weights, node.weights[1], "vec_f32", dt) if len(node.weights) > 1 else None
+        y = self._alloc(node.output_spec.dims, dt)
+        act = _ACT_OF[act_user.kind] if act_user is not None else _lib.NF_ACT_NONE
+        xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, \
+            y.data_ptr()
+        dcode, mcode = K.dtype_code(x), self.mcode
+        self._emit(node.id, lambda st: _lib.call(
+            "nf_grouped_linear", xp, wp, bp, None, yp, groups, rows, k_in, n_out, dcode, layout,
+            act, mcode, st))
+        return DVal(y, node.output_spec.dims)
+
+    def _attention(self, node, v):
+        x = self._materialize(node.id, v)
+        heads = node.attrs["heads"]
+        d = x.shape[-1] // 3
+        dh = d // heads
+        s = x.shape[-2]
+        bt = x.numel() // (s * 3 * d)
+        y = self._alloc(node.output_spec.dims, x.dtype)
+        scale = node.attrs.get("scale") or 1.0 / math.sqrt(dh)
+        xp, yp, dcode, mcode = x.data_ptr(), y.data_ptr(), K.dtype_code(x), self.mcode
+        self._emit(node.id, lambda st: _lib.call("nf_attention", xp, yp, bt, s, heads, dh,
+                                                 float(scale), dcode, mcode, st))
+        return DVal(y, node.output_spec.dims)
+
+    def _norm(self, node, v, weights):
+        groups = node.attrs.get("groups", 1)
+        eps = float(node.attrs["eps"])
+        gam = self._w(weights, node.weights[0], "vec_f32", v.dtype)
+        bet = self._w(weights, node.weights[1], "vec_f32", v.dtype)
+        rank = len(v.dims)
+        ca = channel_axis(rank)
+        c = v.dims[ca]
+        if c % groups:
+            raise ShapeError(f"groups {groups} does not divide channels {c}")
+        geom = None
+        if v.split is not None and v.split == ca and rank in (2, 3):
+            # model-major storage (..., M, C): rows = (M, leading rows)
+            t = v.t
+            m, cm = t.shape[ca], t.shape[ca + 1]
+            if groups % m == 0 and t.stride(ca + 1) == 1:
+                lead = _flatten_rows(t.shape[:ca], t.stride()[:ca])
+                if lead is not None:
+                    rows, srow = lead
+                    g_per = groups // m
+                    cg = cm // g_per
+                    geom = (m, rows, t.stride(ca), srow, g_per, cg, cg, 1, rows)
+                    out = torch.empty_strided(t.shape, t.stride(), dtype=t.dtype,
+                                              device=self.device)
+                    base_t = t
+        if geom is None:
+            x = self._materialize(node.id, v)
+            before = math.prod(x.shape[:ca])
+            after = math.prod(x.shape[ca + 1:])
+            cg = c // groups
+            geom = (before, after, c * after, 1, groups, cg, cg * after, after, 0)
+            out = torch.empty_like(x)
+            base_t = x
+            result = DVal(out, v.dims)
+        else:
+            result = DVal(out, v.dims, split=v.split)
+        xp, yp = base_t.data_ptr(), out.data_ptr()
+        gp, bp = gam.data_ptr(), bet.data_ptr()
+        dcode = K.dtype_code(base_t)
+        self._emit(node.id, lambda st: _lib.call("nf_group_norm", xp, None, gp, bp, yp, *geom,
+                                                 eps, dcode, st))
+        return result
+
+    def _pointwise(self, node, ins):
+        op = _EW_OF[node.kind]
+        if len(ins) == 2 and not _same_physical(ins[0], ins[1]):
+            ins = [DVal(self._materialize(node.id, v), v.dims) for v in ins]
+        v0 = ins[0]
+        if _dense_block(v0.t):
+            out = torch.empty_strided(v0.t.shape, v0.t.stride(), dtype=v0.dtype,
+                                      device=self.device)
+            srcs = [v.t for v in ins]
+            result = DVal(out, v0.dims, v0.split)
+        else:
+            srcs = [self._materialize(node.id, v) for v in ins]
+            out = self._alloc(v0.dims, v0.dtype)
+            result = DVal(out, v0.dims)
+        n = out.numel()
+        ap = srcs[0].data_ptr()
+        bp = srcs[1].data_ptr() if len(srcs) > 1 else None
+        # storage start of a permuted dense block is the min-offset element,
+        # which for non-negative strides is data_ptr() itself.
+        yp, dcode = out.data_ptr(), K.dtype_code(out)
+        self._emit(node.id, lambda st: _lib.call("nf_elementwise", op, ap, bp, yp, n, dcode, st))
+        return result
+
+    def _reshape(self, node, v, dims):
+        if v.split is not None:
+            a = v.split
+            unsplit = v.dims[:a] + (v.t.shape[a], v.t.shape[a + 1]) + v.dims[a + 1:]
+            if dims == unsplit:
+                return DVal(v.t, dims)
+            v = DVal(self._materialize(node.id, v), v.dims)
+        try:
+            return DVal(v.t.view(dims), dims)
+        except RuntimeError:
+            pass
+        src = tuple(v.t.shape)
+        for a in range(len(src) - 1):
+            if src[:a] + (src[a] * src[a + 1],) + src[a + 2:] == dims and v.t.stride(a + 1) == 1:
+                return DVal(v.t, dims, split=a)
+        return DVal(self._materialize(node.id, v).view(dims), dims)
+
+    def _unpack(self, node, v):
+        count, dim, stacked, j = node.attrs["count"], MergeDim(node.attrs["dim"]), \
+            node.attrs["stacked"], node.attrs["index"]
+        if dim is MergeDim.CHANNEL:
+            ca = channel_axis(len(v.dims))
+            if v.split is not None and v.split == ca and v.t.shape[ca] == count:
+                return DVal(v.t.select(ca, j), node.output_spec.dims)
+            x = v.t if v.split is None else self._materialize(node.id, v)
+            c = v.dims[ca] // count
+            return DVal(x.narrow(ca, j * c, c), node.output_spec.dims)
+        x = v.t if v.split is None else self._materialize(node.id, v)
+        if stacked:
+            return DVal(x.select(0, j), node.output_spec.dims)
+        b = v.dims[0] // count
+        return DVal(x.narrow(0, j * b, b), node.output_spec.dims)
+
+    def _softmax(self, node, v):
+        x = self._materialize(node.id, v)
+        ax = node.attrs["axis"] % x.dim()
+        outer = math.prod(x.shape[:ax])
+        inner = math.prod(x.shape[ax + 1:])
+        L = x.shape[ax]
+        y = torch.empty_like(x)
+        xp, yp, dcode = x.data_ptr(), y.data_ptr(), K.dtype_code(x)
+        self._emit(node.id, lambda st: _lib.call("nf_softmax", xp, yp, outer, L, inner,
+                                                 L * inner, inner, 1, dcode, st))
+        return DVal(y, v.dims)
+
+    def _batch_norm(self, node, v, weights):
+        x = self._materialize(node.id, v)
+        ca = channel_axis(x.dim())
+        c = x.shape[ca]
+        vecs = [self._w(weights, w, "vec_f32", x.dtype) for w in node.weights]
+        for name, t in zip(("gamma", "beta", "running_mean", "running_var"), vecs):
+            if tuple(t.shape) != (c,):
+                raise ShapeError(f"{name} must be ({c},), got {tuple(t.shape)}")
+        if bool((vecs[3] < 0).any()):
+            raise ShapeError("running_var has negative entries")
+        y = torch.empty_like(x)
+        n, inner = math.prod(x.shape[:ca]), math.prod(x.shape[ca + 1:])
+        ptrs = [t.data_ptr() for t in vecs]
+        xp, yp, dcode, eps = x.data_ptr(), y.data_ptr(), K.dtype_code(x), float(node.attrs["eps"])
+        self._emit(node.id, lambda st: _lib.call("nf_batch_norm", xp, *ptrs, yp, n, c, inner,
+                                                 eps, dcode, st))
+        return DVal(y, v.dims)
+
+    def _conv(self, node, v, weights):
+        x = self._materialize(node.id, v)
+        w = self._w(weights, node.weights[0], "same", x.dtype)
+        if weights[node.weights[0]].data.dtype != x.dtype:
+            raise ShapeError(f"weight {node.weights[0]!r} dtype does not match input")
+        bias = self._w(weights, node.weights[1], "vec_f32", x.dtype) if len(node.weights) > 1 \
+            else None
+        groups = node.attrs.get("groups", 1)
+        n, cin, h, wd = x.shape
+        cout, cg, k, _ = w.shape
+        if cg != cin // groups or cin % groups or cout % groups:
+            raise ShapeError(f"kernel {tuple(w.shape)} incompatible with {cin} channels in "
+                             f"{groups} group(s)")
+        y = self._alloc(node.output_spec.dims, x.dtype)
+        s, p = node.attrs["stride"], node.attrs["padding"]
+        xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), None if bias is None else bias.data_ptr(), \
+            y.data_ptr()
+        dcode, mcode = K.dtype_code(x), self.mcode
+        self._emit(node.id, lambda st: _lib.call("nf_grouped_conv2d", xp, wp, bp, None, None, yp,
+                                                 n, cin, h, wd, cout, k, s, p, groups, 0, dcode,
+                                                 mcode, st))
+        return DVal(y, node.output_spec.dims)
+
+    def _pool(self, node, v):
+        x = self._materialize(node.id, v)
+        n, c, h, w = x.shape
+        y = self._alloc(node.output_spec.dims, x.dtype)
+        kind = _lib.NF_POOL_MAX if node.kind is OpKind.MAX_POOL2D else _lib.NF_POOL_MEAN
+        k, s, p = node.attrs["kernel"], node.attrs["stride"], node.attrs.get("padding", 0)
+        xp, yp, dcode = x.data_ptr(), y.data_ptr(), K.dtype_code(x)
+        self._emit(node.id, lambda st: _lib.call("nf_pool2d", xp, yp, n, c, h, w, kind, k, s, p,
+                                                 dcode, st))
+        return DVal(y, node.output_spec.dims)
+
+    # -------------------------------------------------------------- running
+    @property
+    def kernel_launches(self) -> int:
+        return sum(n for _, _, n in self.steps)
+
+    def load_inputs(self, inputs: dict, non_blocking: bool = True) -> None:
+        """Copy graph inputs into the plan's static input buffers."""
+        for name, spec in self.graph.graph_inputs.items():
+            if name not in inputs:
+                raise ExecutionError(name, KeyError(f"graph input {name!r} not provided"))
+            val = inputs[name]
+            data = val.data if isinstance(val, TensorValue) else val
+            if not isinstance(data, torch.Tensor):
+                data = torch.as_tensor(data)
+            if tuple(data.shape) != spec.dims or data.dtype != TORCH_DTYPES[spec.dtype]:
+                raise ExecutionError(name, ShapeError(
+                    f"input {name!r}: got {tuple(data.shape)} ({data.dtype}), graph wants "
+                    f"{spec.dims} ({spec.dtype})"))
+            self.input_views[name].copy_(data, non_blocking=non_blocking)
+
+    def launch(self, stream: int | None = None, events: list | None = None) -> None:
+        if self.device.type != "cuda":
+            raise UnsupportedOpError("plan was built for structure inspection only (no device)")
+        st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        if events is None:
+            for _, fn, _ in self.steps:
+                fn(st)
+            return
+        for _, fn, _ in self.steps:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(st)
+            events.append(e0)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        events.append(e)
+
+    def capture(self) -> torch.cuda.CUDAGraph:
+        """Record every launch into one CUDA graph (after one warm-up run)."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.launch()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch()
+        self._cuda_graph = g
+        return g
+
+    def replay(self) -> None:
+        if self._cuda_graph is None:
+            self.capture()
+        self._cuda_graph.replay()
+
+    def outputs(self) -> list[torch.Tensor]:
+        return self.out_buffers
+
+
+# ----------------------------------------------------------------------------
+# Reference-compatible entry point
+# ----------------------------------------------------------------------------
+
+_PLAN_CACHE: dict[tuple, Plan] = {}
+
+
+def compile_plan(graph: Graph, weights: WeightStore, *, mode: str = "fast",
+                 fuse: bool = True) -> Plan:
+    """Build (or fetch the cached) plan for ``graph`` with ``weights``."""
+    key = (id(graph), id(weights), mode, fuse)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None or plan.graph is not graph:
+        plan = Plan(graph, weights, mode=mode, fuse=fuse)
+        _PLAN_CACHE[key] = plan
+    return plan
+
+
+def execute(graph: Graph, weights: WeightStore, inputs: dict[str, TensorValue], *,
+            mode: str = "fast", trace_nodes: bool = False,
+            fuse: bool = True) -> tuple[list[TensorValue], ExecTrace]:
+    """Run a graph on the GPU (reference engine.py:516-573 contract).
+
+    Inputs may live on the host or the device; outputs are fresh device
+    tensors in ``graph_outputs`` order. Missing inputs / shape errors /
+    kernel failures raise ExecutionError naming the node.
+    """
+    for name, spec in graph.graph_inputs.items():
+        tv = inputs.get(name)
+        if tv is None:
+            raise ExecutionError(name, KeyError(f"graph input {name!r} not provided"))
+        if tv.spec.dims != spec.dims or tv.spec.dtype != spec.dtype:
+            raise ExecutionError(name, ShapeError(
+                f"input {name!r}: got {tv.spec.dims} ({tv.spec.dtype}), graph wants "
+                f"{spec.dims} ({spec.dtype})"))
+    plan = compile_plan(graph, weights, mode=mode, fuse=fuse)
+    trace = ExecTrace(op_invocations=plan.op_invocations, dispatch_count=plan.dispatch_count,
+                      kernel_launches=plan.kernel_launches)
+    t0 = time.perf_counter_ns()
+    plan.load_inputs(inputs)
+    events: list | None = [] if trace_nodes else None
+    plan.launch(events=events)
+    outs = [b.clone() for b in plan.outputs()]
+    torch.cuda.synchronize()
+    trace.total_ns = time.perf_counter_ns() - t0
+    if events:
+        for i, (nid, _, _) in enumerate(plan.steps):
+            ms = events[i].elapsed_time(events[i + 1])
+            trace.node_times_ns[nid] = trace.node_times_ns.get(nid, 0) + int(ms * 1e6)
+    result = []
+    for ref, t in zip(graph.graph_outputs, outs):
+        prod = parse_ref(ref)[0]
+        spec = graph.graph_inputs.get(prod) or graph.node_map()[prod].output_spec
+        tv = TensorValue(spec, t)
+        trace.node_outputs[prod] = tv
+        result.append(tv)
+    return result, trace

@@ -1,0 +1,108 @@
+"""End-to-end merged execution on the GPU against the reference.
+
+* Zoo verify matrix (the reference's acceptance criterion 4 shapes): merged
+  GPU execution reproduces the reference's per-model outputs — byte for byte
+  for cnnblock in exact mode (conv/BN/ReLU/Add/max-pool all restate the
+  reference order), within fp32 tolerance where norms/softmax reorder sums.
+* BERT-base merged (bf16, tcgen05 path): every instance's slice matches the
+  CPU oracle's per-instance forward within the bf16 gate (2e-2 normwise),
+  top-1 of the per-task heads bit-exact.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import executor as OX
+from paper_2009_13062_b200 import (ExecutionError, build_zoo, compile_plan, execute, merge,
+                                   merge_backbone, model_inputs)
+from paper_2009_13062_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+ZOO = np.load(Path(__file__).parent / "golden" / "zoo_outputs.npz")
+
+
+def normwise(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30)
+
+
+@pytest.mark.parametrize("name", ["ffnn", "cnnblock", "attnblock"])
+@pytest.mark.parametrize("m", [1, 2, 4])
+@pytest.mark.parametrize("batch", [1, 4])
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_zoo_merged_vs_reference(name, m, batch, mode):
+    graph, stores = build_zoo(name, num_models=m, batch=batch, dtype="f32")
+    merged, mstore = merge(graph, stores)
+    inputs = [model_inputs(graph, seed=0, model=j) for j in range(m)]
+    outs, trace = execute(merged.graph, mstore, merged.bind_inputs(inputs), mode=mode)
+    assert trace.dispatch_count == merged.dispatch_count
+    per = merged.slice_outputs(outs)
+    for j in range(m):
+        got = per[j][0].numpy()
+        want = ZOO[f"{name}/m{m}/b{batch}/f32/out{j}"]
+        if name == "cnnblock" and mode == "exact":
+            assert got.tobytes() == want.tobytes()
+        else:
+            assert normwise(got, want) < 1e-5
+
+
+def test_execute_names_bad_inputs():
+    graph, stores = build_zoo("ffnn", num_models=2)
+    merged, mstore = merge(graph, stores)
+    bound = merged.bind_inputs([model_inputs(graph, model=j) for j in range(2)])
+    bound.pop("x::m1")
+    with pytest.raises(ExecutionError) as exc:
+        execute(merged.graph, mstore, bound)
+    assert exc.value.node_id == "x::m1"
+
+
+def _bert_setup(name, m, batch, heads=True):
+    graph, stores = W.build_zoo(name, num_models=m, batch=batch, dtype="bf16")
+    inputs = [model_inputs(graph, seed=0, model=j) for j in range(m)]
+    if not heads:
+        merged, mstore = merge(graph, stores)
+        return graph, stores, inputs, merged, mstore, None
+    out_spec = graph.node_map()[graph.graph_outputs[0].rsplit(":", 1)[0]].output_spec
+    hs = [W.classifier_head(out_spec, w, seed=100 + j) for j, w in enumerate(W.head_widths(m))]
+    merged, mstore = merge_backbone(graph, {n.id for n in graph.nodes}, stores, hs)
+    return graph, stores, inputs, merged, mstore, hs
+
+
+def test_bert_2layer_merged_vs_oracle_all_instances():
+    graph, stores, inputs, merged, mstore, heads = _bert_setup("bert-2l", 4, 1)
+    outs, _ = execute(merged.graph, mstore, merged.bind_inputs(inputs))
+    per = merged.slice_outputs(outs)
+    for j in range(4):
+        feat = OX.execute(graph, stores[j].tensors, inputs[j])[0]
+        want = OX.execute(heads[j][0], heads[j][1].tensors, {"feat": feat})[0]
+        got = per[j][0].numpy()
+        assert normwise(got, want) < 2e-2
+        assert (got.argmax(-1) == want.argmax(-1)).all()
+
+
+def test_bert_base_12_layer_sampled_instances():
+    """Full BERT-base, N=8, B=1, S=128 (BASELINE configs[1]); oracle on the
+    first and last instance (slices are independent)."""
+    graph, stores, inputs, merged, mstore, heads = _bert_setup("bert-base", 8, 1, heads=False)
+    outs, _ = execute(merged.graph, mstore, merged.bind_inputs(inputs))
+    per = merged.slice_outputs(outs)
+    for j in (0, 7):
+        want = OX.execute(graph, stores[j].tensors, inputs[j])[0]
+        assert normwise(per[j][0].numpy(), want) < 2e-2
+
+
+def test_plan_replay_is_deterministic_and_graph_capturable():
+    graph, stores, inputs, merged, mstore, _ = _bert_setup("bert-2l", 3, 2, heads=False)
+    plan = compile_plan(merged.graph, mstore)
+    plan.load_inputs(merged.bind_inputs(inputs))
+    plan.launch()
+    a = [o.clone() for o in plan.outputs()]
+    plan.capture()
+    plan.replay()
+    torch.cuda.synchronize()
+    for x, y in zip(a, plan.outputs()):
+        assert torch.equal(x, y)

@@ -1,0 +1,54 @@
+"""Host-side executor logic without a GPU: plans built on the CPU device
+(structure only, nothing launches) must lower the merger's glue to views."""
+
+import pytest
+import torch
+
+from paper_2009_13062_b200 import OpKind, Plan, UnsupportedOpError, build_zoo, merge
+from paper_2009_13062_b200 import workloads as W
+
+
+def _copies(plan):
+    return sum(1 for nid, fn, _ in plan.steps
+               if fn.__code__.co_consts and "nf_copy_strided" in fn.__code__.co_consts)
+
+
+def test_bert_glue_is_zero_copy():
+    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    kinds = [merged.graph.node_map()[nid].kind for nid, _, _ in plan.steps
+             if nid in merged.graph.node_map()]
+    assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
+    # only the per-model output copies remain
+    assert _copies(plan) == 3
+    # per layer: qkv, attn, proj, add, ln, ff1(+gelu fused), ff2, add, ln
+    assert len(plan.steps) == 2 * 9 + 3
+    with pytest.raises(UnsupportedOpError):
+        plan.launch()
+
+
+def test_gelu_fused_into_linear_epilogue():
+    graph, stores = W.build_zoo("bert-2l", num_models=2, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    ids = [nid for nid, _, _ in plan.steps]
+    assert "merged::l00.gelu" not in ids and "merged::l00.ff1" in ids
+    assert plan.vals["merged::l00.gelu"] is plan.vals["merged::l00.ff1"]
+
+
+def test_split_values_reach_the_norm():
+    graph, stores = build_zoo("ffnn", num_models=2, batch=4)
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    v = plan.vals["reshape::0"]
+    assert v.split == 1 and tuple(v.t.shape) == (4, 2, 8)
+    assert plan.vals["merged::ln1"].split == 1
+
+
+def test_dispatch_count_matches_reference_semantics():
+    for name in ("ffnn", "cnnblock", "attnblock"):
+        graph, stores = build_zoo(name, num_models=3)
+        merged, mstore = merge(graph, stores)
+        plan = Plan(merged.graph, mstore, device="cpu")
+        assert plan.dispatch_count == merged.dispatch_count
