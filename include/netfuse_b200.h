@@ -90,6 +90,18 @@ int nf_grouped_linear(const void* x, const void* w, const void* bias, const void
                       int w_layout, int act, int mode, void* stream);
 
 /*
+ * nf_grouped_linear with explicit element strides: x row r of group g at
+ * x + g*x_gs + r*x_ld (x_ld >= k), y (and residual) at y + g*y_gs + r*y_ld.
+ * Lets the executor feed the GEMM strided views (e.g. the first-token rows of
+ * every instance's encoder output, or a padded output width) without copies.
+ * Strides must keep 16-byte row alignment for the tensor-core path.
+ */
+int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                              const void* bias, const void* residual, void* y, int64_t y_ld,
+                              int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                              int dtype, int w_layout, int act, int mode, void* stream);
+
+/*
  * Merged Conv2d == reference `grouped_conv2d` (engine.py:155-191), and with
  * groups=1 `conv2d` (engine.py:122-152). NCHW x (N, Cin, H, W), w
  * (Cout, Cin/groups, k, k), y (N, Cout, Ho, Wo). Epilogue (FAST, for the

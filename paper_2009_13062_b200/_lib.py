@@ -35,6 +35,8 @@ SIGNATURES: dict[str, list] = {
     "nf_abi_version": [],
     "nf_status_string": [_i],
     "nf_grouped_linear": [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _i, _i, _i, _p],
+    "nf_grouped_linear_strided": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                                  _i64, _i, _i, _i, _i, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],

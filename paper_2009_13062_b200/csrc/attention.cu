@@ -22,7 +22,7 @@
 namespace nf {
 
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
-                   int box_inner, int box_rows);
+                   int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 
 namespace {
 
@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(128, 2)
     tma_load_4d(sK, &map_qkv, bar_load, 0, H + h, 0, bt, kEvictFirst);
     tma_load_4d(sV, &map_qkv, bar_load, 0, 2 * H + h, 0, bt, kEvictFirst);
   }
+  grid_dependents_launch();
   mbar_wait(bar_load, 0);
 
   if (tid == 0) {
@@ -198,7 +199,6 @@ __global__ void __launch_bounds__(128, 2)
   }
   mbar_wait(bar_o, 0);
   tc_fence_after();
-  grid_dependents_launch();
   {
     uint32_t o[2][32];
     tmem_ld_32x32b_x32(tmem_o + (uint32_t(warp * 32) << 16), o[0]);
@@ -237,6 +237,7 @@ constexpr size_t kAttnSmem = 1024 + 6 * kTileBytes + 64;
 template <typename T>
 __global__ void k_attention_simt(const T* __restrict__ qkv, T* __restrict__ out, int64_t Bt,
                                  int S, int H, int dh, float scale) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -312,7 +313,7 @@ int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int6
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled();
     const float scale_log2 = scale * 1.4426950408889634f;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_attention_tc, map,
                                        static_cast<__nv_bfloat16*>(out), int(S), int(H),
@@ -323,11 +324,11 @@ int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int6
   int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > int64_t(kNumSMs) * 32) blocks = int64_t(kNumSMs) * 32;
   if (dtype == NF_F32)
-    k_attention_simt<float><<<unsigned(blocks), 256, 0, stream>>>(
+    launch_pdl(k_attention_simt<float>, dim3(unsigned(blocks)), dim3(256), 0, stream, 
         static_cast<const float*>(qkv), static_cast<float*>(out), Bt, int(S), int(H), int(dh),
         scale);
   else if (dtype == NF_BF16)
-    k_attention_simt<__nv_bfloat16><<<unsigned(blocks), 256, 0, stream>>>(
+    launch_pdl(k_attention_simt<__nv_bfloat16>, dim3(unsigned(blocks)), dim3(256), 0, stream, 
         static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(out), Bt, int(S),
         int(H), int(dh), scale);
   else

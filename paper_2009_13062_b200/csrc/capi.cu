@@ -17,21 +17,31 @@ const char* nf_status_string(int status) {
   }
 }
 
-int nf_grouped_linear(const void* x, const void* w, const void* bias, const void* residual,
-                      void* y, int64_t groups, int64_t rows, int64_t k, int64_t n, int dtype,
-                      int w_layout, int act, int mode, void* stream) {
+int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                              const void* bias, const void* residual, void* y, int64_t y_ld,
+                              int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                              int dtype, int w_layout, int act, int mode, void* stream) {
   if (!x || !w || !y || groups < 1 || rows < 1 || k < 1 || n < 1) return NF_ERR_SHAPE;
+  if (x_ld < k || y_ld < n || (groups > 1 && (x_gs < 1 || y_gs < 1))) return NF_ERR_SHAPE;
   if (dtype != NF_F32 && dtype != NF_BF16) return NF_ERR_UNSUPPORTED;
   if (w_layout != NF_W_NK && w_layout != NF_W_KN) return NF_ERR_UNSUPPORTED;
   if (act < NF_ACT_NONE || act > NF_ACT_TANH) return NF_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const float* b = static_cast<const float*>(bias);
   if (mode == NF_MODE_FAST && dtype == NF_BF16 && w_layout == NF_W_NK) {
-    int st = nf::grouped_linear_tc(x, w, b, residual, y, groups, rows, k, n, dtype, act, s);
+    int st = nf::grouped_linear_tc(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
+                                   n, dtype, act, s);
     if (st != NF_ERR_UNSUPPORTED) return st;
   }
-  return nf::grouped_linear_simt(x, w, b, residual, y, groups, rows, k, n, dtype, w_layout, act,
-                                 mode == NF_MODE_EXACT, s);
+  return nf::grouped_linear_simt(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
+                                 n, dtype, w_layout, act, mode == NF_MODE_EXACT, s);
+}
+
+int nf_grouped_linear(const void* x, const void* w, const void* bias, const void* residual,
+                      void* y, int64_t groups, int64_t rows, int64_t k, int64_t n, int dtype,
+                      int w_layout, int act, int mode, void* stream) {
+  return nf_grouped_linear_strided(x, k, rows * k, w, bias, residual, y, n, rows * n, groups,
+                                   rows, k, n, dtype, w_layout, act, mode, stream);
 }
 
 int nf_grouped_conv2d(const void* x, const void* w, const float* bias, const float* scale,

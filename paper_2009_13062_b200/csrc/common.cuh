@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/netfuse_b200.h"
 
@@ -29,9 +30,22 @@ template <typename T> NF_DEVICE T from_f32(float v);
 template <> NF_DEVICE float from_f32<float>(float v) { return v; }
 template <> NF_DEVICE __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
+// erf via Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7): one exp, one
+// reciprocal and a degree-5 polynomial instead of the libdevice erff.
+NF_DEVICE float erf_fast(float x) {
+  const float a = fabsf(x);
+  const float t = __fdividef(1.0f, fmaf(0.3275911f, a, 1.0f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  const float r = 1.0f - p * t * __expf(-a * a);
+  return copysignf(r, x);
+}
+
 NF_DEVICE float gelu_erf(float x) {
   // 0.5 x (1 + erf(x / sqrt(2))): the transformers "gelu" (exact erf form).
-  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+  return 0.5f * x * (1.0f + erf_fast(x * 0.70710678118654752440f));
 }
 
 NF_DEVICE float apply_act(float v, int act) {
@@ -257,6 +271,42 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(int M, int N, int a_m
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn_major) << 15) |
          (static_cast<uint32_t>(b_mn_major) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Launch with programmatic dependent launch enabled: the kernel may start
+// while its predecessor in the stream drains; kernels call
+// grid_dependency_wait() before touching data the predecessor writes.
+// Debug knob (read once, immutable after): NF_PDL=0 disables programmatic
+// dependent launch everywhere, for A/B timing.
+inline int pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("NF_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled();
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// Entry of every non-TMA kernel: wait for the producer grid, then let the
+// next grid in the stream begin scheduling.
+NF_DEVICE void pdl_enter() {
+  grid_dependency_wait();
+  grid_dependents_launch();
 }
 
 }  // namespace nf

@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256)
     k_conv_simt(const T* __restrict__ x, const T* __restrict__ w, const float* __restrict__ bias,
                 const float* __restrict__ scale, const T* __restrict__ residual,
                 T* __restrict__ y, ConvGeom g, int relu) {
+  pdl_enter();
   const int64_t total = int64_t(g.N) * g.Cout * g.Ho * g.Wo;
   const int cin_g = g.Cin / g.groups;
   const int cout_g = g.Cout / g.groups;
@@ -71,7 +72,7 @@ int conv2d_simt(const void* x, const void* w, const float* bias, const float* sc
   int64_t blocks = (total + 255) / 256;
   if (blocks > int64_t(kNumSMs) * 64) blocks = int64_t(kNumSMs) * 64;
 #define NF_CONV(T, E)                                                                      \
-  k_conv_simt<T, E><<<unsigned(blocks), 256, 0, s>>>(                                      \
+  launch_pdl(k_conv_simt<T, E>, dim3(unsigned(blocks)), dim3(256), 0, s,                                       \
       static_cast<const T*>(x), static_cast<const T*>(w), bias, scale,                     \
       static_cast<const T*>(residual), static_cast<T*>(y), g, relu)
   if (dtype == NF_F32) {

@@ -119,6 +119,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) NF_TRACE(0);
+  // Let the next kernel in the stream get scheduled as SMs free up; it waits
+  // on griddepcontrol.wait for this grid's results before reading them.
+  grid_dependents_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -186,7 +189,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (threadIdx.x == 64) NF_TRACE(1);
-    grid_dependents_launch();
     const uint32_t stage = smem_u32(smem);  // pipeline buffers are idle now
     const __nv_bfloat16* res =
         epi.residual
@@ -320,11 +322,15 @@ static EncodeTiledFn encode_fn() {
 // 3-D bf16 tensor (G, rows, inner) with inner contiguous -> tensor map with
 // a (box_inner, box_rows, 1) SWIZZLE_128B box (box_inner * 2 == 128 bytes).
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
-                   int box_inner, int box_rows) {
+                   int box_inner, int box_rows, int64_t row_stride, int64_t g_stride) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
+  if (row_stride <= 0) row_stride = inner;
+  if (g_stride <= 0) g_stride = rows * row_stride;
+  if ((row_stride * 2) % 16 || (g_stride * 2) % 16 || (reinterpret_cast<uintptr_t>(base) & 15))
+    return false;
   cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(G)};
-  cuuint64_t strides[2] = {cuuint64_t(inner * 2), cuuint64_t(rows * inner * 2)};
+  cuuint64_t strides[2] = {cuuint64_t(row_stride * 2), cuuint64_t(g_stride * 2)};
   cuuint32_t box[3] = {cuuint32_t(box_inner), cuuint32_t(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
@@ -353,7 +359,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled();
   const int num_kb = (K + kGemmBK - 1) / kGemmBK;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, epi, num_kb);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
@@ -386,26 +392,27 @@ static int launch_tc_act(int act, const CUtensorMap& ma, const CUtensorMap& mb,
 
 // Entry used by the C ABI. x: (G, T, K) bf16; w: (G, N, K) bf16 K-major;
 // bias fp32 (G, N) or null; y/residual: (G, T, N) bf16.
-int grouped_linear_tc(const void* x, const void* w, const float* bias, const void* residual,
-                      void* y, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype, int act,
-                      cudaStream_t stream) {
+int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                      const float* bias, const void* residual, void* y, int64_t y_ld,
+                      int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
+                      int act, cudaStream_t stream) {
   // TMA needs 16-byte aligned row strides for x, w and y.
   if (out_dtype != NF_BF16 || K % 8 != 0 || N % 8 != 0) return NF_ERR_UNSUPPORTED;
   if (G > 65535 || T > (int64_t(1) << 30) || N > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
   GemmEpilogue epi;
   epi.bias = bias;
   epi.residual = residual;
-  epi.out_gstride = T * N;
-  epi.out_ld = N;
+  epi.out_gstride = y_gs;
+  epi.out_ld = y_ld;
   epi.features = int(N);
   CUtensorMap ma, mb, my;
   if (T <= 256) {
     // Swapped: A = weights (rows N), B = activations (rows T).
     const int bn = T <= 64 ? 64 : (T <= 128 ? 128 : 256);
-    if (!make_bf16_map(&ma, w, G, N, K, kGemmBK, kGemmBM) ||
-        !make_bf16_map(&mb, x, G, T, K, kGemmBK, bn) ||
-        !make_bf16_map(&my, y, G, T, N, kOutBlock, bn))
-      return NF_ERR_LAUNCH;
+    if (!make_bf16_map(&ma, w, G, N, K, kGemmBK, kGemmBM, 0, 0) ||
+        !make_bf16_map(&mb, x, G, T, K, kGemmBK, bn, x_ld, x_gs) ||
+        !make_bf16_map(&my, y, G, T, N, kOutBlock, bn, y_ld, y_gs))
+      return NF_ERR_UNSUPPORTED;
     epi.rows_a = int(N);
     epi.rows_b = int(T);
     if (bn == 64)
@@ -417,10 +424,10 @@ int grouped_linear_tc(const void* x, const void* w, const float* bias, const voi
   }
   // Normal: A = activations (rows T), B = weights (rows N).
   const int bn = N >= 256 ? 256 : (N > 64 ? 128 : 64);
-  if (!make_bf16_map(&ma, x, G, T, K, kGemmBK, kGemmBM) ||
-      !make_bf16_map(&mb, w, G, N, K, kGemmBK, bn) ||
-      !make_bf16_map(&my, y, G, T, N, kOutBlock, kGemmBM))
-    return NF_ERR_LAUNCH;
+  if (!make_bf16_map(&ma, x, G, T, K, kGemmBK, kGemmBM, x_ld, x_gs) ||
+      !make_bf16_map(&mb, w, G, N, K, kGemmBK, bn, 0, 0) ||
+      !make_bf16_map(&my, y, G, T, N, kOutBlock, kGemmBM, y_ld, y_gs))
+    return NF_ERR_UNSUPPORTED;
   epi.rows_a = int(T);
   epi.rows_b = int(N);
   if (bn == 64)

@@ -8,13 +8,15 @@
 namespace nf {
 
 // gemm_sm100.cu — tcgen05 grouped GEMM (bf16 in, fp32 accumulate).
-int grouped_linear_tc(const void* x, const void* w, const float* bias, const void* residual,
-                      void* y, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype, int act,
-                      cudaStream_t stream);
+int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                      const float* bias, const void* residual, void* y, int64_t y_ld,
+                      int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
+                      int act, cudaStream_t stream);
 
 // linear_simt.cu — CUDA-core grouped linear (exact reference order or FMA).
-int grouped_linear_simt(const void* x, const void* w, const float* bias, const void* residual,
-                        void* y, int64_t G, int64_t T, int64_t K, int64_t N, int dtype,
+int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                        const float* bias, const void* residual, void* y, int64_t y_ld,
+                        int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int dtype,
                         int w_layout, int act, int exact, cudaStream_t stream);
 
 // pointwise.cu

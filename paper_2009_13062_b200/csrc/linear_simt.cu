@@ -22,12 +22,13 @@ template <typename T, bool EXACT, bool WKN>
 __global__ void __launch_bounds__(kSimtThreads)
     k_linear_simt(const T* __restrict__ x, const T* __restrict__ w, const float* __restrict__ bias,
                   const T* __restrict__ residual, T* __restrict__ y, int T_rows, int K, int N,
-                  int act) {
+                  int act, int64_t x_ld, int64_t x_gs, int64_t y_ld, int64_t y_gs) {
+  pdl_enter();
   __shared__ float xs[kSimtRows][kSimtChunk];
   const int g = blockIdx.z;
   const int t0 = blockIdx.y * kSimtRows;
   const int n = blockIdx.x * kSimtThreads + threadIdx.x;
-  const T* xg = x + int64_t(g) * T_rows * K;
+  const T* xg = x + int64_t(g) * x_gs;
   const T* wg = w + int64_t(g) * K * N;
   float acc[kSimtRows];
 #pragma unroll
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(kSimtThreads)
     for (int idx = threadIdx.x; idx < kSimtRows * kc; idx += kSimtThreads) {
       const int r = idx / kc, kk = idx % kc;
       const int t = t0 + r;
-      xs[r][kk] = t < T_rows ? to_f32(xg[int64_t(t) * K + k0 + kk]) : 0.0f;
+      xs[r][kk] = t < T_rows ? to_f32(xg[int64_t(t) * x_ld + k0 + kk]) : 0.0f;
     }
     __syncthreads();
     if (n < N) {
@@ -65,24 +66,26 @@ __global__ void __launch_bounds__(kSimtThreads)
     float v = acc[r];
     if (bias) v = __fadd_rn(v, b);
     v = apply_act(v, act);
-    const int64_t off = (int64_t(g) * T_rows + t) * N + n;
+    const int64_t off = int64_t(g) * y_gs + int64_t(t) * y_ld + n;
     if (residual) v = __fadd_rn(v, to_f32(residual[off]));
     y[off] = from_f32<T>(v);
   }
 }
 
 template <typename T>
-static int launch_simt(const void* x, const void* w, const float* bias, const void* residual,
-                       void* y, int64_t G, int64_t Tr, int64_t K, int64_t N, int w_layout, int act,
-                       int exact, cudaStream_t stream) {
+static int launch_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                       const float* bias, const void* residual, void* y, int64_t y_ld,
+                       int64_t y_gs, int64_t G, int64_t Tr, int64_t K, int64_t N, int w_layout,
+                       int act, int exact, cudaStream_t stream) {
   dim3 grid((N + kSimtThreads - 1) / kSimtThreads, (Tr + kSimtRows - 1) / kSimtRows, G);
   const T* xp = static_cast<const T*>(x);
   const T* wp = static_cast<const T*>(w);
   const T* rp = static_cast<const T*>(residual);
   T* yp = static_cast<T*>(y);
 #define NF_SIMT(E, L)                                                                       \
-  k_linear_simt<T, E, L><<<grid, kSimtThreads, 0, stream>>>(xp, wp, bias, rp, yp, int(Tr), \
-                                                            int(K), int(N), act)
+  launch_pdl(k_linear_simt<T, E, L>, dim3(grid), dim3(kSimtThreads), 0, stream, xp, wp, bias, rp, yp, int(Tr), \
+                                                            int(K), int(N), act, x_ld, x_gs, \
+                                                            y_ld, y_gs)
   if (exact) {
     if (w_layout == NF_W_KN) NF_SIMT(true, true); else NF_SIMT(true, false);
   } else {
@@ -92,15 +95,17 @@ static int launch_simt(const void* x, const void* w, const float* bias, const vo
   return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 
-int grouped_linear_simt(const void* x, const void* w, const float* bias, const void* residual,
-                        void* y, int64_t G, int64_t T, int64_t K, int64_t N, int dtype,
+int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                        const float* bias, const void* residual, void* y, int64_t y_ld,
+                        int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int dtype,
                         int w_layout, int act, int exact, cudaStream_t stream) {
   if (G > 65535 || (T + kSimtRows - 1) / kSimtRows > 65535) return NF_ERR_UNSUPPORTED;
   if (dtype == NF_F32)
-    return launch_simt<float>(x, w, bias, residual, y, G, T, K, N, w_layout, act, exact, stream);
+    return launch_simt<float>(x, x_ld, x_gs, w, bias, residual, y, y_ld, y_gs, G, T, K, N,
+                              w_layout, act, exact, stream);
   if (dtype == NF_BF16)
-    return launch_simt<__nv_bfloat16>(x, w, bias, residual, y, G, T, K, N, w_layout, act, exact,
-                                      stream);
+    return launch_simt<__nv_bfloat16>(x, x_ld, x_gs, w, bias, residual, y, y_ld, y_gs, G, T, K,
+                                      N, w_layout, act, exact, stream);
   return NF_ERR_UNSUPPORTED;
 }
 

@@ -26,6 +26,7 @@ static inline int grid_for(int64_t work, int threads, int per_sm = 8) {
 template <typename T, int OP>
 __global__ void k_elementwise(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
                               int64_t n) {
+  pdl_enter();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   constexpr int V = Vec8<T>::N;
   const int64_t nv = n / V;
@@ -68,11 +69,11 @@ static int launch_ew(int op, const void* a, const void* b, void* y, int64_t n, c
   T* py = static_cast<T*>(y);
   const int grid = grid_for(n / Vec8<T>::N + 1, 256);
   switch (op) {
-    case NF_EW_ADD: k_elementwise<T, NF_EW_ADD><<<grid, 256, 0, s>>>(pa, pb, py, n); break;
-    case NF_EW_MUL: k_elementwise<T, NF_EW_MUL><<<grid, 256, 0, s>>>(pa, pb, py, n); break;
-    case NF_EW_RELU: k_elementwise<T, NF_EW_RELU><<<grid, 256, 0, s>>>(pa, nullptr, py, n); break;
-    case NF_EW_TANH: k_elementwise<T, NF_EW_TANH><<<grid, 256, 0, s>>>(pa, nullptr, py, n); break;
-    case NF_EW_GELU: k_elementwise<T, NF_EW_GELU><<<grid, 256, 0, s>>>(pa, nullptr, py, n); break;
+    case NF_EW_ADD: launch_pdl(k_elementwise<T, NF_EW_ADD>, dim3(grid), dim3(256), 0, s, pa, pb, py, n); break;
+    case NF_EW_MUL: launch_pdl(k_elementwise<T, NF_EW_MUL>, dim3(grid), dim3(256), 0, s, pa, pb, py, n); break;
+    case NF_EW_RELU: launch_pdl(k_elementwise<T, NF_EW_RELU>, dim3(grid), dim3(256), 0, s, pa, nullptr, py, n); break;
+    case NF_EW_TANH: launch_pdl(k_elementwise<T, NF_EW_TANH>, dim3(grid), dim3(256), 0, s, pa, nullptr, py, n); break;
+    case NF_EW_GELU: launch_pdl(k_elementwise<T, NF_EW_GELU>, dim3(grid), dim3(256), 0, s, pa, nullptr, py, n); break;
     default: return NF_ERR_UNSUPPORTED;
   }
   return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
@@ -103,6 +104,7 @@ struct CopyGeom {
 template <int BYTES>
 __global__ void k_copy_strided(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                CopyGeom g, int64_t n) {
+  pdl_enter();
   using W = typename std::conditional<BYTES == 2, uint16_t,
             typename std::conditional<BYTES == 4, uint32_t, uint64_t>::type>::type;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -139,9 +141,9 @@ int copy_strided(const void* src, void* dst, int rank, const int64_t* dims,
   auto* ps = static_cast<const uint8_t*>(src);
   auto* pd = static_cast<uint8_t*>(dst);
   switch (elem_bytes) {
-    case 2: k_copy_strided<2><<<grid, 256, 0, s>>>(ps, pd, g, n); break;
-    case 4: k_copy_strided<4><<<grid, 256, 0, s>>>(ps, pd, g, n); break;
-    case 8: k_copy_strided<8><<<grid, 256, 0, s>>>(ps, pd, g, n); break;
+    case 2: launch_pdl(k_copy_strided<2>, dim3(grid), dim3(256), 0, s, ps, pd, g, n); break;
+    case 4: launch_pdl(k_copy_strided<4>, dim3(grid), dim3(256), 0, s, ps, pd, g, n); break;
+    case 8: launch_pdl(k_copy_strided<8>, dim3(grid), dim3(256), 0, s, ps, pd, g, n); break;
     default: return NF_ERR_UNSUPPORTED;
   }
   return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(256) k_group_norm(const T* __restrict__ x,
                                                     const float* __restrict__ gamma,
                                                     const float* __restrict__ beta,
                                                     T* __restrict__ y, NormGeom g) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -274,16 +277,16 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     auto* px = static_cast<const __nv_bfloat16*>(x);
     auto* pr = static_cast<const __nv_bfloat16*>(residual);
     auto* py = static_cast<__nv_bfloat16*>(y);
-    if (vec) k_group_norm<__nv_bfloat16, true><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
-    else k_group_norm<__nv_bfloat16, false><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
+    if (vec) launch_pdl(k_group_norm<__nv_bfloat16, true>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else launch_pdl(k_group_norm<__nv_bfloat16, false>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else if (dtype == NF_F32) {
     const bool vec = g.sc == 1 && g.Cg % 4 == 0 && g.Cg <= 4 * 32 * (kNormCache / 4) &&
                      (al & 15) == 0 && g.s1 % 4 == 0 && g.s2 % 4 == 0 && g.sg % 4 == 0;
     auto* px = static_cast<const float*>(x);
     auto* pr = static_cast<const float*>(residual);
     auto* py = static_cast<float*>(y);
-    if (vec) k_group_norm<float, true><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
-    else k_group_norm<float, false><<<grid, 256, 0, s>>>(px, pr, gamma, beta, py, g);
+    if (vec) launch_pdl(k_group_norm<float, true>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else launch_pdl(k_group_norm<float, false>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else {
     return NF_ERR_UNSUPPORTED;
   }
@@ -298,6 +301,7 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
 template <typename T>
 __global__ void k_softmax_rows(const T* __restrict__ x, T* __restrict__ y, int64_t rows,
                                int64_t L, int64_t so, int64_t inner, int64_t si) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -316,6 +320,7 @@ __global__ void k_softmax_rows(const T* __restrict__ x, T* __restrict__ y, int64
 template <typename T>
 __global__ void k_softmax_cols(const T* __restrict__ x, T* __restrict__ y, int64_t outer,
                                int64_t L, int64_t inner, int64_t so, int64_t sl, int64_t si) {
+  pdl_enter();
   const int64_t n = outer * inner;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
        t += int64_t(gridDim.x) * blockDim.x) {
@@ -359,6 +364,7 @@ __global__ void k_batch_norm(const T* __restrict__ x, const float* __restrict__ 
                              const float* __restrict__ beta, const float* __restrict__ mean,
                              const float* __restrict__ var, T* __restrict__ y, int64_t n,
                              int64_t C, int64_t inner, float eps) {
+  pdl_enter();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t c = (i / inner) % C;
@@ -375,10 +381,10 @@ int batch_norm(const void* x, const float* gamma, const float* beta, const float
   if (n < 1) return NF_ERR_SHAPE;
   const int grid = grid_for(n, 256);
   if (dtype == NF_F32)
-    k_batch_norm<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), gamma, beta, mean, var,
+    launch_pdl(k_batch_norm<float>, dim3(grid), dim3(256), 0, s, static_cast<const float*>(x), gamma, beta, mean, var,
                                             static_cast<float*>(y), n, C, inner, eps);
   else if (dtype == NF_BF16)
-    k_batch_norm<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), gamma,
+    launch_pdl(k_batch_norm<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(x), gamma,
                                                     beta, mean, var,
                                                     static_cast<__nv_bfloat16*>(y), n, C, inner,
                                                     eps);
@@ -395,6 +401,7 @@ int batch_norm(const void* x, const float* gamma, const float* beta, const float
 template <typename T, bool MAXP>
 __global__ void k_pool2d(const T* __restrict__ x, T* __restrict__ y, int64_t NC, int H, int W,
                          int Ho, int Wo, int k, int stride, int pad) {
+  pdl_enter();
   const int64_t n = NC * Ho * Wo;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -428,9 +435,9 @@ int pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind,
     auto* px = static_cast<const T*>(x);                                                    \
     auto* py = static_cast<T*>(y);                                                          \
     if (kind == NF_POOL_MAX)                                                                \
-      k_pool2d<T, true><<<grid, 256, 0, s>>>(px, py, N * C, H, W, Ho, Wo, k, stride, pad);  \
+      launch_pdl(k_pool2d<T, true>, dim3(grid), dim3(256), 0, s, px, py, N * C, H, W, Ho, Wo, k, stride, pad);  \
     else                                                                                    \
-      k_pool2d<T, false><<<grid, 256, 0, s>>>(px, py, N * C, H, W, Ho, Wo, k, stride, pad); \
+      launch_pdl(k_pool2d<T, false>, dim3(grid), dim3(256), 0, s, px, py, N * C, H, W, Ho, Wo, k, stride, pad); \
   } while (0)
   if (dtype == NF_F32) NF_POOL(float);
   else if (dtype == NF_BF16) NF_POOL(__nv_bfloat16);

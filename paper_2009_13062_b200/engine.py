@@ -138,6 +138,10 @@ class Plan:
         self.out_buffers: list[torch.Tensor] = []
         self.out_sources: list[DVal] = []
         self._wcache: dict[tuple, torch.Tensor] = {}
+        # Adds whose launch is deferred so the consuming norm can fuse them:
+        # output data_ptr -> (node id, a, b, out, launch closure)
+        self._deferred: dict[int, tuple] = {}
+        self._add_into_norm: dict[str, str] = {}
         self._cuda_graph: torch.cuda.CUDAGraph | None = None
         self.dispatch_count = 0
         self.op_invocations = 0
@@ -173,6 +177,7 @@ class Plan:
 
     def _copy_step(self, node_id: str, src: torch.Tensor, dst: torch.Tensor) -> None:
         import ctypes
+        self._flush_deferred(src)
         rank = max(src.dim(), 1)
         arr = ctypes.c_int64 * rank
         dims = arr(*(src.shape or (1,)))
@@ -252,7 +257,12 @@ class Plan:
                 self._copy_step(p.id, self._materialize(p.id, src), view)
 
         fused_into: dict[str, str] = {}
-        for node in order:
+        self._add_into_norm = self._fusable_adds(order, users, outputs) if self.fuse else {}
+        groups = self._sibling_groups(order) if self.fuse else {}
+        done: set[str] = set()
+        for node in self._grouped_order(order, groups):
+            if node.id in done:
+                continue
             if node.kind is OpKind.PACK:
                 self.op_invocations += 1
                 continue
@@ -261,7 +271,21 @@ class Plan:
                 self.op_invocations += 1
                 self.dispatch_count += 1
                 continue
+            members = groups.get(node.id)
+            if members is not None:
+                try:
+                    batched = self._lower_siblings(members, weights, users, outputs, fused_into)
+                except (ShapeError, UnsupportedOpError) as exc:
+                    raise ExecutionError(node.id, exc) from exc
+                if batched:
+                    for mem in members:
+                        done.add(mem.id)
+                        self.op_invocations += 1
+                        self.dispatch_count += 1
+                    continue
             ins = [self.vals[parse_ref(r)[0]] for r in node.inputs]
+            for v in ins:
+                self._flush_deferred(v.t, keep_for=node)
             try:
                 act_user = None
                 if self.fuse and node.kind in (OpKind.MATMUL, OpKind.BATCH_MATMUL):
@@ -282,6 +306,8 @@ class Plan:
             self.op_invocations += 1
             if node.kind not in _BOUNDARY:
                 self.dispatch_count += 1
+        for key in list(self._deferred):
+            self._emit_deferred(key)
 
         for ref in g.graph_outputs:
             v = self.vals[parse_ref(ref)[0]]
@@ -293,6 +319,182 @@ class Plan:
                 m, c = v.t.shape[a], v.t.shape[a + 1]
                 self._copy_step("output", v.t, buf.view(v.dims[:a] + (m, c) + v.dims[a + 1:]))
             self.out_buffers.append(buf)
+
+    # ------------------------------------------------------- fusion helpers
+    @staticmethod
+    def _fusable_adds(order, users, outputs) -> dict[str, str]:
+        """Add nodes whose only effective consumer (looking through glue
+        Reshape/Transpose views) is a Layer/GroupNorm: add_id -> norm_id."""
+        glue = (OpKind.RESHAPE, OpKind.TRANSPOSE)
+        out = {}
+        for n in order:
+            if n.kind is not OpKind.ADD or n.id in outputs:
+                continue
+            frontier, seen_norm, ok = [n.id], None, True
+            while frontier and ok:
+                cur = frontier.pop()
+                for u in users.get(cur, []):
+                    if u.kind in glue and u.id not in outputs:
+                        frontier.append(u.id)
+                    elif u.kind in (OpKind.LAYER_NORM, OpKind.GROUP_NORM) and seen_norm is None:
+                        seen_norm = u.id
+                    else:
+                        ok = False
+            if ok and seen_norm is not None:
+                out[n.id] = seen_norm
+        return out
+
+    def _deferred_for(self, t: torch.Tensor):
+        p = t.data_ptr()
+        for key, entry in self._deferred.items():
+            o = entry[3]
+            if key <= p < key + o.numel() * o.element_size():
+                return key, entry
+        return None, None
+
+    def _emit_deferred(self, key: int) -> None:
+        nid, _, _, _, fn = self._deferred.pop(key)
+        self._emit(nid, fn)
+
+    def _flush_deferred(self, t: torch.Tensor, keep_for: OpNode | None = None) -> None:
+        key, entry = self._deferred_for(t)
+        if key is None:
+            return
+        if keep_for is not None and self._add_into_norm.get(entry[0]) == keep_for.id:
+            return
+        if keep_for is not None and keep_for.kind in (OpKind.RESHAPE, OpKind.TRANSPOSE):
+            return  # views; a materialising copy flushes through _copy_step
+        self._emit_deferred(key)
+
+    # ------------------------------------------------------ sibling heads
+    @staticmethod
+    def _sibling_groups(order) -> dict[str, list[OpNode]]:
+        """Per-model head nodes ``head<m>::<id>`` present for every model with
+        the same kind and attributes: first member id -> all members."""
+        import re
+        pat = re.compile(r"^head(\d+)::(.+)$")
+        by_suffix: dict[str, dict[int, OpNode]] = {}
+        for n in order:
+            mt = pat.match(n.id)
+            if mt:
+                by_suffix.setdefault(mt.group(2), {})[int(mt.group(1))] = n
+        out = {}
+        for suffix, members in by_suffix.items():
+            if len(members) < 2 or sorted(members) != list(range(len(members))):
+                continue
+            ms = [members[i] for i in range(len(members))]
+            k0 = ms[0]
+            if any(m.kind is not k0.kind or m.attrs != k0.attrs or
+                   len(m.inputs) != len(k0.inputs) for m in ms):
+                continue
+            out[ms[0].id] = ms
+        return out
+
+    @staticmethod
+    def _grouped_order(order, groups):
+        """Topological order in which every sibling group is contiguous: a
+        Kahn sort over super-nodes (a group = the union of its members'
+        dependencies), ties broken by position in ``order``."""
+        if not groups:
+            return order
+        import heapq
+        unit_of = {}
+        units: dict[str, list[OpNode]] = {}
+        for first, ms in groups.items():
+            units[first] = ms
+            for m in ms:
+                unit_of[m.id] = first
+        for n in order:
+            if n.id not in unit_of:
+                unit_of[n.id] = n.id
+                units[n.id] = [n]
+        rank = {n.id: i for i, n in enumerate(order)}
+        deps: dict[str, set[str]] = {u: set() for u in units}
+        users: dict[str, set[str]] = {u: set() for u in units}
+        for u, ms in units.items():
+            for m in ms:
+                for r in m.inputs:
+                    p = parse_ref(r)[0]
+                    if p in unit_of and unit_of[p] != u:
+                        deps[u].add(unit_of[p])
+                        users[unit_of[p]].add(u)
+        key = {u: min(rank[m.id] for m in ms) for u, ms in units.items()}
+        heap = [(key[u], u) for u in units if not deps[u]]
+        heapq.heapify(heap)
+        out = []
+        while heap:
+            _, u = heapq.heappop(heap)
+            out.extend(units[u])
+            for v in users[u]:
+                deps[v].discard(u)
+                if not deps[v]:
+                    heapq.heappush(heap, (key[v], v))
+        assert len(out) == len(order), "sibling grouping broke the dependency order"
+        return out
+
+    def _lower_siblings(self, members, weights, users, outputs, fused_into) -> bool:
+        """One grouped launch for M same-shape per-model MatMuls (different
+        weights, possibly different output widths): inputs read in place
+        through a uniformly strided view, weights stacked (zero-padded to a
+        common width) once at compile time."""
+        first = members[0]
+        if first.kind is not OpKind.MATMUL or self.mcode != _lib.NF_MODE_FAST:
+            return False
+        ins = [self.vals[parse_ref(m.inputs[0])[0]] for m in members]
+        if any(v.split is not None for v in ins):
+            return False
+        t0 = ins[0].t
+        if t0.dtype != torch.bfloat16 or any(v.t.shape != t0.shape or
+                                              v.t.stride() != t0.stride() for v in ins):
+            return False
+        esz = t0.element_size()
+        ptrs = [v.t.data_ptr() for v in ins]
+        gaps = {(b - a) for a, b in zip(ptrs, ptrs[1:])}
+        if len(gaps) != 1 or next(iter(gaps)) <= 0 or next(iter(gaps)) % esz:
+            return False
+        gstride = next(iter(gaps)) // esz
+        if t0.stride(-1) != 1:
+            return False
+        lead = _flatten_rows(t0.shape[:-1], t0.stride()[:-1])
+        if lead is None:
+            return False
+        rows, xld = lead
+        k_in = t0.shape[-1]
+        xld = xld or k_in
+        widths = [weights[m.weights[0]].spec.dims[1] for m in members]
+        if any(weights[m.weights[0]].spec.dims[0] != k_in for m in members):
+            return False
+        npad = -(-max(widths) // 8) * 8
+        G = len(members)
+        dev, dt = self.device, t0.dtype
+        w = torch.zeros((G, npad, k_in), dtype=dt, device=dev)
+        bias = torch.zeros((G, npad), dtype=torch.float32, device=dev)
+        has_bias = all(len(m.weights) > 1 for m in members)
+        for j, m in enumerate(members):
+            w[j, :widths[j]] = weights[m.weights[0]].data.to(dev, dt).t()
+            if has_bias:
+                bias[j, :widths[j]] = weights[m.weights[1]].data.to(dev, torch.float32)
+        self._wcache[("siblings", first.id)] = (w, bias)
+        act, act_users = _lib.NF_ACT_NONE, []
+        us = [users.get(m.id, []) for m in members]
+        if all(len(u) == 1 and u[0].kind in _ACT_OF and m.id not in outputs
+               for u, m in zip(us, members)) and len({u[0].kind for u in us}) == 1:
+            act = _ACT_OF[us[0][0].kind]
+            act_users = [u[0] for u in us]
+        y = self._alloc((G,) + tuple(t0.shape[:-1]) + (npad,), dt)
+        xp, wp, bp, yp = t0.data_ptr(), w.data_ptr(), bias.data_ptr() if has_bias else None, \
+            y.data_ptr()
+        yld, ygs = npad, rows * npad
+        mcode = self.mcode
+        self._emit(first.id, lambda st: _lib.call(
+            "nf_grouped_linear_strided", xp, xld, gstride, wp, bp, None, yp, yld, ygs, G, rows,
+            k_in, npad, _lib.NF_BF16, _lib.NF_W_NK, act, mcode, st))
+        for j, m in enumerate(members):
+            view = y[j].narrow(-1, 0, widths[j])
+            self.vals[m.id] = DVal(view, m.output_spec.dims)
+            if act_users:
+                fused_into[act_users[j].id] = m.id
+        return True
 
     @staticmethod
     def _aliases(buf: torch.Tensor, view: torch.Tensor) -> bool:
@@ -434,9 +636,18 @@ class Plan:
         else:
             result = DVal(out, v.dims, split=v.split)
         xp, yp = base_t.data_ptr(), out.data_ptr()
+        rp = None
+        key, entry = self._deferred_for(base_t)
+        if key is not None and self._add_into_norm.get(entry[0]) == node.id:
+            off = xp - key
+            a_t, b_t = entry[1], entry[2]
+            xp, rp = a_t.data_ptr() + off, b_t.data_ptr() + off
+            del self._deferred[key]
+        elif key is not None:
+            self._emit_deferred(key)
         gp, bp = gam.data_ptr(), bet.data_ptr()
         dcode = K.dtype_code(base_t)
-        self._emit(node.id, lambda st: _lib.call("nf_group_norm", xp, None, gp, bp, yp, *geom,
+        self._emit(node.id, lambda st: _lib.call("nf_group_norm", xp, rp, gp, bp, yp, *geom,
                                                  eps, dcode, st))
         return result
 
@@ -460,7 +671,12 @@ class Plan:
         # storage start of a permuted dense block is the min-offset element,
         # which for non-negative strides is data_ptr() itself.
         yp, dcode = out.data_ptr(), K.dtype_code(out)
-        self._emit(node.id, lambda st: _lib.call("nf_elementwise", op, ap, bp, yp, n, dcode, st))
+        fn = lambda st: _lib.call("nf_elementwise", op, ap, bp, yp, n, dcode, st)
+        if node.id in self._add_into_norm and srcs[0] is ins[0].t and \
+                srcs[1] is ins[1].t and self.mcode == _lib.NF_MODE_FAST:
+            self._deferred[yp] = (node.id, srcs[0], srcs[1], out, fn)
+        else:
+            self._emit(node.id, fn)
         return result
 
     def _reshape(self, node, v, dims):

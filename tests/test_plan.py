@@ -22,8 +22,9 @@ def test_bert_glue_is_zero_copy():
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
     # only the per-model output copies remain
     assert _copies(plan) == 3
-    # per layer: qkv, attn, proj, add, ln, ff1(+gelu fused), ff2, add, ln
-    assert len(plan.steps) == 2 * 9 + 3
+    # per layer: qkv, attn, proj, ln(+residual add), ff1(+gelu), ff2, ln(+add)
+    assert len(plan.steps) == 2 * 7 + 3
+    assert not any("res" in nid for nid, _, _ in plan.steps)
     with pytest.raises(UnsupportedOpError):
         plan.launch()
 
@@ -52,3 +53,16 @@ def test_dispatch_count_matches_reference_semantics():
         merged, mstore = merge(graph, stores)
         plan = Plan(merged.graph, mstore, device="cpu")
         assert plan.dispatch_count == merged.dispatch_count
+
+
+def test_sibling_heads_batch_into_grouped_launches():
+    from paper_2009_13062_b200 import merge_backbone
+    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
+    out = graph.node_map()["l01.ln2"].output_spec
+    heads = [W.classifier_head(out, w, seed=j) for j, w in enumerate((2, 3, 5))]
+    merged, mstore = merge_backbone(graph, {n.id for n in graph.nodes}, stores, heads)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    head_steps = [nid for nid, _, _ in plan.steps if nid.startswith("head")]
+    # pooler (tanh fused) and classifier: one launch each for all 3 models
+    assert head_steps == ["head0::pool", "head0::logits"]
+    assert [plan.vals[f"head{j}::logits"].dims for j in range(3)] == [(1, 2), (1, 3), (1, 5)]

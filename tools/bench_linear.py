@@ -18,6 +18,7 @@ SHAPES = {
     "bert_b1_proj": (8, 128, 768, 768),
     "bert_b1_ff1": (8, 128, 768, 3072),
     "bert_b1_ff2": (8, 128, 3072, 768),
+    "bert_b1_ff1_gelu": (8, 128, 768, 3072),
     "xlnet_b4_ff1": (32, 512, 768, 3072),
     "xlnet_b4_ff2": (32, 512, 3072, 768),
     "bert_b8_ff1": (32, 1024, 768, 3072),
@@ -52,9 +53,11 @@ def run(name, G, T, K, N, reps, flush):
                     launch_on(torch.cuda.current_stream().cuda_stream)
         return g
 
+    act = _lib.NF_ACT_GELU if name.endswith("gelu") else _lib.NF_ACT_NONE
+
     def launch_on(st):
         _lib.call("nf_grouped_linear", x.data_ptr(), w.data_ptr(), b.data_ptr(), None,
-                  y.data_ptr(), G, T, K, N, _lib.NF_BF16, _lib.NF_W_NK, _lib.NF_ACT_NONE,
+                  y.data_ptr(), G, T, K, N, _lib.NF_BF16, _lib.NF_W_NK, act,
                   _lib.NF_MODE_FAST, st)
 
     def timed(g):
