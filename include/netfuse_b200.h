@@ -102,6 +102,24 @@ int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const v
                               int dtype, int w_layout, int act, int mode, void* stream);
 
 /*
+ * Split-K workspace for nf_grouped_linear_ws: bytes needed for this shape (0
+ * when the tile count already covers the GPU). The workspace must be
+ * zero-initialised once; kernels restore its semaphores before returning.
+ */
+int64_t nf_linear_workspace_bytes(int64_t groups, int64_t rows, int64_t k, int64_t n);
+
+/*
+ * nf_grouped_linear_strided plus a split-K workspace (NULL / 0 disables
+ * split-K). Low-tile-count shapes (e.g. 8 instances x 768 features) split K
+ * across otherwise idle SMs; partials reduce in split order (deterministic).
+ */
+int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const void* bias, const void* residual, void* y, int64_t y_ld,
+                         int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                         int dtype, int w_layout, int act, int mode, void* workspace,
+                         int64_t workspace_bytes, void* stream);
+
+/*
  * Merged Conv2d == reference `grouped_conv2d` (engine.py:155-191), and with
  * groups=1 `conv2d` (engine.py:122-152). NCHW x (N, Cin, H, W), w
  * (Cout, Cin/groups, k, k), y (N, Cout, Ho, Wo). Epilogue (FAST, for the
@@ -178,6 +196,14 @@ int nf_batch_norm(const void* x, const float* gamma, const float* beta, const fl
  */
 int nf_pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind, int kernel,
               int stride, int pad, int dtype, void* stream);
+
+/*
+ * Warm the 126 MB L2 with a byte range (e.g. the next merged Linear's
+ * weights) while other kernels run, so weight streaming from HBM continues
+ * across kernel boundaries. Stream-ordered like every other entry point: the
+ * following kernel still observes everything that preceded this call.
+ */
+int nf_l2_prefetch(const void* ptr, int64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,10 @@ SIGNATURES: dict[str, list] = {
     "nf_grouped_linear": [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _i, _i, _i, _p],
     "nf_grouped_linear_strided": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                                   _i64, _i, _i, _i, _i, _p],
+    "nf_linear_workspace_bytes": [_i64, _i64, _i64, _i64],
+    "nf_grouped_linear_ws": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                             _i64, _i, _i, _i, _i, _p, _i64, _p],
+    "nf_l2_prefetch": [_p, _i64, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],
@@ -47,7 +51,7 @@ SIGNATURES: dict[str, list] = {
     "nf_pool2d": [_p, _p, _i64, _i64, _i, _i, _i, _i, _i, _i, _i, _p],
 }
 
-_RESTYPES = {"nf_status_string": ctypes.c_char_p}
+_RESTYPES = {"nf_status_string": ctypes.c_char_p, "nf_linear_workspace_bytes": ctypes.c_int64}
 
 _lib: ctypes.CDLL | None = None
 

@@ -11,9 +11,10 @@
 //   TMA loads Q, K, V tiles (128 x 64, SWIZZLE_128B) straight out of the
 //   fused QKV rows; S = Q K^T accumulates in TMEM (128 x 128 fp32); each
 //   thread owns one query row, does the max/exp2/sum in registers and writes
-//   unnormalised P (bf16) to smem in the K-major SWIZZLE_128B layout; V is
-//   transposed in smem; O = P V^T accumulates in TMEM (128 x 64) and is
-//   scaled by 1/rowsum in the epilogue. Scores never touch HBM.
+//   unnormalised P (bf16) to smem in the K-major SWIZZLE_128B layout; V's
+//   TMA tile is consumed in place as an MN-major operand; O = P V
+//   accumulates in TMEM (128 x 64) and is scaled by 1/rowsum in the
+//   epilogue. Scores never touch HBM.
 // SIMT path (any S, dh <= 128, f32 or bf16): one warp per query row with an
 //   online softmax, for shapes / dtypes the tensor-core path does not take.
 #include "common.cuh"
@@ -81,8 +82,7 @@ __global__ void __launch_bounds__(128, 2)
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + kTileBytes;
   uint8_t* sV = sK + kTileBytes;
-  uint8_t* sVt = sV + kTileBytes;          // 64 rows (dh) x 128 keys, 2 k-blocks
-  uint8_t* sP = sVt + kTileBytes;          // 128 rows x 128 keys, 2 k-blocks (32 KB)
+  uint8_t* sP = sV + kTileBytes;           // 128 rows x 128 keys, 2 k-blocks (32 KB)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kTileBytes);
   uint64_t* bar_load = bars;
   uint64_t* bar_s = bars + 1;
@@ -130,24 +130,6 @@ __global__ void __launch_bounds__(128, 2)
     umma_commit(bar_s);
   }
 
-  // Transpose V (keys x dh) into Vt (dh x keys, K-major over keys) while the
-  // score MMA runs. Thread t handles key row t: 8 chunks of 8 dh values.
-  {
-    const int key = tid;
-    const uint32_t vrow = smem_u32(sV) + key * 128;
-#pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-      uint4 u;
-      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-                   : "r"(vrow + (((ch ^ (key & 7)) << 4))));
-      const uint16_t* e = reinterpret_cast<const uint16_t*>(&u);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) st_shared_u16(smem_u32(sVt) + kmajor_off(ch * 8 + j, key, 64), e[j]);
-    }
-  }
-  fence_proxy_async_smem();
-
   // Softmax over this thread's query row (TMEM lane = tid).
   mbar_wait(bar_s, 0);
   tc_fence_after();
@@ -187,13 +169,15 @@ __global__ void __launch_bounds__(128, 2)
 
   if (tid == 0) {
     tc_fence_after();
-    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64);
-    const uint32_t pa = smem_u32(sP), va = smem_u32(sVt);
+    // B = V straight from its TMA tile: keys (the K dim) are 128-byte rows of
+    // 64 dh values, i.e. the MN-major SWIZZLE_128B layout; 16 keys per MMA.
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64, 0, 1);
+    const uint32_t pa = smem_u32(sP), va = smem_u32(sV);
 #pragma unroll
     for (int kk = 0; kk < kAttnS / 16; ++kk) {
       const int blk = kk >> 2, sub = kk & 3;
       umma_f16_ss(tmem_o, make_sw128_kmajor_desc(pa + blk * 128 * 128 + sub * 32),
-                  make_sw128_kmajor_desc(va + blk * 64 * 128 + sub * 32), idesc, kk != 0);
+                  make_sw128_mnmajor_desc(va + kk * 16 * 128, 8192, 1024), idesc, kk != 0);
     }
     umma_commit(bar_o);
   }
@@ -229,7 +213,7 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-constexpr size_t kAttnSmem = 1024 + 6 * kTileBytes + 64;
+constexpr size_t kAttnSmem = 1024 + 5 * kTileBytes + 64;
 
 // ---------------------------------------------------------------------------
 // SIMT fallback: one warp per (sequence, head, query), online softmax.

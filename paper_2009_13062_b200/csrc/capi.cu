@@ -17,10 +17,16 @@ const char* nf_status_string(int status) {
   }
 }
 
-int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                              const void* bias, const void* residual, void* y, int64_t y_ld,
-                              int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
-                              int dtype, int w_layout, int act, int mode, void* stream) {
+int64_t nf_linear_workspace_bytes(int64_t groups, int64_t rows, int64_t k, int64_t n) {
+  if (groups < 1 || rows < 1 || k < 1 || n < 1) return 0;
+  return nf::linear_workspace_bytes(groups, rows, k, n);
+}
+
+int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const void* bias, const void* residual, void* y, int64_t y_ld,
+                         int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                         int dtype, int w_layout, int act, int mode, void* workspace,
+                         int64_t workspace_bytes, void* stream) {
   if (!x || !w || !y || groups < 1 || rows < 1 || k < 1 || n < 1) return NF_ERR_SHAPE;
   if (x_ld < k || y_ld < n || (groups > 1 && (x_gs < 1 || y_gs < 1))) return NF_ERR_SHAPE;
   if (dtype != NF_F32 && dtype != NF_BF16) return NF_ERR_UNSUPPORTED;
@@ -30,11 +36,19 @@ int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const v
   const float* b = static_cast<const float*>(bias);
   if (mode == NF_MODE_FAST && dtype == NF_BF16 && w_layout == NF_W_NK) {
     int st = nf::grouped_linear_tc(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
-                                   n, dtype, act, s);
+                                   n, dtype, act, workspace, workspace_bytes, s);
     if (st != NF_ERR_UNSUPPORTED) return st;
   }
   return nf::grouped_linear_simt(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
                                  n, dtype, w_layout, act, mode == NF_MODE_EXACT, s);
+}
+
+int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                              const void* bias, const void* residual, void* y, int64_t y_ld,
+                              int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                              int dtype, int w_layout, int act, int mode, void* stream) {
+  return nf_grouped_linear_ws(x, x_ld, x_gs, w, bias, residual, y, y_ld, y_gs, groups, rows, k, n,
+                              dtype, w_layout, act, mode, nullptr, 0, stream);
 }
 
 int nf_grouped_linear(const void* x, const void* w, const void* bias, const void* residual,
@@ -106,6 +120,10 @@ int nf_pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int ki
   if (kind != NF_POOL_MAX && kind != NF_POOL_MEAN) return NF_ERR_UNSUPPORTED;
   return nf::pool2d(x, y, N, C, H, W, kind, kernel, stride, pad, dtype,
                     static_cast<cudaStream_t>(stream));
+}
+
+int nf_l2_prefetch(const void* ptr, int64_t bytes, void* stream) {
+  return nf::l2_prefetch(ptr, bytes, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

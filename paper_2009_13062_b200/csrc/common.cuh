@@ -263,6 +263,21 @@ NF_DEVICE uint64_t make_sw128_kmajor_desc(uint32_t smem_addr) {
   return d;
 }
 
+// Shared-memory descriptor for an MN-major operand in the SWIZZLE_128B
+// canonical layout ((64 MN elems, n), (8 K rows, k)) : ((contig, LBO), (128 B,
+// SBO)) for 16-bit types: 128-byte rows hold 64 consecutive MN elements, one
+// row per K index, 8-row (1 KB) swizzle atoms stacked along K at `sbo` bytes
+// and further 64-element MN chunks at `lbo` bytes (CUTLASS make_umma_desc).
+NF_DEVICE uint64_t make_sw128_mnmajor_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(2u) << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16 with bf16 A/B, fp32 D, both K-major.
 //   [4,6) D fmt (1=f32)  [7,10) A fmt (1=bf16)  [10,13) B fmt (1=bf16)
 //   [15] A major  [16] B major  [17,23) N>>3  [24,29) M>>4

@@ -11,7 +11,8 @@ namespace nf {
 int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
-                      int act, cudaStream_t stream);
+                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream);
+int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
 
 // linear_simt.cu — CUDA-core grouped linear (exact reference order or FMA).
 int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
@@ -44,6 +45,8 @@ int conv2d_simt(const void* x, const void* w, const float* bias, const float* sc
                 const void* residual, void* y, int N, int Cin, int H, int W, int Cout, int k,
                 int stride, int pad, int groups, int relu, int dtype, int exact,
                 cudaStream_t s);
+
+int l2_prefetch(const void* ptr, int64_t bytes, cudaStream_t s);
 
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,

@@ -166,7 +166,108 @@ struct NormGeom {
 
 constexpr int kNormCache = 32;  // fp32 values cached per lane
 
-template <typename T, bool VEC>
+// Vector path: sc == 1, Cg a multiple of 8 (bf16) / 4 (f32), Cg <= 32 * V *
+// (kNormCache / V). Lane l owns 16-byte chunks l, l+32, ... of its row's
+// group; the per-channel affine (a weight, independent of the producer grid)
+// is fetched before the programmatic-dependency wait so its latency hides
+// behind the previous kernel's tail.
+template <typename T>
+__global__ void __launch_bounds__(256) k_group_norm_vec(const T* __restrict__ x,
+                                                        const T* __restrict__ res,
+                                                        const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta,
+                                                        T* __restrict__ y, NormGeom g) {
+  grid_dependents_launch();
+  constexpr int V = Vec8<T>::N;
+  constexpr int Q = kNormCache / V;  // chunks per lane
+  const int lane = threadIdx.x & 31;
+  const int warp_id = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = int((int64_t(gridDim.x) * blockDim.x) >> 5);
+  const int G = int(g.G), R2 = int(g.R2);
+  const int units = int(g.R1) * R2 * G;
+  const int Cg = int(g.Cg);
+  const int nchunks = Cg / V;
+  bool waited = false;
+  for (int u = warp_id; u < units; u += nwarps) {
+    const int row = u / G, grp = u - (u / G) * G;
+    const int r1 = row / R2, r2 = row - r1 * R2;
+    const int64_t base = int64_t(r1) * g.s1 + int64_t(r2) * g.s2 + int64_t(grp) * g.sg;
+    const int64_t aff = (g.rows_per_affine > 0 ? int64_t(row / int(g.rows_per_affine)) : 0) *
+                            g.G * g.Cg + int64_t(grp) * Cg;
+    float ga[kNormCache], be[kNormCache];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < nchunks) {
+#pragma unroll
+        for (int e = 0; e < V; e += 4) {
+          const float4 a4 = __ldg(reinterpret_cast<const float4*>(gamma + aff + ch * V + e));
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + aff + ch * V + e));
+          ga[q * V + e] = a4.x; ga[q * V + e + 1] = a4.y; ga[q * V + e + 2] = a4.z;
+          ga[q * V + e + 3] = a4.w;
+          be[q * V + e] = b4.x; be[q * V + e + 1] = b4.y; be[q * V + e + 2] = b4.z;
+          be[q * V + e + 3] = b4.w;
+        }
+      }
+    }
+    if (!waited) {
+      grid_dependency_wait();
+      waited = true;
+    }
+    float v[kNormCache];
+    uint4 ux[Q], ur[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < nchunks) {
+        ux[q] = *reinterpret_cast<const uint4*>(x + base + int64_t(ch) * V);
+        if (res) ur[q] = *reinterpret_cast<const uint4*>(res + base + int64_t(ch) * V);
+      }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (lane + 32 * q < nchunks) {
+        const T* px = reinterpret_cast<const T*>(&ux[q]);
+        const T* pr = reinterpret_cast<const T*>(&ur[q]);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          float t = to_f32(px[e]);
+          if (res) t = __fadd_rn(t, to_f32(pr[e]));
+          v[q * V + e] = t;
+          sum += t;
+        }
+      }
+    }
+    const float mean = warp_sum(sum) / float(Cg);
+    float sq = 0.f;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (lane + 32 * q < nchunks)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const float d = v[q * V + e] - mean;
+          sq += d * d;
+        }
+    const float rstd = rsqrtf(warp_sum(sq) / float(Cg) + g.eps);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < nchunks) {
+        uint4 uo;
+        T* po = reinterpret_cast<T*>(&uo);
+#pragma unroll
+        for (int e = 0; e < V; ++e)
+          po[e] = from_f32<T>(ga[q * V + e] * ((v[q * V + e] - mean) * rstd) + be[q * V + e]);
+        *reinterpret_cast<uint4*>(y + base + int64_t(ch) * V) = uo;
+      }
+    }
+  }
+  if (!waited) grid_dependency_wait();
+}
+
+// Generic strided path: three passes over memory, one warp per (row, group).
+template <typename T>
 __global__ void __launch_bounds__(256) k_group_norm(const T* __restrict__ x,
                                                     const T* __restrict__ res,
                                                     const float* __restrict__ gamma,
@@ -176,89 +277,32 @@ __global__ void __launch_bounds__(256) k_group_norm(const T* __restrict__ x,
   const int lane = threadIdx.x & 31;
   const int64_t warp_id = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int64_t rows = g.R1 * g.R2;
-  const int64_t units = rows * g.G;
+  const int64_t units = g.R1 * g.R2 * g.G;
   for (int64_t u = warp_id; u < units; u += nwarps) {
     const int64_t row = u / g.G, grp = u % g.G;
     const int64_t base = (row / g.R2) * g.s1 + (row % g.R2) * g.s2 + grp * g.sg;
     const int64_t aff = (g.rows_per_affine > 0 ? (row / g.rows_per_affine) : 0) * g.G * g.Cg +
                         grp * g.Cg;
     const int Cg = int(g.Cg);
-    float v[kNormCache];
     float sum = 0.f;
-    if (VEC) {
-      // sc == 1, Cg % (8 * 32) handled by the cached vector path: each lane
-      // owns 16-byte chunks lane, lane+32, ...
-      constexpr int V = Vec8<T>::N;
-      const int nchunks = Cg / V;
-#pragma unroll
-      for (int q = 0; q < kNormCache / V; ++q) {
-        const int ch = lane + 32 * q;
-        if (ch < nchunks) {
-          uint4 ux = *reinterpret_cast<const uint4*>(x + base + int64_t(ch) * V);
-          const T* px = reinterpret_cast<const T*>(&ux);
-          uint4 ur;
-          const T* pr = reinterpret_cast<const T*>(&ur);
-          if (res) ur = *reinterpret_cast<const uint4*>(res + base + int64_t(ch) * V);
-#pragma unroll
-          for (int e = 0; e < V; ++e) {
-            float t = to_f32(px[e]);
-            if (res) t = __fadd_rn(t, to_f32(pr[e]));
-            v[q * V + e] = t;
-            sum += t;
-          }
-        }
-      }
-      sum = warp_sum(sum);
-      const float mean = sum / float(Cg);
-      float sq = 0.f;
-#pragma unroll
-      for (int q = 0; q < kNormCache / V; ++q) {
-        if (lane + 32 * q < nchunks) {
-#pragma unroll
-          for (int e = 0; e < V; ++e) {
-            const float d = v[q * V + e] - mean;
-            sq += d * d;
-          }
-        }
-      }
-      sq = warp_sum(sq);
-      const float rstd = 1.0f / sqrtf(sq / float(Cg) + g.eps);
-#pragma unroll
-      for (int q = 0; q < kNormCache / V; ++q) {
-        const int ch = lane + 32 * q;
-        if (ch < nchunks) {
-          uint4 uo;
-          T* po = reinterpret_cast<T*>(&uo);
-#pragma unroll
-          for (int e = 0; e < V; ++e) {
-            const int c = ch * V + e;
-            po[e] = from_f32<T>(gamma[aff + c] * ((v[q * V + e] - mean) * rstd) + beta[aff + c]);
-          }
-          *reinterpret_cast<uint4*>(y + base + int64_t(ch) * V) = uo;
-        }
-      }
-    } else {
-      // Generic strided path: three passes over memory.
-      for (int c = lane; c < Cg; c += 32) {
-        float t = to_f32(x[base + c * g.sc]);
-        if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
-        sum += t;
-      }
-      const float mean = warp_sum(sum) / float(Cg);
-      float sq = 0.f;
-      for (int c = lane; c < Cg; c += 32) {
-        float t = to_f32(x[base + c * g.sc]);
-        if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
-        const float d = t - mean;
-        sq += d * d;
-      }
-      const float rstd = 1.0f / sqrtf(warp_sum(sq) / float(Cg) + g.eps);
-      for (int c = lane; c < Cg; c += 32) {
-        float t = to_f32(x[base + c * g.sc]);
-        if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
-        y[base + c * g.sc] = from_f32<T>(gamma[aff + c] * ((t - mean) * rstd) + beta[aff + c]);
-      }
+    for (int c = lane; c < Cg; c += 32) {
+      float t = to_f32(x[base + c * g.sc]);
+      if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
+      sum += t;
+    }
+    const float mean = warp_sum(sum) / float(Cg);
+    float sq = 0.f;
+    for (int c = lane; c < Cg; c += 32) {
+      float t = to_f32(x[base + c * g.sc]);
+      if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
+      const float d = t - mean;
+      sq += d * d;
+    }
+    const float rstd = 1.0f / sqrtf(warp_sum(sq) / float(Cg) + g.eps);
+    for (int c = lane; c < Cg; c += 32) {
+      float t = to_f32(x[base + c * g.sc]);
+      if (res) t = __fadd_rn(t, to_f32(res[base + c * g.sc]));
+      y[base + c * g.sc] = from_f32<T>(gamma[aff + c] * ((t - mean) * rstd) + beta[aff + c]);
     }
   }
 }
@@ -269,24 +313,27 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
   if (g.R1 < 1 || g.R2 < 1 || g.G < 1 || g.Cg < 1) return NF_ERR_SHAPE;
   const int64_t units = g.R1 * g.R2 * g.G;
   const int grid = grid_for(units * 32, 256);
+  const bool small = units < (int64_t(1) << 31) && g.R1 * g.R2 < (int64_t(1) << 31) &&
+                     (reinterpret_cast<uintptr_t>(gamma) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(beta) & 15) == 0;
   const uintptr_t al = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(residual) |
                        reinterpret_cast<uintptr_t>(y);
   if (dtype == NF_BF16) {
-    const bool vec = g.sc == 1 && g.Cg % 8 == 0 && g.Cg <= 8 * 32 * (kNormCache / 8) &&
+    const bool vec = small && g.sc == 1 && g.Cg % 8 == 0 && g.Cg <= 8 * 32 * (kNormCache / 8) &&
                      (al & 15) == 0 && g.s1 % 8 == 0 && g.s2 % 8 == 0 && g.sg % 8 == 0;
     auto* px = static_cast<const __nv_bfloat16*>(x);
     auto* pr = static_cast<const __nv_bfloat16*>(residual);
     auto* py = static_cast<__nv_bfloat16*>(y);
-    if (vec) launch_pdl(k_group_norm<__nv_bfloat16, true>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
-    else launch_pdl(k_group_norm<__nv_bfloat16, false>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    if (vec) launch_pdl(k_group_norm_vec<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else launch_pdl(k_group_norm<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else if (dtype == NF_F32) {
-    const bool vec = g.sc == 1 && g.Cg % 4 == 0 && g.Cg <= 4 * 32 * (kNormCache / 4) &&
+    const bool vec = small && g.sc == 1 && g.Cg % 4 == 0 && g.Cg <= 4 * 32 * (kNormCache / 4) &&
                      (al & 15) == 0 && g.s1 % 4 == 0 && g.s2 % 4 == 0 && g.sg % 4 == 0;
     auto* px = static_cast<const float*>(x);
     auto* pr = static_cast<const float*>(residual);
     auto* py = static_cast<float*>(y);
-    if (vec) launch_pdl(k_group_norm<float, true>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
-    else launch_pdl(k_group_norm<float, false>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    if (vec) launch_pdl(k_group_norm_vec<float>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else launch_pdl(k_group_norm<float>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else {
     return NF_ERR_UNSUPPORTED;
   }
@@ -443,6 +490,41 @@ int pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind,
   else if (dtype == NF_BF16) NF_POOL(__nv_bfloat16);
   else return NF_ERR_UNSUPPORTED;
 #undef NF_POOL
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+// ---------------------------------------------------------------------------
+// L2 prefetch of a byte range (the next GEMM's weights): fire-and-forget
+// cp.async.bulk.prefetch.L2 in 16 KB pieces spread over the grid. The kernel
+// lets its successor launch immediately, and only then waits for its own
+// predecessor, so stream dependencies still chain through it.
+// ---------------------------------------------------------------------------
+constexpr int64_t kPrefetchPiece = 16 * 1024;
+
+__global__ void k_l2_prefetch(const uint8_t* __restrict__ base, int64_t bytes) {
+  grid_dependents_launch();
+  const int64_t pieces = (bytes + kPrefetchPiece - 1) / kPrefetchPiece;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pieces;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t off = i * kPrefetchPiece;
+    int64_t len = bytes - off < kPrefetchPiece ? bytes - off : kPrefetchPiece;
+    len &= ~int64_t(15);
+    if (len > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off),
+                   "r"(uint32_t(len))
+                   : "memory");
+  }
+  grid_dependency_wait();
+}
+
+int l2_prefetch(const void* ptr, int64_t bytes, cudaStream_t s) {
+  if (!ptr || bytes <= 0) return NF_OK;
+  if (reinterpret_cast<uintptr_t>(ptr) & 15) return NF_ERR_SHAPE;
+  const int64_t pieces = (bytes + kPrefetchPiece - 1) / kPrefetchPiece;
+  int64_t blocks = (pieces + 63) / 64;
+  if (blocks > kNumSMs) blocks = kNumSMs;
+  launch_pdl(k_l2_prefetch, dim3(unsigned(blocks)), dim3(64), 0, s,
+             static_cast<const uint8_t*>(ptr), bytes);
   return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 

@@ -120,7 +120,8 @@ class Plan:
     kernel. ``run`` executes eagerly; ``capture`` records a CUDA graph."""
 
     def __init__(self, graph: Graph, weights: WeightStore, *, mode: str = "fast",
-                 device: str | torch.device = "cuda", fuse: bool = True):
+                 device: str | torch.device = "cuda", fuse: bool = True,
+                 prefetch: bool = False):
         if mode not in _MODES:
             raise ValueError(f"mode must be one of {sorted(_MODES)}")
         if torch.device(device).type == "cuda" and not torch.cuda.is_available():
@@ -141,6 +142,8 @@ class Plan:
         # Adds whose launch is deferred so the consuming norm can fuse them:
         # output data_ptr -> (node id, a, b, out, launch closure)
         self._deferred: dict[int, tuple] = {}
+        self._linear_w: dict[int, tuple[int, int]] = {}  # step index -> (weight ptr, bytes)
+        self.prefetch = prefetch
         self._add_into_norm: dict[str, str] = {}
         self._cuda_graph: torch.cuda.CUDAGraph | None = None
         self.dispatch_count = 0
@@ -169,6 +172,18 @@ class Plan:
         return out
 
     # ---------------------------------------------------------------- helpers
+    def _workspace(self, groups, rows, k, n) -> torch.Tensor | None:
+        """One zero-initialised split-K workspace shared by every GEMM of the
+        plan (launches are stream-ordered; the kernel re-arms semaphores)."""
+        need = int(_lib.load().nf_linear_workspace_bytes(groups, rows, k, n))
+        if need <= 0:
+            return None
+        cur = getattr(self, "_ws", None)
+        if cur is None or cur.numel() < need:
+            # A larger shape gets a fresh buffer; earlier launches keep theirs.
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
     def _alloc(self, dims, dtype) -> torch.Tensor:
         return torch.empty(tuple(dims), dtype=dtype, device=self.device)
 
@@ -308,6 +323,8 @@ class Plan:
                 self.dispatch_count += 1
         for key in list(self._deferred):
             self._emit_deferred(key)
+        if self.fuse and self.device.type == "cuda" and self.prefetch:
+            self._insert_l2_prefetch()
 
         for ref in g.graph_outputs:
             v = self.vals[parse_ref(ref)[0]]
@@ -496,6 +513,23 @@ class Plan:
                 fused_into[act_users[j].id] = m.id
         return True
 
+    def _insert_l2_prefetch(self) -> None:
+        """Before each merged Linear, warm L2 with the *next* Linear's weights
+        so HBM keeps streaming through the attention / norm / epilogue phases
+        in between (B200: 126 MB L2 holds a whole merged layer's GEMM)."""
+        lin = sorted(self._linear_w)
+        if len(lin) < 2:
+            return
+        nxt = {i: self._linear_w[j] for i, j in zip(lin, lin[1:])}
+        steps = []
+        for i, step in enumerate(self.steps):
+            if i in nxt:
+                ptr, nbytes = nxt[i]
+                steps.append(("l2_prefetch", lambda st, p=ptr, b=nbytes:
+                              _lib.call("nf_l2_prefetch", p, b, st), 1))
+            steps.append(step)
+        self.steps = steps
+
     @staticmethod
     def _aliases(buf: torch.Tensor, view: torch.Tensor) -> bool:
         lo = buf.data_ptr()
@@ -580,9 +614,12 @@ class Plan:
         xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, \
             y.data_ptr()
         dcode, mcode = K.dtype_code(x), self.mcode
+        ws = self._workspace(groups, rows, k_in, n_out) if fast_tc else None
+        self._linear_w[len(self.steps)] = (w.data_ptr(), w.numel() * w.element_size())
+        wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
         self._emit(node.id, lambda st: _lib.call(
-            "nf_grouped_linear", xp, wp, bp, None, yp, groups, rows, k_in, n_out, dcode, layout,
-            act, mcode, st))
+            "nf_grouped_linear_ws", xp, k_in, rows * k_in, wp, bp, None, yp, n_out,
+            rows * n_out, groups, rows, k_in, n_out, dcode, layout, act, mcode, wsp, wsb, st))
         return DVal(y, node.output_spec.dims)
 
     def _attention(self, node, v):
@@ -844,12 +881,12 @@ _PLAN_CACHE: dict[tuple, Plan] = {}
 
 
 def compile_plan(graph: Graph, weights: WeightStore, *, mode: str = "fast",
-                 fuse: bool = True) -> Plan:
+                 fuse: bool = True, prefetch: bool = False) -> Plan:
     """Build (or fetch the cached) plan for ``graph`` with ``weights``."""
-    key = (id(graph), id(weights), mode, fuse)
+    key = (id(graph), id(weights), mode, fuse, prefetch)
     plan = _PLAN_CACHE.get(key)
     if plan is None or plan.graph is not graph:
-        plan = Plan(graph, weights, mode=mode, fuse=fuse)
+        plan = Plan(graph, weights, mode=mode, fuse=fuse, prefetch=prefetch)
         _PLAN_CACHE[key] = plan
     return plan
 

@@ -55,10 +55,13 @@ def run(name, G, T, K, N, reps, flush):
 
     act = _lib.NF_ACT_GELU if name.endswith("gelu") else _lib.NF_ACT_NONE
 
+    wsb = int(_lib.load().nf_linear_workspace_bytes(G, T, K, N))
+    ws = torch.zeros(max(wsb, 1), dtype=torch.uint8, device=dev)
+
     def launch_on(st):
-        _lib.call("nf_grouped_linear", x.data_ptr(), w.data_ptr(), b.data_ptr(), None,
-                  y.data_ptr(), G, T, K, N, _lib.NF_BF16, _lib.NF_W_NK, act,
-                  _lib.NF_MODE_FAST, st)
+        _lib.call("nf_grouped_linear_ws", x.data_ptr(), K, T * K, w.data_ptr(), b.data_ptr(),
+                  None, y.data_ptr(), N, T * N, G, T, K, N, _lib.NF_BF16, _lib.NF_W_NK, act,
+                  _lib.NF_MODE_FAST, ws.data_ptr() if wsb else None, wsb, st)
 
     def timed(g):
         g.replay()

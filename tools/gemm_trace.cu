@@ -18,12 +18,17 @@ int main(int argc, char** argv) {
   cudaMalloc(&y, ny * 2);
   cudaMemset(x, 0, nx * 2);
   cudaMemset(w, 0, nw * 2);
+  int64_t ws_bytes = nf::linear_workspace_bytes(G, T, K, N);
+  void* ws = nullptr;
+  if (ws_bytes) { cudaMalloc(&ws, ws_bytes); cudaMemset(ws, 0, ws_bytes); }
+  printf("workspace %lld bytes\n", (long long)ws_bytes);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int it = 0; it < 3; ++it) {
     cudaEventRecord(e0);
-    int st = nf::grouped_linear_tc(x, w, nullptr, nullptr, y, G, T, K, N, NF_BF16, 0, 0);
+    int st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, y, N, int64_t(T) * N,
+                                   G, T, K, N, NF_BF16, 0, ws, ws_bytes, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float ms;
@@ -34,12 +39,12 @@ int main(int argc, char** argv) {
   cudaMemcpyFromSymbol(tr.data(), nf::g_gemm_trace, sizeof(unsigned long long) * 4096);
   unsigned long long t0 = tr[0];
   int num_kb = (K + 63) / 64;
-  printf("start=0  epi_start=%lld  end=%lld\n", (long long)(tr[1] - t0), (long long)(tr[2] - t0));
-  for (int i = 10; i < 18; ++i) if (tr[i]) printf("  chunk %d ld done %lld\n", i - 10, (long long)(tr[i] - t0));
-  printf("  staged %lld  barrier %lld  stored %lld\n", (long long)(tr[3] - t0), (long long)(tr[4] - t0), (long long)(tr[5] - t0));
-  for (int kb = 0; kb < num_kb; ++kb)
-    printf("kb %3d  producer_free %8lld  mma_full %8lld\n", kb,
-           tr[100 + kb] ? (long long)(tr[100 + kb] - t0) : -1LL,
-           (long long)(tr[1000 + kb] - t0));
+  printf("end=%lld\n", (long long)(tr[2] - t0));
+  for (int l = 0; l < 4; ++l)
+    if (tr[1 + 4 * l] > t0)
+      printf("unit %d: acc ready %lld  partial published %lld  stored %lld\n", l,
+             (long long)(tr[1 + 4 * l] - t0), tr[3 + 4 * l] > t0 ? (long long)(tr[3 + 4 * l] - t0) : -1LL,
+             tr[4 + 4 * l] > t0 ? (long long)(tr[4 + 4 * l] - t0) : -1LL);
+  (void)num_kb;
   return 0;
 }

@@ -25,11 +25,12 @@ def main():
     ap.add_argument("--instances", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-heads", action="store_true")
+    ap.add_argument("--prefetch", action="store_true")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
     args = ap.parse_args()
     _, _, inputs, merged, mstore, _ = bench.build_workload(
         args.model, args.instances, args.batch, "bf16", 0, heads=not args.no_heads)
-    plan = compile_plan(merged.graph, mstore)
+    plan = compile_plan(merged.graph, mstore, prefetch=args.prefetch)
     plan.load_inputs(merged.bind_inputs(inputs))
     g = plan.capture()
     for _ in range(5):
