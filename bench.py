@@ -175,9 +175,10 @@ def run_ours(args) -> dict | None:
 
     from paper_2009_13062_b200 import compile_plan
 
+    from paper_2009_13062_b200.sharding import shard_range
+    shard = shard_range(args.instances * world, world, rank)  # weak scaling: N per GPU
     graph, stores, inputs, merged, mstore, heads = build_workload(
-        args.model, args.instances, args.batch, args.dtype, rank * args.instances,
-        heads=not args.no_heads)
+        args.model, len(shard), args.batch, args.dtype, shard.start, heads=not args.no_heads)
     plan = compile_plan(merged.graph, mstore, mode="fast")
     bound = merged.bind_inputs(inputs)
     plan.load_inputs(bound)

@@ -507,7 +507,7 @@ static int choose_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) 
   s = s < kMaxSplits ? s : kMaxSplits;
   // Each split adds a partial write + reduction to the critical path; only
   // worth it when every split still streams a long K range.
-  s = s < kb_total / 24 ? s : kb_total / 24;
+  s = s < kb_total / 64 ? s : kb_total / 64;
   while (s > 1 && tiles * s * int64_t(kGemmBM) * bn * 4 > ws_bytes - kCounterBytes) --s;
   return s < 1 ? 1 : s;
 }
