@@ -126,8 +126,11 @@ def build_workload(model: str, instances: int, batch: int, dtype: str, first_ins
     head_list = None
     if heads:
         out = graph.node_map()[graph.graph_outputs[0].rsplit(":", 1)[0]].output_spec
-        widths = W.head_widths(first_instance + instances)[first_instance:]
-        head_list = [W.classifier_head(out, w, seed=100 + m) for m, w in zip(ids, widths)]
+        if len(out.dims) == 4:  # CNN: per-task FC 2048 -> 1000 on the pooled features
+            head_list = [W.fc_head(out, 1000, seed=100 + m) for m in ids]
+        else:
+            widths = W.head_widths(first_instance + instances)[first_instance:]
+            head_list = [W.classifier_head(out, w, seed=100 + m) for m, w in zip(ids, widths)]
         merged, mstore = merge_backbone(graph, {n.id for n in graph.nodes}, stores, head_list)
     else:
         merged, mstore = merge(graph, stores)
@@ -288,14 +291,15 @@ def run_ours(args) -> dict | None:
         "dtype": args.dtype,
         "data": "synthetic (seeded U[-1,1] embeddings; fan-in-scaled random-init weights)",
         "config": {
-            "workload": f"{args.model} merged N={args.instances} B={args.batch} S=128 per GPU"
+            "workload": f"{args.model} merged N={args.instances} B={args.batch} per GPU"
                         + ("" if args.no_heads else " + per-task classifier heads"),
             "model": args.model,
             "instances_per_gpu": args.instances,
             "global_instances": args.instances * world,
             "global_batch": args.instances * args.batch * world,
             "batch": args.batch,
-            "seq_len": 128,
+            "seq_len": 128 if "bert" in args.model or "xlnet" in args.model else None,
+            "image": 224 if "res" in args.model else None,
             "parallelism": f"instance-shard x{world} (no collective on the hot path)",
             "l2": "flushed between timed steps (256 MiB write outside the events)",
             "timing": "CUDA events around each CUDA-graph replay; max over ranks",

@@ -78,7 +78,7 @@ const char* nf_status_string(int status);
 /*
  * Merged Linear == reference `batch_matmul` (engine.py:215-235), and with
  * groups=1 the unmerged `matmul` (engine.py:194-212):
- *   y[g, t, :] = act(x[g, t, :] @ W[g] + bias[g]) + residual[g, t, :]
+ *   y[g, t, :] = act(x[g, t, :] @ W[g] + bias[g] + residual[g, t, :])
  * x: (groups, rows, k) row-major; W per `w_layout`; bias: (groups, n) or NULL;
  * residual: (groups, rows, n) or NULL; y: (groups, rows, n).
  * FAST bf16 runs a tcgen05/TMEM/TMA tile kernel (weights streamed once per
@@ -100,6 +100,27 @@ int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const v
                               const void* bias, const void* residual, void* y, int64_t y_ld,
                               int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
                               int dtype, int w_layout, int act, int mode, void* stream);
+
+/*
+ * NHWC helpers for merged convs lowered to grouped GEMMs (reference
+ * `grouped_conv2d`, engine.py:155-191): im2col rows [pixel][group][Kpad]
+ * with column (kh*k + kw)*Cg + c (zeros beyond k*k*Cg), x NHWC (N,H,W,C).
+ */
+int nf_im2col_nhwc(const void* x, void* y, int N, int H, int W, int C, int groups, int kernel,
+                   int stride, int pad, int kpad, int dtype, void* stream);
+
+/*
+ * Direct NHWC grouped conv for small groups (ResNeXt 4..32 channels / group):
+ * w (Cout, kh, kw, Cin/groups), y = relu?(conv + bias[c] + residual), fp32
+ * bias (folded BN shift) or NULL, residual NHWC like y or NULL.
+ */
+int nf_conv_nhwc_direct(const void* x, const void* w, const float* bias, const void* residual,
+                        void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
+                        int stride, int pad, int relu, int dtype, void* stream);
+
+/* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
+int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
+                   int stride, int pad, int dtype, void* stream);
 
 /*
  * Split-K workspace for nf_grouped_linear_ws: bytes needed for this shape (0

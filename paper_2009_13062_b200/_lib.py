@@ -41,6 +41,9 @@ SIGNATURES: dict[str, list] = {
     "nf_grouped_linear_ws": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                              _i64, _i, _i, _i, _i, _p, _i64, _p],
     "nf_l2_prefetch": [_p, _i64, _p],
+    "nf_im2col_nhwc": [_p, _p] + [_i] * 10 + [_p],
+    "nf_conv_nhwc_direct": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p],
+    "nf_pool2d_nhwc": [_p, _p] + [_i] * 9 + [_p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],

@@ -122,6 +122,29 @@ int nf_pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int ki
                     static_cast<cudaStream_t>(stream));
 }
 
+int nf_im2col_nhwc(const void* x, void* y, int N, int H, int W, int C, int groups, int kernel,
+                   int stride, int pad, int kpad, int dtype, void* stream) {
+  if (!x || !y || N < 1 || H < 1 || W < 1 || C < 1) return NF_ERR_SHAPE;
+  return nf::im2col_nhwc(x, y, N, H, W, C, groups, kernel, stride, pad, kpad, dtype,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int nf_conv_nhwc_direct(const void* x, const void* w, const float* bias, const void* residual,
+                        void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
+                        int stride, int pad, int relu, int dtype, void* stream) {
+  if (!x || !w || !y || N < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return NF_ERR_SHAPE;
+  return nf::conv_nhwc_direct(x, w, bias, residual, y, N, H, W, C, Cout, groups, kernel, stride,
+                              pad, relu, dtype, static_cast<cudaStream_t>(stream));
+}
+
+int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
+                   int stride, int pad, int dtype, void* stream) {
+  if (!x || !y || N < 1 || H < 1 || W < 1 || C < 1) return NF_ERR_SHAPE;
+  if (kind != NF_POOL_MAX && kind != NF_POOL_MEAN) return NF_ERR_UNSUPPORTED;
+  return nf::pool_nhwc(x, y, N, H, W, C, kind, kernel, stride, pad, dtype,
+                       static_cast<cudaStream_t>(stream));
+}
+
 int nf_l2_prefetch(const void* ptr, int64_t bytes, void* stream) {
   return nf::l2_prefetch(ptr, bytes, static_cast<cudaStream_t>(stream));
 }

@@ -2,7 +2,7 @@
 // ("grouped") bf16 GEMM. tcgen05.mma accumulates in TMEM (two accumulator
 // buffers, so one tile's epilogue overlaps the next tile's main loop), TMA
 // streams operands through an mbarrier ring that runs continuously across
-// tiles, and the fused bias / activation / residual epilogue goes
+// tiles, and the fused epilogue y = act(acc + bias + residual) goes
 // tcgen05.ld -> registers -> swizzled smem -> TMA bulk-tensor store.
 //
 // Replaces the reference's merged-Linear kernel `batch_matmul`
@@ -333,14 +333,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (f0 + j < p.rows_b) v[j] += __ldg(bias + f0 + j);
             }
           }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = act_t<ACT>(v[j]);
           if (HAS_RES && tok < p.rows_a) {
             const __nv_bfloat16* rp = res + int64_t(tok) * p.out_ld + f0;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (f0 + j < p.rows_b) v[j] += __bfloat162float(rp[j]);
           }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_t<ACT>(v[j]);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM),
@@ -355,12 +355,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const float b = (bias && feat < p.rows_a) ? __ldg(bias + feat) : 0.0f;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            v[j] = act_t<ACT>(v[j] + b);
+            v[j] += b;
             if (HAS_RES) {
               const int tok = n0 + cc + j;
               if (feat < p.rows_a && tok < p.rows_b)
                 v[j] += __bfloat162float(res[int64_t(tok) * p.out_ld + feat]);
             }
+            v[j] = act_t<ACT>(v[j]);
           }
           const bool odd = lane & 1;
           const int feven = row & ~1;

@@ -48,6 +48,15 @@ int conv2d_simt(const void* x, const void* w, const float* bias, const float* sc
 
 int l2_prefetch(const void* ptr, int64_t bytes, cudaStream_t s);
 
+// conv_nhwc.cu
+int im2col_nhwc(const void* x, void* y, int N, int H, int W, int C, int G, int k, int stride,
+                int pad, int Kpad, int dtype, cudaStream_t s);
+int conv_nhwc_direct(const void* x, const void* w, const float* bias, const void* residual,
+                     void* y, int N, int H, int W, int C, int Cout, int G, int k, int stride,
+                     int pad, int relu, int dtype, cudaStream_t s);
+int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int k, int stride,
+              int pad, int dtype, cudaStream_t s);
+
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
               float scale, int dtype, int mode, cudaStream_t stream);

@@ -65,10 +65,9 @@ __global__ void __launch_bounds__(kSimtThreads)
     if (t >= T_rows) break;
     float v = acc[r];
     if (bias) v = __fadd_rn(v, b);
-    v = apply_act(v, act);
     const int64_t off = int64_t(g) * y_gs + int64_t(t) * y_ld + n;
     if (residual) v = __fadd_rn(v, to_f32(residual[off]));
-    y[off] = from_f32<T>(v);
+    y[off] = from_f32<T>(apply_act(v, act));
   }
 }
 

@@ -139,6 +139,7 @@ class Plan:
         self.out_buffers: list[torch.Tensor] = []
         self.out_sources: list[DVal] = []
         self._wcache: dict[tuple, torch.Tensor] = {}
+        self._buffers: list[torch.Tensor] = []
         # Adds whose launch is deferred so the consuming norm can fuse them:
         # output data_ptr -> (node id, a, b, out, launch closure)
         self._deferred: dict[int, tuple] = {}
@@ -181,11 +182,18 @@ class Plan:
         cur = getattr(self, "_ws", None)
         if cur is None or cur.numel() < need:
             # A larger shape gets a fresh buffer; earlier launches keep theirs.
-            self._ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+            self._ws = self._own(torch.zeros(need, dtype=torch.uint8, device=self.device))
         return self._ws
 
     def _alloc(self, dims, dtype) -> torch.Tensor:
-        return torch.empty(tuple(dims), dtype=dtype, device=self.device)
+        return self._own(torch.empty(tuple(dims), dtype=dtype, device=self.device))
+
+    def _own(self, t: torch.Tensor) -> torch.Tensor:
+        """Launch closures capture raw device pointers, so the plan must own
+        every buffer it hands to a kernel for its whole lifetime (otherwise
+        the caching allocator would recycle a temporary's memory)."""
+        self._buffers.append(t)
+        return t
 
     def _emit(self, node_id: str, fn: Callable[[int], None], launches: int = 1) -> None:
         self.steps.append((node_id, fn, launches))
@@ -274,6 +282,9 @@ class Plan:
         fused_into: dict[str, str] = {}
         self._add_into_norm = self._fusable_adds(order, users, outputs) if self.fuse else {}
         groups = self._sibling_groups(order) if self.fuse else {}
+        chains = self._conv_chains(order, users, outputs) \
+            if self.fuse and self.mcode == _lib.NF_MODE_FAST else {}
+        groups.update({cid: ch["nodes"] for cid, ch in chains.items()})
         done: set[str] = set()
         for node in self._grouped_order(order, groups):
             if node.id in done:
@@ -285,6 +296,22 @@ class Plan:
                 self.vals[node.id] = self.vals[fused_into[node.id]]
                 self.op_invocations += 1
                 self.dispatch_count += 1
+                continue
+            if node.id in chains:
+                ch = chains[node.id]
+                try:
+                    out = self._lower_conv_chain(ch, weights)
+                except (ShapeError, UnsupportedOpError) as exc:
+                    raise ExecutionError(node.id, exc) from exc
+                last = ch["nodes"][-1]
+                if tuple(out.dims) != last.output_spec.dims:
+                    raise ExecutionError(node.id, ShapeError(
+                        f"kernel produced {out.dims}, node declares {last.output_spec.dims}"))
+                self.vals[last.id] = out
+                for mem in ch["nodes"]:
+                    done.add(mem.id)
+                    self.op_invocations += 1
+                    self.dispatch_count += 1
                 continue
             members = groups.get(node.id)
             if members is not None:
@@ -382,6 +409,156 @@ class Plan:
         if keep_for is not None and keep_for.kind in (OpKind.RESHAPE, OpKind.TRANSPOSE):
             return  # views; a materialising copy flushes through _copy_step
         self._emit_deferred(key)
+
+    # ------------------------------------------------------ conv chains
+    @staticmethod
+    def _conv_chains(order, users, outputs) -> dict[str, dict]:
+        """Conv -> [BatchNorm] -> (ReLU | Add(other) -> [ReLU]) chains whose
+        interior values have exactly one consumer: lowered as one conv launch
+        with BN folded into weights/bias and the residual + ReLU in the
+        epilogue (the CNN plans' only inter-op traffic is then conv outputs)."""
+        out = {}
+        claimed: set[str] = set()
+
+        def single(nid):
+            us = users.get(nid, [])
+            u = us[0] if len(us) == 1 and nid not in outputs else None
+            return None if u is None or u.id in claimed else u
+
+        for n in order:
+            if n.kind not in (OpKind.CONV2D, OpKind.GROUPED_CONV2D):
+                continue
+            nodes, bn, add, other, relu = [n], None, None, None, False
+            cur = n
+            u = single(cur.id)
+            if u is not None and u.kind is OpKind.BATCH_NORM:
+                bn, cur = u, u
+                nodes.append(u)
+                u = single(cur.id)
+            if u is not None and u.kind is OpKind.RELU:
+                nodes.append(u)
+                relu = True
+            elif u is not None and u.kind is OpKind.ADD and len(u.inputs) == 2:
+                refs = [parse_ref(r)[0] for r in u.inputs]
+                if refs.count(cur.id) == 1:
+                    add, other = u, refs[1] if refs[0] == cur.id else refs[0]
+                    nodes.append(u)
+                    u2 = single(u.id)
+                    if u2 is not None and u2.kind is OpKind.RELU:
+                        nodes.append(u2)
+                        relu = True
+            if len(nodes) > 1:
+                out[n.id] = {"nodes": nodes, "conv": n, "bn": bn, "add": add, "other": other,
+                             "relu": relu}
+                claimed.update(m.id for m in nodes)
+        return out
+
+    def _nhwc(self, node_id: str, v: DVal) -> torch.Tensor:
+        """Contiguous NHWC storage of a logical NCHW value (copy if needed)."""
+        if v.split is None and v.t.dim() == 4:
+            p = v.t.permute(0, 2, 3, 1)
+            if p.is_contiguous():
+                return p
+        src = v.t if v.split is None else self._materialize(node_id, v)
+        n, c, h, w = v.dims
+        out = self._alloc((n, h, w, c), v.dtype)
+        self._copy_step(node_id, src, out.permute(0, 3, 1, 2))
+        return out
+
+    def _folded_conv(self, ch, weights, dt):
+        """Conv weights with BatchNorm folded in: returns (w (Cout, k, k, Cg)
+        fp32 scaled, bias (Cout,) fp32)."""
+        conv, bn = ch["conv"], ch["bn"]
+        w = weights[conv.weights[0]].data.to(self.device, torch.float32)
+        cout = w.shape[0]
+        bias = weights[conv.weights[1]].data.to(self.device, torch.float32) \
+            if len(conv.weights) > 1 else torch.zeros(cout, device=self.device)
+        if bn is not None:
+            g, b, m, v = (weights[x].data.to(self.device, torch.float32) for x in bn.weights)
+            if bool((v < 0).any()):
+                raise ShapeError("running_var has negative entries")
+            scale = g / torch.sqrt(v + float(bn.attrs["eps"]))
+            w = w * scale.view(-1, 1, 1, 1)
+            bias = (bias - m) * scale + b
+        return w.permute(0, 2, 3, 1).contiguous(), bias.contiguous()
+
+    def _lower_conv_chain(self, ch, weights) -> DVal:
+        conv = ch["conv"]
+        a = conv.attrs
+        v = self.vals[parse_ref(conv.inputs[0])[0]]
+        dt = v.dtype
+        groups = a.get("groups", 1)
+        k, s, pad = a["kernel"], a["stride"], a["padding"]
+        n, c, h, wd = v.dims
+        last = ch["nodes"][-1]
+        _, cout, ho, wo = last.output_spec.dims
+        if c % groups or cout % groups:
+            raise ShapeError(f"groups {groups} does not divide channels ({c} in, {cout} out)")
+        cg, coutg = c // groups, cout // groups
+        wsrc = weights[conv.weights[0]]
+        if wsrc.spec.dims != (cout, cg, k, k):
+            raise ShapeError(f"kernel {wsrc.spec.dims} incompatible with {c} channels in "
+                             f"{groups} group(s)")
+        key = ("convchain", conv.id)
+        if key not in self._wcache:
+            self._wcache[key] = self._folded_conv(ch, weights, dt)
+        wf, bias = self._wcache[key]
+        relu = 1 if ch["relu"] else 0
+        other = self.vals[ch["other"]] if ch["add"] is not None else None
+        if dt != torch.bfloat16:
+            # fp32: NCHW direct conv with the fused scale-free folded epilogue
+            x = self._materialize(conv.id, v)
+            wn = wf.permute(0, 3, 1, 2).contiguous().to(dt)
+            r = self._materialize(conv.id, other) if other is not None else None
+            y = self._alloc((n, cout, ho, wo), dt)
+            self._wcache[key + ("nchw",)] = wn
+            xp, wp, bp, yp = x.data_ptr(), wn.data_ptr(), bias.data_ptr(), y.data_ptr()
+            rp = r.data_ptr() if r is not None else None
+            dcode = K.dtype_code(x)
+            self._emit(conv.id, lambda st: _lib.call(
+                "nf_grouped_conv2d", xp, wp, bp, None, rp, yp, n, c, h, wd, cout, k, s, pad,
+                groups, relu, dcode, _lib.NF_MODE_FAST, st))
+            return DVal(y, (n, cout, ho, wo))
+        xn = self._nhwc(conv.id, v)
+        yn = self._alloc((n, ho, wo, cout), dt)
+        rn = self._nhwc(conv.id, other) if other is not None else None
+        rp = rn.data_ptr() if rn is not None else None
+        pix = n * ho * wo
+        kk = k * k * cg
+        if coutg % 8 == 0 and kk >= 32:
+            kpad = -(-kk // 8) * 8
+            wkey = key + ("gemm",)
+            if wkey not in self._wcache:
+                wg = wf.reshape(groups, coutg, kk)
+                if kpad != kk:
+                    wg = torch.nn.functional.pad(wg, (0, kpad - kk))
+                self._wcache[wkey] = (wg.to(dt).contiguous(), bias.view(groups, coutg).contiguous())
+            wg, bg = self._wcache[wkey]
+            if k == 1 and s == 1 and pad == 0 and cg % 8 == 0:
+                xp, xld, xgs, kdim = xn.data_ptr(), c, cg, cg
+            else:
+                col = self._alloc((pix, groups, kpad), dt)
+                xsrc, colp = xn.data_ptr(), col.data_ptr()
+                self._emit(conv.id, lambda st: _lib.call(
+                    "nf_im2col_nhwc", xsrc, colp, n, h, wd, c, groups, k, s, pad, kpad,
+                    _lib.NF_BF16, st))
+                xp, xld, xgs, kdim = colp, groups * kpad, kpad, kpad
+            act = _lib.NF_ACT_RELU if relu else _lib.NF_ACT_NONE
+            wp, bp, yp = wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
+            self._linear_w[len(self.steps)] = (wp, wg.numel() * wg.element_size())
+            self._emit(conv.id, lambda st: _lib.call(
+                "nf_grouped_linear_ws", xp, xld, xgs, wp, bp, rp, yp, cout, coutg, groups, pix,
+                kdim, coutg, _lib.NF_BF16, _lib.NF_W_NK, act, _lib.NF_MODE_FAST, None, 0, st))
+        else:
+            wkey = key + ("direct",)
+            if wkey not in self._wcache:
+                self._wcache[wkey] = wf.to(dt).contiguous()
+            wd_t = self._wcache[wkey]
+            xp, wp, bp, yp = xn.data_ptr(), wd_t.data_ptr(), bias.data_ptr(), yn.data_ptr()
+            self._emit(conv.id, lambda st: _lib.call(
+                "nf_conv_nhwc_direct", xp, wp, bp, rp, yp, n, h, wd, c, cout, groups, k, s, pad,
+                relu, _lib.NF_BF16, st))
+        return DVal(yn.permute(0, 3, 1, 2), (n, cout, ho, wo))
 
     # ------------------------------------------------------ sibling heads
     @staticmethod
@@ -484,8 +661,8 @@ class Plan:
         npad = -(-max(widths) // 8) * 8
         G = len(members)
         dev, dt = self.device, t0.dtype
-        w = torch.zeros((G, npad, k_in), dtype=dt, device=dev)
-        bias = torch.zeros((G, npad), dtype=torch.float32, device=dev)
+        w = self._own(torch.zeros((G, npad, k_in), dtype=dt, device=dev))
+        bias = self._own(torch.zeros((G, npad), dtype=torch.float32, device=dev))
         has_bias = all(len(m.weights) > 1 for m in members)
         for j, m in enumerate(members):
             w[j, :widths[j]] = weights[m.weights[0]].data.to(dev, dt).t()
@@ -658,8 +835,8 @@ class Plan:
                     g_per = groups // m
                     cg = cm // g_per
                     geom = (m, rows, t.stride(ca), srow, g_per, cg, cg, 1, rows)
-                    out = torch.empty_strided(t.shape, t.stride(), dtype=t.dtype,
-                                              device=self.device)
+                    out = self._own(torch.empty_strided(t.shape, t.stride(), dtype=t.dtype,
+                                                        device=self.device))
                     base_t = t
         if geom is None:
             x = self._materialize(node.id, v)
@@ -667,7 +844,7 @@ class Plan:
             after = math.prod(x.shape[ca + 1:])
             cg = c // groups
             geom = (before, after, c * after, 1, groups, cg, cg * after, after, 0)
-            out = torch.empty_like(x)
+            out = self._own(torch.empty_like(x))
             base_t = x
             result = DVal(out, v.dims)
         else:
@@ -694,8 +871,8 @@ class Plan:
             ins = [DVal(self._materialize(node.id, v), v.dims) for v in ins]
         v0 = ins[0]
         if _dense_block(v0.t):
-            out = torch.empty_strided(v0.t.shape, v0.t.stride(), dtype=v0.dtype,
-                                      device=self.device)
+            out = self._own(torch.empty_strided(v0.t.shape, v0.t.stride(), dtype=v0.dtype,
+                                                device=self.device))
             srcs = [v.t for v in ins]
             result = DVal(out, v0.dims, v0.split)
         else:
@@ -755,7 +932,7 @@ class Plan:
         outer = math.prod(x.shape[:ax])
         inner = math.prod(x.shape[ax + 1:])
         L = x.shape[ax]
-        y = torch.empty_like(x)
+        y = self._own(torch.empty_like(x))
         xp, yp, dcode = x.data_ptr(), y.data_ptr(), K.dtype_code(x)
         self._emit(node.id, lambda st: _lib.call("nf_softmax", xp, yp, outer, L, inner,
                                                  L * inner, inner, 1, dcode, st))
@@ -771,7 +948,7 @@ class Plan:
                 raise ShapeError(f"{name} must be ({c},), got {tuple(t.shape)}")
         if bool((vecs[3] < 0).any()):
             raise ShapeError("running_var has negative entries")
-        y = torch.empty_like(x)
+        y = self._own(torch.empty_like(x))
         n, inner = math.prod(x.shape[:ca]), math.prod(x.shape[ca + 1:])
         ptrs = [t.data_ptr() for t in vecs]
         xp, yp, dcode, eps = x.data_ptr(), y.data_ptr(), K.dtype_code(x), float(node.attrs["eps"])
@@ -803,6 +980,18 @@ class Plan:
         return DVal(y, node.output_spec.dims)
 
     def _pool(self, node, v):
+        kind = _lib.NF_POOL_MAX if node.kind is OpKind.MAX_POOL2D else _lib.NF_POOL_MEAN
+        k, s, p = node.attrs["kernel"], node.attrs["stride"], node.attrs.get("padding", 0)
+        if v.split is None and v.t.dim() == 4 and v.t.permute(0, 2, 3, 1).is_contiguous() \
+                and not v.t.is_contiguous():
+            xn = v.t.permute(0, 2, 3, 1)
+            n, h, w, c = xn.shape
+            _, _, ho, wo = node.output_spec.dims
+            yn = self._alloc((n, ho, wo, c), xn.dtype)
+            xp, yp, dcode = xn.data_ptr(), yn.data_ptr(), K.dtype_code(xn)
+            self._emit(node.id, lambda st: _lib.call("nf_pool2d_nhwc", xp, yp, n, h, w, c, kind,
+                                                     k, s, p, dcode, st))
+            return DVal(yn.permute(0, 3, 1, 2), node.output_spec.dims)
         x = self._materialize(node.id, v)
         n, c, h, w = x.shape
         y = self._alloc(node.output_spec.dims, x.dtype)

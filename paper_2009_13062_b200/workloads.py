@@ -180,7 +180,93 @@ def bert_layers(n: int) -> Callable[[int, str], tuple[Graph, WeightPlan]]:
     return lambda batch, dtype: _bert(batch, dtype, cfg)
 
 
+def _resnet(batch: int, dtype: str, *, groups: int = 1, width_per_group: int = 64,
+            layers=(3, 4, 6, 3), image: int = 224, stages: int = 4) -> tuple[Graph, WeightPlan]:
+    """torchvision ResNet-50 (groups=1) / ResNeXt-50 32x4d (groups=32,
+    width_per_group=4) backbone, v1.5 (stride on the 3x3), up to the global
+    average pool: (B, 3, 224, 224) -> (B, 2048, 1, 1). Convs have no bias
+    (BatchNorm follows every conv); the stem max-pool is padded (3x3 s2 p1)."""
+    nodes: list[OpNode] = []
+    plan: WeightPlan = []
+    img = lambda c, h: _spec(dtype, batch, c, h, h)  # noqa: E731
+
+    def conv(nid, src, cin, cout, k, stride, pad, h_in, g=1):
+        h = (h_in + 2 * pad - k) // stride + 1
+        kind = OpKind.GROUPED_CONV2D if g > 1 else OpKind.CONV2D
+        attrs = {"kernel": k, "stride": stride, "padding": pad}
+        if g > 1:
+            attrs["groups"] = g
+        nodes.append(OpNode(nid, kind, (src,), img(cout, h), weights=(f"{nid}.w",), attrs=attrs))
+        plan.append((f"{nid}.w", (cout, cin // g, k, k), f"fan:{cin // g * k * k}"))
+        return f"{nid}:0", h
+
+    def bn(nid, src, c, h):
+        nodes.append(OpNode(nid, OpKind.BATCH_NORM, (src,), img(c, h),
+                            weights=tuple(f"{nid}.{s}" for s in ("g", "b", "m", "v")),
+                            attrs={"eps": 1e-5}))
+        plan.extend([(f"{nid}.g", (c,), "gamma"), (f"{nid}.b", (c,), "beta"),
+                     (f"{nid}.m", (c,), "beta"), (f"{nid}.v", (c,), "var")])
+        return f"{nid}:0"
+
+    def relu(nid, src, c, h):
+        nodes.append(OpNode(nid, OpKind.RELU, (src,), img(c, h)))
+        return f"{nid}:0"
+
+    x, h = conv("stem.conv", "x:0", 3, 64, 7, 2, 3, image)
+    x = relu("stem.relu", bn("stem.bn", x, 64, h), 64, h)
+    hp = (h + 2 - 3) // 2 + 1
+    nodes.append(OpNode("stem.pool", OpKind.MAX_POOL2D, (x,), img(64, hp),
+                        attrs={"kernel": 3, "stride": 2, "padding": 1}))
+    x, h, cin = "stem.pool:0", hp, 64
+    for li, (nblocks, planes) in enumerate(zip(layers[:stages], (64, 128, 256, 512))):
+        width = planes * width_per_group // 64 * groups
+        cout = planes * 4
+        for bi in range(nblocks):
+            p = f"l{li + 1}.b{bi}"
+            stride = 2 if (bi == 0 and li > 0) else 1
+            y, h1 = conv(f"{p}.conv1", x, cin, width, 1, 1, 0, h)
+            y = relu(f"{p}.relu1", bn(f"{p}.bn1", y, width, h1), width, h1)
+            y, h2 = conv(f"{p}.conv2", y, width, width, 3, stride, 1, h1, g=groups)
+            y = relu(f"{p}.relu2", bn(f"{p}.bn2", y, width, h2), width, h2)
+            y, h3 = conv(f"{p}.conv3", y, width, cout, 1, 1, 0, h2)
+            y = bn(f"{p}.bn3", y, cout, h3)
+            if bi == 0:
+                sc, _ = conv(f"{p}.down", x, cin, cout, 1, stride, 0, h)
+                sc = bn(f"{p}.down_bn", sc, cout, h3)
+            else:
+                sc = x
+            nodes.append(OpNode(f"{p}.add", OpKind.ADD, (y, sc), img(cout, h3)))
+            x = relu(f"{p}.relu3", f"{p}.add:0", cout, h3)
+            h, cin = h3, cout
+    nodes.append(OpNode("pool", OpKind.MEAN_POOL2D, (x,), img(cin, 1),
+                        attrs={"kernel": h, "stride": h}))
+    g = Graph(tuple(nodes), {"x": img(3, image)}, ("pool:0",),
+              metadata={"model": "resnext50_32x4d" if groups > 1 else "resnet50",
+                        "batch": batch, "dtype": dtype})
+    return g, plan
+
+
+def fc_head(in_spec: TensorSpec, width: int, *, seed: int) -> tuple[Graph, WeightStore]:
+    """Per-task CNN classifier: (B, C, 1, 1) -> Reshape (B, C) -> Linear."""
+    dt = in_spec.dtype
+    b, c = in_spec.dims[0], in_spec.dims[1]
+    nodes = (OpNode("flat", OpKind.RESHAPE, ("feat:0",), _spec(dt, b, c), attrs={"dims": [b, c]}),
+             OpNode("fc", OpKind.MATMUL, ("flat:0",), _spec(dt, b, width),
+                    weights=("fc.w", "fc.b")))
+    plan = [("fc.w", (c, width), f"fan:{c}"), ("fc.b", (width,), f"fan:{c}")]
+    rng = np.random.default_rng([seed, 2, width])
+    store = WeightStore({n: TensorValue(TensorSpec(dt, dims), _materialize(
+        _draw(rng, dims, draw, False), dt)) for n, dims, draw in plan})
+    return Graph(nodes, {"feat": in_spec}, ("fc:0",)), store
+
+
 _BUILDERS: dict[str, Callable[[int, str], tuple[Graph, WeightPlan]]] = {
+    "resnet50": lambda b, d: _resnet(b, d),
+    "resnext50_32x4d": lambda b, d: _resnet(b, d, groups=32, width_per_group=4),
+    # reduced variants for fast tests: one bottleneck per stage at 64x64
+    "resnet-mini": lambda b, d: _resnet(b, d, layers=(1, 1, 1, 1), image=64),
+    "resnext-mini": lambda b, d: _resnet(b, d, groups=32, width_per_group=4, layers=(1, 1, 1, 1),
+                                         image=64),
     "ffnn": _ffnn,
     "cnnblock": _cnnblock,
     "attnblock": _attnblock,

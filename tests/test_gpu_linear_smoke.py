@@ -32,10 +32,10 @@ def test_tc_linear_bf16_vs_torch(G, T, K, N, act):
     y = torch.empty(G, T, N, device=dev, dtype=torch.bfloat16)
     _call_linear(x, w, b, r, y, act, _lib.NF_MODE_FAST, _lib.NF_BF16)
     torch.cuda.synchronize()
-    ref = torch.einsum("gtk,gnk->gtn", x.float(), w.float()) + b[:, None, :]
+    # epilogue contract: y = act(x @ W + bias + residual)
+    ref = torch.einsum("gtk,gnk->gtn", x.float(), w.float()) + b[:, None, :] + r.float()
     if act == _lib.NF_ACT_GELU:
         ref = torch.nn.functional.gelu(ref)
-    ref = ref + r.float()
     err = (y.float() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 2e-2, err
 
