@@ -271,7 +271,99 @@ __global__ void k_attention_simt(const T* __restrict__ qkv, T* __restrict__ out,
   }
 }
 
+// XLNet relative attention (attn_type "bi", no segments / mask): warp per
+// (sequence, head, query i), online softmax over keys j of
+//   score = ((q + r_w_bias) . k_j + (q + r_r_bias) . kr_{S - i + j}) * scale
+// where kr = the projected positional keys (2S rows per sequence) and the
+// index S - i + j is transformers' rel_shift_bnij. Biases are per instance:
+// sequence b belongs to instance b / seqs_per_bias.
+template <typename T>
+__global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restrict__ r,
+                                     const float* __restrict__ rwb, const float* __restrict__ rrb,
+                                     T* __restrict__ out, int64_t Bt, int S, int H, int dh,
+                                     int seqs_per_bias, float scale) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t D = int64_t(H) * dh;
+  const int64_t units = Bt * H * S;
+  for (int64_t u = w; u < units; u += nw) {
+    const int i = int(u % S);
+    const int h = int((u / S) % H);
+    const int64_t b = u / (int64_t(S) * H);
+    const int64_t inst = b / seqs_per_bias;
+    const T* base = qkv + b * S * 3 * D;
+    const T* rb = r + b * 2 * S * D + int64_t(h) * dh;
+    const T* q = base + int64_t(i) * 3 * D + int64_t(h) * dh;
+    const float* bw = rwb + (inst * H + h) * dh;
+    const float* br = rrb + (inst * H + h) * dh;
+    float qw[4], qr[4], acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int d = lane + 32 * e;
+      const float qv = d < dh ? to_f32(q[d]) : 0.f;
+      qw[e] = d < dh ? qv + bw[d] : 0.f;
+      qr[e] = d < dh ? qv + br[d] : 0.f;
+      acc[e] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < S; ++j) {
+      const T* k = base + int64_t(j) * 3 * D + D + int64_t(h) * dh;
+      const T* v = k + D;
+      const T* kr = rb + int64_t(S - i + j) * D;
+      float dot = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int d = lane + 32 * e;
+        if (d < dh) dot += qw[e] * to_f32(k[d]) + qr[e] * to_f32(kr[d]);
+      }
+      dot = warp_sum(dot) * scale;
+      const float mn = fmaxf(m, dot);
+      const float corr = expf(m - mn);
+      const float p = expf(dot - mn);
+      l = l * corr + p;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int d = lane + 32 * e;
+        acc[e] = acc[e] * corr + (d < dh ? p * to_f32(v[d]) : 0.f);
+      }
+      m = mn;
+    }
+    T* o = out + (b * S + i) * D + int64_t(h) * dh;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int d = lane + 32 * e;
+      if (d < dh) o[d] = from_f32<T>(acc[e] / l);
+    }
+  }
+}
+
 }  // namespace
+
+int rel_attention(const void* qkv, const void* r, const float* rwb, const float* rrb, void* out,
+                  int64_t Bt, int64_t S, int64_t H, int64_t dh, int64_t seqs_per_bias,
+                  float scale, int dtype, int mode, cudaStream_t stream) {
+  (void)mode;
+  if (Bt < 1 || S < 1 || H < 1 || dh < 1 || seqs_per_bias < 1 || Bt % seqs_per_bias)
+    return NF_ERR_SHAPE;
+  if (dh > 128) return NF_ERR_UNSUPPORTED;
+  const int64_t warps = Bt * H * S;
+  int64_t blocks = (warps * 32 + 255) / 256;
+  if (blocks > int64_t(kNumSMs) * 32) blocks = int64_t(kNumSMs) * 32;
+  if (dtype == NF_F32)
+    launch_pdl(k_rel_attention_simt<float>, dim3(unsigned(blocks)), dim3(256), 0, stream,
+               static_cast<const float*>(qkv), static_cast<const float*>(r), rwb, rrb,
+               static_cast<float*>(out), Bt, int(S), int(H), int(dh), int(seqs_per_bias), scale);
+  else if (dtype == NF_BF16)
+    launch_pdl(k_rel_attention_simt<__nv_bfloat16>, dim3(unsigned(blocks)), dim3(256), 0, stream,
+               static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(r), rwb,
+               rrb, static_cast<__nv_bfloat16*>(out), Bt, int(S), int(H), int(dh),
+               int(seqs_per_bias), scale);
+  else
+    return NF_ERR_UNSUPPORTED;
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
 
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
               float scale, int dtype, int mode, cudaStream_t stream) {

@@ -723,6 +723,8 @@ class Plan:
             return self._linear(node, ins[0], weights, act_user)
         if k is OpKind.ATTENTION:
             return self._attention(node, ins[0])
+        if k is OpKind.REL_ATTENTION:
+            return self._rel_attention(node, ins[0], ins[1], weights)
         if k in (OpKind.LAYER_NORM, OpKind.GROUP_NORM):
             return self._norm(node, ins[0], weights)
         if k in (OpKind.ADD, OpKind.MUL, OpKind.RELU, OpKind.TANH, OpKind.GELU):
@@ -811,6 +813,27 @@ class Plan:
         xp, yp, dcode, mcode = x.data_ptr(), y.data_ptr(), K.dtype_code(x), self.mcode
         self._emit(node.id, lambda st: _lib.call("nf_attention", xp, yp, bt, s, heads, dh,
                                                  float(scale), dcode, mcode, st))
+        return DVal(y, node.output_spec.dims)
+
+    def _rel_attention(self, node, v, rv, weights):
+        x = self._materialize(node.id, v)
+        r = self._materialize(node.id, rv)
+        heads = node.attrs["heads"]
+        d = x.shape[-1] // 3
+        dh = d // heads
+        s = x.shape[-2]
+        bt = x.numel() // (s * 3 * d)
+        rw = self._w(weights, node.weights[0], "vec_f32", x.dtype).reshape(-1, heads, dh)
+        rr = self._w(weights, node.weights[1], "vec_f32", x.dtype).reshape(-1, heads, dh)
+        if bt % rw.shape[0]:
+            raise ShapeError("bias instances do not divide the sequences")
+        y = self._alloc(node.output_spec.dims, x.dtype)
+        scale = node.attrs.get("scale") or 1.0 / math.sqrt(dh)
+        xp, rp, yp = x.data_ptr(), r.data_ptr(), y.data_ptr()
+        wp, bp, spb = rw.data_ptr(), rr.data_ptr(), bt // rw.shape[0]
+        dcode, mcode = K.dtype_code(x), self.mcode
+        self._emit(node.id, lambda st: _lib.call("nf_rel_attention", xp, rp, wp, bp, yp, bt, s,
+                                                 heads, dh, spb, float(scale), dcode, mcode, st))
         return DVal(y, node.output_spec.dims)
 
     def _norm(self, node, v, weights):

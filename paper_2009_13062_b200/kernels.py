@@ -266,6 +266,30 @@ def attention(qkv: torch.Tensor, *, heads: int, scale: float | None = None,
     return y
 
 
+def rel_attention(qkv: torch.Tensor, r: torch.Tensor, r_w_bias: torch.Tensor,
+                  r_r_bias: torch.Tensor, *, heads: int, scale: float | None = None,
+                  mode: str = "fast") -> torch.Tensor:
+    """XLNet relative attention; biases (H, dh) or per instance (M, H, dh)
+    with qkv (M, ..., S, 3D)."""
+    _cuda(qkv, r, r_w_bias, r_r_bias)
+    d = qkv.shape[-1] // 3
+    s = qkv.shape[-2]
+    dh = d // heads
+    if qkv.shape[-1] != 3 * d or r.shape[-1] != d or r.shape[-2] != 2 * s or d % heads:
+        raise ShapeError(f"rel attention operands {tuple(qkv.shape)} / {tuple(r.shape)}")
+    bt = qkv.numel() // (s * 3 * d)
+    rw = _f32(r_w_bias).reshape(-1, heads, dh)
+    rr = _f32(r_r_bias).reshape(-1, heads, dh)
+    if bt % rw.shape[0]:
+        raise ShapeError("bias instances do not divide the sequences")
+    y = torch.empty(qkv.shape[:-1] + (d,), dtype=qkv.dtype, device=qkv.device)
+    sc = 1.0 / math.sqrt(dh) if scale is None else scale
+    _lib.call("nf_rel_attention", qkv.contiguous().data_ptr(), r.contiguous().data_ptr(),
+              rw.data_ptr(), rr.data_ptr(), y.data_ptr(), bt, s, heads, dh, bt // rw.shape[0],
+              float(sc), dtype_code(qkv), _MODES[mode], stream_ptr())
+    return y
+
+
 # ---------------------------------------------------------------------------
 # Layout
 # ---------------------------------------------------------------------------

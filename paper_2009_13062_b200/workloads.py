@@ -174,6 +174,76 @@ def _bert(batch: int, dtype: str, cfg: BertConfig = BERT_BASE) -> tuple[Graph, W
     return g, plan
 
 
+@dataclass(frozen=True)
+class XLNetConfig:
+    layers: int = 12
+    hidden: int = 768
+    heads: int = 12
+    ffn: int = 3072
+    seq: int = 128
+    eps: float = 1e-12
+
+
+XLNET_BASE = XLNetConfig()
+
+
+def _xlnet(batch: int, dtype: str, cfg: XLNetConfig = XLNET_BASE) -> tuple[Graph, WeightPlan]:
+    """XLNet-base encoder (attn_type "bi", no memory / segments / masks) on
+    (B, S, 768) embeddings plus the sinusoidal relative positional embedding
+    input ``pos`` (B, 2S, 768). Per layer (transformers XLNetLayer): fused
+    q|k|v projection (no bias), positional-key projection r, relative
+    attention with per-instance r_w_bias / r_r_bias, output projection o (no
+    bias), Add + LayerNorm, FF1 + GELU + FF2, Add + LayerNorm."""
+    b, s, d, f, h = batch, cfg.seq, cfg.hidden, cfg.ffn, cfg.heads
+    dh = d // h
+    tok, qkv, wide = _spec(dtype, b, s, d), _spec(dtype, b, s, 3 * d), _spec(dtype, b, s, f)
+    rsp = _spec(dtype, b, 2 * s, d)
+    nodes: list[OpNode] = []
+    plan: WeightPlan = []
+    x = "x:0"
+    for i in range(cfg.layers):
+        p = f"l{i:02d}"
+        nodes += [
+            OpNode(f"{p}.qkv", OpKind.MATMUL, (x,), qkv, weights=(f"{p}.qkv.w",)),
+            OpNode(f"{p}.r", OpKind.MATMUL, ("pos:0",), rsp, weights=(f"{p}.r.w",)),
+            OpNode(f"{p}.attn", OpKind.REL_ATTENTION, (f"{p}.qkv:0", f"{p}.r:0"), tok,
+                   weights=(f"{p}.rwb", f"{p}.rrb"), attrs={"heads": h}),
+            OpNode(f"{p}.proj", OpKind.MATMUL, (f"{p}.attn:0",), tok, weights=(f"{p}.o.w",)),
+            OpNode(f"{p}.res1", OpKind.ADD, (f"{p}.proj:0", x), tok),
+            OpNode(f"{p}.ln1", OpKind.LAYER_NORM, (f"{p}.res1:0",), tok,
+                   weights=(f"{p}.ln1.g", f"{p}.ln1.b"), attrs={"eps": cfg.eps}),
+            OpNode(f"{p}.ff1", OpKind.MATMUL, (f"{p}.ln1:0",), wide,
+                   weights=(f"{p}.ff1.w", f"{p}.ff1.b")),
+            OpNode(f"{p}.gelu", OpKind.GELU, (f"{p}.ff1:0",), wide),
+            OpNode(f"{p}.ff2", OpKind.MATMUL, (f"{p}.gelu:0",), tok,
+                   weights=(f"{p}.ff2.w", f"{p}.ff2.b")),
+            OpNode(f"{p}.res2", OpKind.ADD, (f"{p}.ff2:0", f"{p}.ln1:0"), tok),
+            OpNode(f"{p}.ln2", OpKind.LAYER_NORM, (f"{p}.res2:0",), tok,
+                   weights=(f"{p}.ln2.g", f"{p}.ln2.b"), attrs={"eps": cfg.eps}),
+        ]
+        plan += [(f"{p}.qkv.w", (d, 3 * d), f"fan:{d}"), (f"{p}.r.w", (d, d), f"fan:{d}"),
+                 (f"{p}.rwb", (h, dh), f"fan:{dh}"), (f"{p}.rrb", (h, dh), f"fan:{dh}"),
+                 (f"{p}.o.w", (d, d), f"fan:{d}"),
+                 (f"{p}.ln1.g", (d,), "gamma"), (f"{p}.ln1.b", (d,), "beta"),
+                 (f"{p}.ff1.w", (d, f), f"fan:{d}"), (f"{p}.ff1.b", (f,), f"fan:{d}"),
+                 (f"{p}.ff2.w", (f, d), f"fan:{f}"), (f"{p}.ff2.b", (d,), f"fan:{f}"),
+                 (f"{p}.ln2.g", (d,), "gamma"), (f"{p}.ln2.b", (d,), "beta")]
+        x = f"{p}.ln2:0"
+    g = Graph(tuple(nodes), {"x": tok, "pos": rsp}, (x,),
+              metadata={"model": "xlnet-base", "batch": batch, "dtype": dtype,
+                        "layers": cfg.layers, "sinusoid_inputs": ["pos"]})
+    return g, plan
+
+
+def relative_positional_embedding(seq: int, d_model: int) -> np.ndarray:
+    """transformers XLNetModel.relative_positional_encoding, attn_type "bi",
+    klen = qlen = seq: positions seq, seq-1, ..., -seq+1; [sin | cos]."""
+    inv_freq = 1.0 / np.power(10000.0, np.arange(0, d_model, 2.0) / d_model)
+    pos_seq = np.arange(seq, -seq, -1.0)
+    inp = np.outer(pos_seq, inv_freq)
+    return np.concatenate([np.sin(inp), np.cos(inp)], axis=-1)
+
+
 def bert_layers(n: int) -> Callable[[int, str], tuple[Graph, WeightPlan]]:
     """BERT builder truncated to ``n`` layers (tests; oracle sampling)."""
     cfg = BertConfig(layers=n)
@@ -272,6 +342,8 @@ _BUILDERS: dict[str, Callable[[int, str], tuple[Graph, WeightPlan]]] = {
     "attnblock": _attnblock,
     "bert-base": _bert,
     "bert-2l": bert_layers(2),
+    "xlnet-base": _xlnet,
+    "xlnet-2l": lambda b, d: _xlnet(b, d, XLNetConfig(layers=2)),
 }
 
 MODEL_NAMES = tuple(_BUILDERS)
@@ -342,9 +414,14 @@ def build_zoo(name: str, *, batch: int = 1, dtype: str = "f32", seed: int = 0,
 def model_inputs(graph: Graph, *, seed: int = 0, model: int = 0) -> dict[str, TensorValue]:
     """Seeded inputs for one model, U[-1, 1] (zoo.py:173-184)."""
     rng = np.random.default_rng([seed, 1, model])
+    fixed = set(graph.metadata.get("sinusoid_inputs", ()))
     out = {}
     for name, spec in graph.graph_inputs.items():
-        arr = rng.uniform(-1.0, 1.0, size=spec.dims)
+        if name in fixed:  # deterministic positional input, same for every model
+            emb = relative_positional_embedding(spec.dims[-2] // 2, spec.dims[-1])
+            arr = np.broadcast_to(emb, spec.dims)
+        else:
+            arr = rng.uniform(-1.0, 1.0, size=spec.dims)
         out[name] = TensorValue(spec, _materialize(arr, spec.dtype))
     return out
 

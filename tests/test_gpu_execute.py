@@ -106,3 +106,15 @@ def test_plan_replay_is_deterministic_and_graph_capturable():
     torch.cuda.synchronize()
     for x, y in zip(a, plan.outputs()):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("dtype,tol", [("bf16", 2e-2), ("f32", 1e-4)])
+def test_xlnet_2layer_merged_vs_oracle(dtype, tol):
+    graph, stores = W.build_zoo("xlnet-2l", num_models=3, batch=1, dtype=dtype)
+    inputs = [model_inputs(graph, seed=0, model=j) for j in range(3)]
+    merged, mstore = merge(graph, stores)
+    outs, _ = execute(merged.graph, mstore, merged.bind_inputs(inputs))
+    per = merged.slice_outputs(outs)
+    for j in range(3):
+        want = OX.execute(graph, stores[j].tensors, inputs[j])[0]
+        assert normwise(per[j][0].numpy(), want) < tol

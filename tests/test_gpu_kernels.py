@@ -175,3 +175,18 @@ def test_shape_errors_surface():
                           torch.zeros(4, 1, 1, 1, device="cuda"), groups=3)
     with pytest.raises(ShapeError):
         GK.max_pool2d(torch.zeros(1, 1, 5, 5, device="cuda"), kernel=2, stride=2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_rel_attention_vs_oracle(dtype):
+    rng = np.random.default_rng(4)
+    M, B, S, H, dh = 3, 2, 33, 4, 64
+    qkv = rng.uniform(-1, 1, (M, B, S, 3 * H * dh)).astype(np.float32)
+    r = rng.uniform(-1, 1, (M, B, 2 * S, H * dh)).astype(np.float32)
+    rw = rng.uniform(-.3, .3, (M, H, dh)).astype(np.float32)
+    rr = rng.uniform(-.3, .3, (M, H, dh)).astype(np.float32)
+    if dtype == torch.bfloat16:
+        qkv, r = OK.bf16_round(qkv), OK.bf16_round(r)
+    want = np.stack([OK.rel_attention(qkv[m], r[m], rw[m], rr[m], heads=H) for m in range(M)])
+    got = host(GK.rel_attention(cuda(qkv, dtype), cuda(r, dtype), cuda(rw), cuda(rr), heads=H))
+    assert normwise(got, want) < (2e-2 if dtype == torch.bfloat16 else 1e-5)

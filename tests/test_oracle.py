@@ -136,3 +136,36 @@ def test_oracle_vs_live_reference_random():
         xm = rng.uniform(-1, 1, (g, 5, 33)).astype(np.float32)
         wm = rng.uniform(-.5, .5, (g, 33, 9)).astype(np.float32)
         assert OK.batch_matmul(xm, wm).tobytes() == E.batch_matmul(xm, wm).tobytes()
+
+
+def test_rel_attention_oracle_matches_transformers_xlnet():
+    """The unpinned XLNet restatement vs transformers' rel_attn_core (f64)."""
+    import torch
+    from transformers import XLNetConfig
+    from transformers.models.xlnet import modeling_xlnet as X
+    torch.manual_seed(0)
+    att = X.XLNetRelativeAttention(XLNetConfig(d_model=64, n_head=4, d_inner=128)).eval().double()
+    for p in att.parameters():
+        torch.nn.init.uniform_(p, -0.5, 0.5)
+    S, B, H, dh = 9, 2, 4, 16
+    q, k, v = (torch.rand(S, B, H, dh, dtype=torch.float64) - .5 for _ in range(3))
+    kr = torch.rand(2 * S, B, H, dh, dtype=torch.float64) - .5
+    with torch.no_grad():
+        ref = att.rel_attn_core(q, k, v, kr)
+    ref = ref[0] if isinstance(ref, tuple) else ref
+    D = H * dh
+    qkv = torch.cat([t.permute(1, 0, 2, 3).reshape(B, S, D) for t in (q, k, v)], -1).numpy()
+    r = kr.permute(1, 0, 2, 3).reshape(B, 2 * S, D).numpy()
+    got = OK.rel_attention(qkv, r, att.r_w_bias.detach().numpy(), att.r_r_bias.detach().numpy(),
+                           heads=H)
+    np.testing.assert_allclose(got, ref.permute(1, 0, 2, 3).reshape(B, S, D).numpy(),
+                               rtol=1e-12, atol=1e-12)
+
+
+def test_relative_positional_embedding_matches_transformers():
+    import torch
+    from transformers import XLNetConfig, XLNetModel
+    from paper_2009_13062_b200.workloads import relative_positional_embedding
+    m = XLNetModel(XLNetConfig(d_model=32, n_head=2, d_inner=64, n_layer=1, attn_type="bi"))
+    ref = m.relative_positional_encoding(7, 7, bsz=1)[:, 0, :].numpy()
+    np.testing.assert_allclose(relative_positional_embedding(7, 32), ref, rtol=1e-6, atol=1e-6)
