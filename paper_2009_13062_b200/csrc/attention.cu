@@ -25,6 +25,22 @@ namespace nf {
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 
+#ifdef NF_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[64];
+#define NF_ATRACE(slot)                                                               \
+  do {                                                                                \
+    if (blockIdx.x == 0) {                                                            \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_attn_trace[(slot)] = t_;                                                      \
+    }                                                                                 \
+  } while (0)
+#else
+#define NF_ATRACE(slot) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kAttnS = 128;   // max keys / queries per CTA
@@ -106,6 +122,7 @@ __global__ void __launch_bounds__(128, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tid == 0) NF_ATRACE(0);
   const uint32_t tmem_s = tmem;        // columns [0, 128): scores
   const uint32_t tmem_o = tmem + 128;  // columns [128, 192): context
 
@@ -118,6 +135,7 @@ __global__ void __launch_bounds__(128, 2)
   }
   grid_dependents_launch();
   mbar_wait(bar_load, 0);
+  if (tid == 0) NF_ATRACE(1);
 
   if (tid == 0) {
     tc_fence_after();
@@ -133,39 +151,61 @@ __global__ void __launch_bounds__(128, 2)
   // Softmax over this thread's query row (TMEM lane = tid).
   mbar_wait(bar_s, 0);
   tc_fence_after();
+  if (tid == 0) NF_ATRACE(2);
   float mx = -INFINITY;
-  uint32_t r[4][32];
+  uint32_t r[4][32];  // this query row's 128 scores
 #pragma unroll
   for (int c = 0; c < 4; ++c)
     tmem_ld_32x32b_x32(tmem_s + (uint32_t(warp * 32) << 16) + uint32_t(c * 32), r[c]);
   tmem_ld_wait();
+  if (tid == 0) NF_ATRACE(10);
+  // Branch-free: out-of-range keys (S < 128) are masked to -inf by select,
+  // so every exp is independent straight-line code the scheduler can overlap.
+  {
+    float m8[8];
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
+    for (int q = 0; q < 8; ++q) m8[q] = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (c * 32 + j < S) mx = fmaxf(mx, __uint_as_float(r[c][j]));
-  float sum = 0.f;
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float v = __uint_as_float(r[c][j]);
+        m8[j & 7] = fmaxf(m8[j & 7], (c * 32 + j < S) ? v : -INFINITY);
+      }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mx = fmaxf(mx, m8[q]);
+  }
+  if (tid == 0) NF_ATRACE(11);
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
   const uint32_t prow = smem_u32(sP);
+  const float mxs = mx * scale_log2;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    float p[32];
+    uint32_t pk[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float v = (c * 32 + j < S) ? exp2f((__uint_as_float(r[c][j]) - mx) * scale_log2) : 0.f;
-      // Round to the bf16 operand value before summing so the normaliser
-      // matches the probabilities the PV MMA actually consumes.
-      p[j] = __bfloat162float(__float2bfloat16_rn(v));
-      sum += p[j];
+    for (int j = 0; j < 32; j += 2) {
+      const float x0 = (c * 32 + j < S) ? fmaf(__uint_as_float(r[c][j]), scale_log2, -mxs)
+                                        : -INFINITY;
+      const float x1 = (c * 32 + j + 1 < S)
+                           ? fmaf(__uint_as_float(r[c][j + 1]), scale_log2, -mxs)
+                           : -INFINITY;
+      // Probabilities are rounded to the bf16 values the PV MMA consumes and
+      // the normaliser sums exactly those values.
+      const uint32_t packed = pack_bf16x2(ex2_approx(x0), ex2_approx(x1));
+      s4[(j >> 1) & 3] += __uint_as_float(packed << 16) + __uint_as_float(packed & 0xffff0000u);
+      pk[j >> 1] = packed;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      st_shared_v4(prow + kmajor_off(tid, c * 32 + q * 8, 128), pack_bf16x2(p[8 * q], p[8 * q + 1]),
-                   pack_bf16x2(p[8 * q + 2], p[8 * q + 3]), pack_bf16x2(p[8 * q + 4], p[8 * q + 5]),
-                   pack_bf16x2(p[8 * q + 6], p[8 * q + 7]));
+      st_shared_v4(prow + kmajor_off(tid, c * 32 + q * 8, 128), pk[4 * q], pk[4 * q + 1],
+                   pk[4 * q + 2], pk[4 * q + 3]);
   }
+  const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  if (tid == 0) NF_ATRACE(12);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) NF_ATRACE(3);
 
   if (tid == 0) {
     tc_fence_after();
@@ -183,6 +223,7 @@ __global__ void __launch_bounds__(128, 2)
   }
   mbar_wait(bar_o, 0);
   tc_fence_after();
+  if (tid == 0) NF_ATRACE(4);
   {
     uint32_t o[2][32];
     tmem_ld_32x32b_x32(tmem_o + (uint32_t(warp * 32) << 16), o[0]);
@@ -207,6 +248,7 @@ __global__ void __launch_bounds__(128, 2)
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) NF_ATRACE(5);
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);

@@ -65,6 +65,13 @@ NF_DEVICE float act_t(float v) {
   else return v;
 }
 
+// 2^x, flush-to-zero approximate (MUFU.EX2, one instruction).
+NF_DEVICE float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 NF_DEVICE float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

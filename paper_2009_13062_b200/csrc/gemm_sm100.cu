@@ -34,6 +34,9 @@ constexpr int kGemmBK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int kGemmThreads = 192;
 constexpr int kOutBlock = 64;  // features per 128-byte output block (bf16)
 constexpr int kMaxSplits = 8;
+#ifndef NF_GEMM_BUDGET_KB
+#define NF_GEMM_BUDGET_KB 220  // smem for the operand ring + output staging
+#endif
 constexpr int64_t kCounterBytes = 64 * 1024;  // semaphores at the workspace head
 
 #ifdef NF_GEMM_TRACE
@@ -72,7 +75,8 @@ struct GemmCfg {
   static constexpr int kBBytes = BN * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = kGemmBM * BN * 2;
-  static constexpr int kStages = (220 * 1024 - kOutBytes) / kStageBytes;
+  static constexpr int kStages =
+      ((BN >= 256 ? 220 : NF_GEMM_BUDGET_KB) * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
   static constexpr size_t kBytes =
       1024 + size_t(kStages) * kStageBytes + kOutBytes + 256;

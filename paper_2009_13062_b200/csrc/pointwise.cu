@@ -171,15 +171,14 @@ constexpr int kNormCache = 32;  // fp32 values cached per lane
 // group; the per-channel affine (a weight, independent of the producer grid)
 // is fetched before the programmatic-dependency wait so its latency hides
 // behind the previous kernel's tail.
-template <typename T>
-__global__ void __launch_bounds__(256) k_group_norm_vec(const T* __restrict__ x,
+template <typename T, int Q>
+__global__ void __launch_bounds__(256, 2) k_group_norm_vec(const T* __restrict__ x,
                                                         const T* __restrict__ res,
                                                         const float* __restrict__ gamma,
                                                         const float* __restrict__ beta,
                                                         T* __restrict__ y, NormGeom g) {
   grid_dependents_launch();
-  constexpr int V = Vec8<T>::N;
-  constexpr int Q = kNormCache / V;  // chunks per lane
+  constexpr int V = Vec8<T>::N;  // Q = 16-byte chunks per lane (ceil(Cg / (32 V)))
   const int lane = threadIdx.x & 31;
   const int warp_id = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = int((int64_t(gridDim.x) * blockDim.x) >> 5);
@@ -194,7 +193,7 @@ __global__ void __launch_bounds__(256) k_group_norm_vec(const T* __restrict__ x,
     const int64_t base = int64_t(r1) * g.s1 + int64_t(r2) * g.s2 + int64_t(grp) * g.sg;
     const int64_t aff = (g.rows_per_affine > 0 ? int64_t(row / int(g.rows_per_affine)) : 0) *
                             g.G * g.Cg + int64_t(grp) * Cg;
-    float ga[kNormCache], be[kNormCache];
+    float ga[Q * V], be[Q * V];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int ch = lane + 32 * q;
@@ -214,7 +213,7 @@ __global__ void __launch_bounds__(256) k_group_norm_vec(const T* __restrict__ x,
       grid_dependency_wait();
       waited = true;
     }
-    float v[kNormCache];
+    float v[Q * V];
     uint4 ux[Q], ur[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -324,7 +323,11 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     auto* px = static_cast<const __nv_bfloat16*>(x);
     auto* pr = static_cast<const __nv_bfloat16*>(residual);
     auto* py = static_cast<__nv_bfloat16*>(y);
-    if (vec) launch_pdl(k_group_norm_vec<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    const int q = int((g.Cg / 8 + 31) / 32);
+    if (vec && q == 1) launch_pdl(k_group_norm_vec<__nv_bfloat16, 1>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else if (vec && q == 2) launch_pdl(k_group_norm_vec<__nv_bfloat16, 2>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else if (vec && q == 3) launch_pdl(k_group_norm_vec<__nv_bfloat16, 3>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else if (vec) launch_pdl(k_group_norm_vec<__nv_bfloat16, 4>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else launch_pdl(k_group_norm<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else if (dtype == NF_F32) {
     const bool vec = small && g.sc == 1 && g.Cg % 4 == 0 && g.Cg <= 4 * 32 * (kNormCache / 4) &&
@@ -332,7 +335,10 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     auto* px = static_cast<const float*>(x);
     auto* pr = static_cast<const float*>(residual);
     auto* py = static_cast<float*>(y);
-    if (vec) launch_pdl(k_group_norm_vec<float>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    const int q = int((g.Cg / 4 + 31) / 32);
+    if (vec && q == 1) launch_pdl(k_group_norm_vec<float, 1>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else if (vec && q <= 4) launch_pdl(k_group_norm_vec<float, 4>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    else if (vec) launch_pdl(k_group_norm_vec<float, 8>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else launch_pdl(k_group_norm<float>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else {
     return NF_ERR_UNSUPPORTED;
