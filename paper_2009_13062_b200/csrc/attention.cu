@@ -381,15 +381,315 @@ __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// XLNet relative attention on the tensor cores (bf16, dh == 64, S == 128).
+// One CTA per (sequence, head), 128 threads, thread = query row i:
+//   AC  = Q K^T                      tcgen05 -> TMEM cols [0,128) -> registers
+//   raw = Q KR^T (KR = 2S = 256 rows) tcgen05 -> TMEM cols [0,256)
+//   score[i][j] = (AC + bw[j] + raw[i][S-i+j] + cr[S-i+j]) * scale
+// where bw[j] = r_w_bias . k_j and cr[p] = r_r_bias . kr_p (fp32 dot
+// products, so (q + bias) is never rounded to bf16). The rel-shift
+// raw[i][S-i+j] differs per TMEM lane; each warp stages a 32 x 64 window of
+// raw through a padded smem buffer (pitch 68 words: 128-bit stores and the
+// skewed scalar reads are both bank-conflict free) and reads it back
+// diagonally. P overwrites KR's smem once the raw MMA retired; O = P V
+// reuses TMEM cols [0,64). 256 TMEM cols + ~86 KB smem -> 2 CTAs per SM.
+// ---------------------------------------------------------------------------
+constexpr int kRelPitch = 68;                           // words per staged row
+constexpr int kRelStageBytes = 4 * 32 * kRelPitch * 4;  // 34816 B (4 warps)
+constexpr size_t kRelSmem = 1024 + 2 * kTileBytes + 4096 + kTileBytes + 2 * kTileBytes +
+                            (128 + 256 + 128) * 4 + 64;
+
+// positional keys r viewed as 4-D (dh, H, 2S, Bt); box (64, 1, 128, 1).
+bool make_r_map(CUtensorMap* map, const void* r, int64_t Bt, int64_t S, int64_t H) {
+  EncodeTiledFn fn = encode_fn_attn();
+  if (!fn) return false;
+  const int64_t D = H * kAttnD;
+  cuuint64_t dims[4] = {cuuint64_t(kAttnD), cuuint64_t(H), cuuint64_t(2 * S), cuuint64_t(Bt)};
+  cuuint64_t strides[3] = {cuuint64_t(kAttnD * 2), cuuint64_t(D * 2), cuuint64_t(2 * S * D * 2)};
+  cuuint32_t box[4] = {kAttnD, 1, kAttnS, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(r), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp32 dot of a (64-element, fp32) bias vector with row `row` of a K-major
+// SWIZZLE_128B bf16 tile.
+__device__ __forceinline__ float bias_dot_row(const uint8_t* tile, int row, const float* bias) {
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 u = *reinterpret_cast<const uint4*>(tile + row * 128 + ((c ^ (row & 7)) << 4));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc = fmaf(__uint_as_float(w[e] << 16), bias[c * 8 + 2 * e], acc);
+      acc = fmaf(__uint_as_float(w[e] & 0xffff0000u), bias[c * 8 + 2 * e + 1], acc);
+    }
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(128, 2)
+    k_rel_attention_tc(const __grid_constant__ CUtensorMap map_qkv,
+                       const __grid_constant__ CUtensorMap map_r, const float* __restrict__ rwb,
+                       const float* __restrict__ rrb, __nv_bfloat16* __restrict__ out, int H,
+                       int seqs_per_bias, float scale_log2) {
+  constexpr int S = kAttnS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTileBytes;
+  uint8_t* sStage = sQ;  // Q | K | 4 KB pad, reused after the raw MMA retired
+  uint8_t* sV = sK + kTileBytes + 4096;
+  uint8_t* sKR = sV + kTileBytes;  // 256 rows; later P (128 x 128, 2 k-blocks)
+  float* sBw = reinterpret_cast<float*>(sKR + 2 * kTileBytes);
+  float* sCr = sBw + 128;
+  float* sRb = sCr + 256;  // r_w_bias | r_r_bias of this (instance, head)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sRb + 128);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_s = bars + 1;
+  uint64_t* bar_bd = bars + 2;
+  uint64_t* bar_o = bars + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int bt = blockIdx.x / H;
+  const int h = blockIdx.x % H;
+  const int inst = bt / seqs_per_bias;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&map_qkv);
+    tma_prefetch_desc(&map_r);
+    mbar_init(bar_load, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_bd, 1);
+    mbar_init(bar_o, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+
+  if (tid == 0) {
+    grid_dependency_wait();
+    mbar_arrive_expect_tx(bar_load, 5 * kTileBytes);
+    tma_load_4d(sQ, &map_qkv, bar_load, 0, h, 0, bt, kEvictFirst);
+    tma_load_4d(sK, &map_qkv, bar_load, 0, H + h, 0, bt, kEvictFirst);
+    tma_load_4d(sV, &map_qkv, bar_load, 0, 2 * H + h, 0, bt, kEvictFirst);
+    tma_load_4d(sKR, &map_r, bar_load, 0, h, 0, bt, kEvictFirst);
+    tma_load_4d(sKR + kTileBytes, &map_r, bar_load, 0, h, S, bt, kEvictFirst);
+  }
+  grid_dependents_launch();
+  const float* bw_src = rwb + (int64_t(inst) * H + h) * kAttnD;
+  const float* br_src = rrb + (int64_t(inst) * H + h) * kAttnD;
+  mbar_wait(bar_load, 0);
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 128);
+    const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK);
+#pragma unroll
+    for (int kk = 0; kk < kAttnD / 16; ++kk)
+      umma_f16_ss(tmem, make_sw128_kmajor_desc(qa + kk * 32),
+                  make_sw128_kmajor_desc(ka + kk * 32), idesc, kk != 0);
+    umma_commit(bar_s);
+  }
+  // bias . key rows (fp32) while the MMA runs.
+  if (tid < 32) {
+    sRb[tid] = __ldg(bw_src + tid);
+    sRb[tid + 32] = __ldg(bw_src + tid + 32);
+  } else if (tid < 64) {
+    sRb[tid + 32] = __ldg(br_src + tid - 32);
+    sRb[tid + 64] = __ldg(br_src + tid);
+  }
+  __syncthreads();
+  sBw[tid] = bias_dot_row(sK, tid, sRb);
+  sCr[tid] = bias_dot_row(sKR, tid, sRb + 64);
+  sCr[tid + 128] = bias_dot_row(sKR, tid + 128, sRb + 64);
+
+  mbar_wait(bar_s, 0);
+  tc_fence_after();
+  uint32_t r[4][32];  // AC row of this query
+#pragma unroll
+  for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + uint32_t(c * 32), r[c]);
+  tmem_ld_wait();
+  tc_fence_before();
+  __syncthreads();  // AC consumed by everyone; bias vectors visible
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 256);
+    const uint32_t qa = smem_u32(sQ), ra = smem_u32(sKR);
+#pragma unroll
+    for (int kk = 0; kk < kAttnD / 16; ++kk)
+      umma_f16_ss(tmem, make_sw128_kmajor_desc(qa + kk * 32),
+                  make_sw128_kmajor_desc(ra + kk * 32), idesc, kk != 0);
+    umma_commit(bar_bd);
+  }
+  // AC + bw, in log2 units (scale folded).
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      r[c][j] = __float_as_uint(__uint_as_float(r[c][j]) + sBw[c * 32 + j]);
+
+  mbar_wait(bar_bd, 0);
+  tc_fence_after();
+  // Rel-shift through the per-warp staging window.
+  const uint32_t stage_w = smem_u32(sStage) + uint32_t(warp * 32 * kRelPitch * 4);
+  const int i_row = warp * 32 + lane;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int p0 = 97 - 32 * warp + 32 * c;  // window start for lane 31, jj 0
+    const int base = p0 < 192 ? p0 : 192;
+    const int shift = 31 - lane + (p0 - base);
+    __syncwarp();  // previous chunk's reads of the window are done
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t wv[32];
+      tmem_ld_32x32b_x32(lane_base + uint32_t(base + 32 * half), wv);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        st_shared_v4(stage_w + uint32_t((lane * kRelPitch + 32 * half + 4 * q) * 4), wv[4 * q],
+                     wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+    }
+    __syncwarp();
+    const float* row = reinterpret_cast<const float*>(sStage + warp * 32 * kRelPitch * 4) +
+                       lane * kRelPitch + shift;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int p = S - i_row + c * 32 + jj;
+      r[c][jj] = __float_as_uint(__uint_as_float(r[c][jj]) + row[jj] + sCr[p]);
+    }
+  }
+  __syncwarp();
+
+  // Softmax over the row (all 128 keys valid).
+  float mx = -INFINITY;
+  {
+    float m8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m8[q] = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) m8[j & 7] = fmaxf(m8[j & 7], __uint_as_float(r[c][j]));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mx = fmaxf(mx, m8[q]);
+  }
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  uint8_t* sP = sKR;  // the raw MMA (last reader of KR) has retired
+  const uint32_t prow = smem_u32(sP);
+  const float mxs = mx * scale_log2;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const float x0 = fmaf(__uint_as_float(r[c][j]), scale_log2, -mxs);
+      const float x1 = fmaf(__uint_as_float(r[c][j + 1]), scale_log2, -mxs);
+      const uint32_t packed = pack_bf16x2(ex2_approx(x0), ex2_approx(x1));
+      s4[(j >> 1) & 3] += __uint_as_float(packed << 16) + __uint_as_float(packed & 0xffff0000u);
+      pk[j >> 1] = packed;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      st_shared_v4(prow + kmajor_off(tid, c * 32 + q * 8, 128), pk[4 * q], pk[4 * q + 1],
+                   pk[4 * q + 2], pk[4 * q + 3]);
+  }
+  const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();  // P complete; every raw TMEM read done
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64, 0, 1);
+    const uint32_t pa = smem_u32(sP), va = smem_u32(sV);
+#pragma unroll
+    for (int kk = 0; kk < kAttnS / 16; ++kk) {
+      const int blk = kk >> 2, sub = kk & 3;
+      umma_f16_ss(tmem, make_sw128_kmajor_desc(pa + blk * 128 * 128 + sub * 32),
+                  make_sw128_mnmajor_desc(va + kk * 16 * 128, 8192, 1024), idesc, kk != 0);
+    }
+    umma_commit(bar_o);
+  }
+  mbar_wait(bar_o, 0);
+  tc_fence_after();
+  {
+    uint32_t o[2][32];
+    tmem_ld_32x32b_x32(lane_base, o[0]);
+    tmem_ld_32x32b_x32(lane_base + 32, o[1]);
+    tmem_ld_wait();
+    const float inv = 1.0f / sum;
+    const int64_t D = int64_t(H) * kAttnD;
+    __nv_bfloat16* dst = out + (int64_t(bt) * S + tid) * D + int64_t(h) * kAttnD;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(o[c][8 * q]) * inv, __uint_as_float(o[c][8 * q + 1]) * inv);
+        u.y = pack_bf16x2(__uint_as_float(o[c][8 * q + 2]) * inv, __uint_as_float(o[c][8 * q + 3]) * inv);
+        u.z = pack_bf16x2(__uint_as_float(o[c][8 * q + 4]) * inv, __uint_as_float(o[c][8 * q + 5]) * inv);
+        u.w = pack_bf16x2(__uint_as_float(o[c][8 * q + 6]) * inv, __uint_as_float(o[c][8 * q + 7]) * inv);
+        *reinterpret_cast<uint4*>(dst + c * 32 + q * 8) = u;
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
 }  // namespace
 
 int rel_attention(const void* qkv, const void* r, const float* rwb, const float* rrb, void* out,
                   int64_t Bt, int64_t S, int64_t H, int64_t dh, int64_t seqs_per_bias,
                   float scale, int dtype, int mode, cudaStream_t stream) {
-  (void)mode;
   if (Bt < 1 || S < 1 || H < 1 || dh < 1 || seqs_per_bias < 1 || Bt % seqs_per_bias)
     return NF_ERR_SHAPE;
   if (dh > 128) return NF_ERR_UNSUPPORTED;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(r) |
+                       reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(rwb) |
+                       reinterpret_cast<uintptr_t>(rrb);
+  if (dtype == NF_BF16 && mode == NF_MODE_FAST && dh == kAttnD && S == kAttnS && (al & 15) == 0 &&
+      Bt * H <= (int64_t(1) << 31) - 1) {
+    CUtensorMap mq, mr;
+    if (!make_qkv_map(&mq, qkv, Bt, S, H) || !make_r_map(&mr, r, Bt, S, H)) return NF_ERR_LAUNCH;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaFuncSetAttribute(k_rel_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kRelSmem));
+      attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(Bt * H));
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = kRelSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled();
+    const float scale_log2 = scale * 1.4426950408889634f;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_rel_attention_tc, mq, mr, rwb, rrb,
+                                       static_cast<__nv_bfloat16*>(out), int(H),
+                                       int(seqs_per_bias), scale_log2);
+    return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+  }
   const int64_t warps = Bt * H * S;
   int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > int64_t(kNumSMs) * 32) blocks = int64_t(kNumSMs) * 32;

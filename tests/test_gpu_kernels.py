@@ -177,10 +177,12 @@ def test_shape_errors_surface():
         GK.max_pool2d(torch.zeros(1, 1, 5, 5, device="cuda"), kernel=2, stride=2)
 
 
-@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_rel_attention_vs_oracle(dtype):
+@pytest.mark.parametrize("dtype,S", [(torch.float32, 33), (torch.bfloat16, 33),
+                                     (torch.bfloat16, 128)])
+def test_rel_attention_vs_oracle(dtype, S):
+    """S=128 bf16 takes the tcgen05 kernel (TMEM rel-shift); the rest SIMT."""
     rng = np.random.default_rng(4)
-    M, B, S, H, dh = 3, 2, 33, 4, 64
+    M, B, H, dh = 3, 2, 4, 64
     qkv = rng.uniform(-1, 1, (M, B, S, 3 * H * dh)).astype(np.float32)
     r = rng.uniform(-1, 1, (M, B, 2 * S, H * dh)).astype(np.float32)
     rw = rng.uniform(-.3, .3, (M, H, dh)).astype(np.float32)
