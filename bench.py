@@ -268,6 +268,9 @@ def run_ours(args) -> dict | None:
     if tfile.exists():
         traffic = json.loads(tfile.read_text()).get(f"{args.model}/N{args.instances}/B{args.batch}")
 
+    unmerged = None if args.no_unmerged else unmerged_legs(
+        args, graph, stores, inputs, heads, flush, stream, value)
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -320,10 +323,117 @@ def run_ours(args) -> dict | None:
             "share_of_step": round(lin_ms / all_ms, 4) if all_ms else None,
             "tflops": round(lin_flops / (lin_ms / 1e3) / 1e12, 1),
         },
+        "unmerged": unmerged,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": plan.kernel_launches * args.steps,
     }
+
+
+def _time_steps(fn, n: int, flush, stream) -> float:
+    """Mean device ms of ``fn`` over ``n`` L2-flushed steps (CUDA events)."""
+    import torch
+    evs = []
+    for _ in range(n):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        fn()
+        e.record(stream)
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    return sum(s.elapsed_time(e) for s, e in evs) / n
+
+
+def unmerged_legs(args, graph, stores, inputs, heads, flush, stream, merged_value) -> dict:
+    """The metric's denominator: the same N instances run as N separate
+    (unmerged) forwards, sequentially in one stream on this GPU (SURVEY §8d,
+    PAPER.md:394-399 "sequential" baseline):
+      * ours_sequential: this framework's kernels at M=1, N per-instance plans
+        (backbone + head) recorded into one CUDA graph;
+      * torch_eager_sequential: stock PyTorch ops (cuBLAS / cuDNN / SDPA),
+        eager, one instance after another;
+      * torch_graph_sequential: the same PyTorch ops captured in a CUDA graph
+        (no launch overhead: the strongest unmerged baseline)."""
+    import torch
+
+    from baselines.torch_eager import TorchModel
+    from paper_2009_13062_b200 import compile_plan
+
+    n_inst = len(stores)
+    items = n_inst * args.batch
+    steps = max(3, min(args.steps, 20))
+    out: dict = {"instances": n_inst, "steps": steps}
+
+    plans = []
+    for m in range(n_inst):
+        p = compile_plan(graph, stores[m], mode="fast")
+        p.load_inputs(inputs[m])
+        hp = compile_plan(heads[m][0], heads[m][1], mode="fast") if heads else None
+        plans.append((p, hp))
+
+    def ours_all():
+        for p, hp in plans:
+            p.launch()
+            if hp is not None:
+                hp.input_views["feat"].copy_(p.outputs()[0])
+                hp.launch()
+
+    ours_all()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ours_all()
+    _time_steps(g.replay, 3, flush, stream)
+    ms = _time_steps(g.replay, steps, flush, stream)
+    out["ours_sequential"] = {"value": round(items / (ms / 1e3), 2), "ms_per_step": round(ms, 4),
+                              "kernel_launches": sum(p.kernel_launches +
+                                                     (hp.kernel_launches if hp else 0)
+                                                     for p, hp in plans)}
+    del g, plans
+
+    models = []
+    for m in range(n_inst):
+        tm = TorchModel(graph, stores[m])
+        tm.load(inputs[m])
+        hm = TorchModel(heads[m][0], heads[m][1]) if heads else None
+        models.append((tm, hm))
+
+    @torch.inference_mode()
+    def torch_all():
+        res = []
+        for tm, hm in models:
+            y = tm.forward()[0]
+            if hm is not None:
+                hm.inputs["feat"].copy_(y)
+                y = hm.forward()[0]
+            res.append(y)
+        return res
+
+    torch_all()
+    _time_steps(torch_all, 3, flush, stream)
+    ms = _time_steps(torch_all, steps, flush, stream)
+    out["torch_eager_sequential"] = {"value": round(items / (ms / 1e3), 2),
+                                     "ms_per_step": round(ms, 4)}
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s2):
+        torch_all()
+    torch.cuda.current_stream().wait_stream(s2)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        torch_all()
+    _time_steps(g.replay, 3, flush, stream)
+    ms = _time_steps(g.replay, steps, flush, stream)
+    out["torch_graph_sequential"] = {"value": round(items / (ms / 1e3), 2),
+                                     "ms_per_step": round(ms, 4)}
+    del g, models
+    out["speedup"] = {k: round(merged_value / out[k]["value"], 3)
+                      for k in ("ours_sequential", "torch_eager_sequential",
+                                "torch_graph_sequential")}
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -437,6 +547,8 @@ def main(argv=None) -> int:
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-heads", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-unmerged", action="store_true",
+                    help="skip the N-separate-runs legs (speedup denominator)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
