@@ -118,6 +118,23 @@ int nf_conv_nhwc_direct(const void* x, const void* w, const float* bias, const v
                         void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
                         int stride, int pad, int relu, int dtype, void* stream);
 
+/*
+ * Merged / grouped Conv2d as an implicit GEMM on the tensor cores (replaces
+ * reference `grouped_conv2d` / `conv2d`, engine.py:122-191, for the
+ * BN-folded bf16 CNN plans). x NHWC (N, H, W, C) bf16, w (groups, Cout/groups,
+ * kpad) bf16 K-major with K = (kh*k + kw)*(C/groups) + c zero-padded to kpad,
+ * bias fp32 (Cout) or NULL, residual NHWC like y or NULL, y NHWC
+ * (N, Ho, Wo, Cout) = relu?(conv + bias + residual). Needs C/groups % 4 == 0
+ * and Cout/groups % 4 == 0. workspace (from nf_conv_workspace_bytes, zeroed
+ * once) enables split-K; NULL disables it.
+ */
+int nf_grouped_conv_tc(const void* x, const void* w, const float* bias, const void* residual,
+                       void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
+                       int stride, int pad, int kpad, int relu, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups, int kernel,
+                                int stride, int pad, int kpad);
+
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream);

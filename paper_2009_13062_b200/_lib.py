@@ -44,6 +44,8 @@ SIGNATURES: dict[str, list] = {
     "nf_im2col_nhwc": [_p, _p] + [_i] * 10 + [_p],
     "nf_conv_nhwc_direct": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p],
     "nf_pool2d_nhwc": [_p, _p] + [_i] * 9 + [_p],
+    "nf_grouped_conv_tc": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _i64, _p],
+    "nf_conv_workspace_bytes": [_i] * 10,
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],
@@ -55,7 +57,8 @@ SIGNATURES: dict[str, list] = {
     "nf_pool2d": [_p, _p, _i64, _i64, _i, _i, _i, _i, _i, _i, _i, _p],
 }
 
-_RESTYPES = {"nf_status_string": ctypes.c_char_p, "nf_linear_workspace_bytes": ctypes.c_int64}
+_RESTYPES = {"nf_status_string": ctypes.c_char_p, "nf_linear_workspace_bytes": ctypes.c_int64,
+             "nf_conv_workspace_bytes": ctypes.c_int64}
 
 _lib: ctypes.CDLL | None = None
 

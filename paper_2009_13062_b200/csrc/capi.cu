@@ -146,6 +146,21 @@ int nf_conv_nhwc_direct(const void* x, const void* w, const float* bias, const v
                               pad, relu, dtype, static_cast<cudaStream_t>(stream));
 }
 
+int nf_grouped_conv_tc(const void* x, const void* w, const float* bias, const void* residual,
+                       void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
+                       int stride, int pad, int kpad, int relu, void* workspace,
+                       int64_t workspace_bytes, void* stream) {
+  if (!x || !w || !y || N < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return NF_ERR_SHAPE;
+  return nf::grouped_conv_tc(x, w, bias, residual, y, N, H, W, C, Cout, groups, kernel, stride,
+                             pad, kpad, relu, workspace, workspace_bytes,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups, int kernel,
+                                int stride, int pad, int kpad) {
+  return nf::conv_workspace_bytes(N, H, W, C, Cout, groups, kernel, stride, pad, kpad);
+}
+
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream) {
   if (!x || !y || N < 1 || H < 1 || W < 1 || C < 1) return NF_ERR_SHAPE;

@@ -1,0 +1,147 @@
+// Merged / grouped convolution as an implicit GEMM on the tensor cores.
+//
+// Replaces the reference's `grouped_conv2d` / `conv2d`
+// (pkg/src/modelmerge/engine.py:122-191) for NHWC bf16 activations: group g
+// is the GEMM  y[p, g*coutg + o] = sum_{kh,kw,c} x[pix(p)+(kh,kw), g*cg + c]
+// * W[g][o][(kh*k + kw)*cg + c]  with folded BatchNorm bias, optional
+// residual and ReLU in the epilogue. The kernel is k_grouped_gemm_tc
+// (gemm_sm100.cuh) with GATHER warps: im2col rows are gathered from HBM/L2
+// into shared memory by cp.async, never written to HBM.
+//
+// Orientation: pixels on the 128-row MMA side (normal) with a narrow N tile
+// (16 / 32 / 64 / 128 / 256 output channels of one group: ResNeXt's 4..32
+// channel groups waste at most 4x of a tiny MMA), or, for few pixels and
+// wide groups (ResNet layer3/4 at batch 1), weights on the 128-row side
+// (swapped) plus split-K so the weight stream covers every SM.
+#include "gemm_sm100.cuh"
+
+namespace nf {
+
+namespace {
+
+int conv_pick(int64_t pix, int64_t coutg, bool* swap) {
+  *swap = pix <= 256 && coutg >= 128;
+  if (*swap) return pix <= 64 ? 64 : (pix <= 128 ? 128 : 256);
+  if (coutg <= 16) return 16;
+  if (coutg <= 32) return 32;
+  if (coutg <= 64) return 64;
+  if (coutg <= 128 || pix < 4096) return 128;
+  return 256;
+}
+
+int conv_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) {
+  if (ws_bytes <= kCounterBytes || tiles >= 96 || tiles > kCounterBytes / 4) return 1;
+  int s = int(kNumSMs / tiles);
+  s = s < kMaxSplits ? s : kMaxSplits;
+  s = s < kb_total / 4 ? s : kb_total / 4;  // >= 4 K blocks per split
+  while (s > 1 && tiles * s * int64_t(kGemmBM) * bn * 4 > ws_bytes - kCounterBytes) --s;
+  return s < 1 ? 1 : s;
+}
+
+template <int BN, bool SWAP, int GATHER>
+int launch_conv(bool relu, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
+                const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t st) {
+  if (relu) return launch_tc_res<BN, SWAP, NF_ACT_RELU, GATHER>(ma, mb, my, mr, p, grid, st);
+  return launch_tc_res<BN, SWAP, NF_ACT_NONE, GATHER>(ma, mb, my, mr, p, grid, st);
+}
+
+}  // namespace
+
+int64_t conv_workspace_bytes(int64_t N, int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t G,
+                             int64_t k, int64_t stride, int64_t pad, int64_t Kpad) {
+  if (G < 1 || C % G || Cout % G || stride < 1) return 0;
+  const int64_t Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  const int64_t pix = N * Ho * Wo, coutg = Cout / G;
+  bool swap;
+  const int bn = conv_pick(pix, coutg, &swap);
+  const int64_t ta = swap ? (coutg + kGemmBM - 1) / kGemmBM : (pix + kGemmBM - 1) / kGemmBM;
+  const int64_t tb = swap ? (pix + bn - 1) / bn : (coutg + bn - 1) / bn;
+  const int64_t tiles = G * ta * tb;
+  const int s = conv_splits(tiles, int((Kpad + kGemmBK - 1) / kGemmBK), bn, INT64_MAX);
+  if (s <= 1) return 0;
+  return kCounterBytes + tiles * s * int64_t(kGemmBM) * bn * 4;
+}
+
+int grouped_conv_tc(const void* x, const void* w, const float* bias, const void* residual,
+                    void* y, int N, int H, int W, int C, int Cout, int G, int k, int stride,
+                    int pad, int Kpad, int relu, void* ws, int64_t ws_bytes, cudaStream_t stream) {
+  if (G < 1 || C % G || Cout % G || k < 1 || stride < 1 || pad < 0) return NF_ERR_SHAPE;
+  const int cg = C / G, coutg = Cout / G;
+  const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  if (Ho < 1 || Wo < 1 || Kpad < k * k * cg || Kpad % 8) return NF_ERR_SHAPE;
+  const int gather = cg % 8 == 0 ? 16 : (cg % 4 == 0 ? 8 : 0);
+  if (!gather || coutg % 4 || G > 65535) return NF_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) return NF_ERR_UNSUPPORTED;
+  if (ws && (reinterpret_cast<uintptr_t>(ws) & 255)) return NF_ERR_SHAPE;
+  const int64_t pix = int64_t(N) * Ho * Wo;
+  if (pix > (int64_t(1) << 30) || int64_t(N) * H * W > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
+  bool swap;
+  const int bn = conv_pick(pix, coutg, &swap);
+  if (gather == 8 && (swap || bn > 64)) return NF_ERR_UNSUPPORTED;
+
+  GemmParams p{};
+  p.bias = bias;
+  p.residual = residual;
+  p.out_gstride = coutg;
+  p.out_ld = Cout;
+  p.features = coutg;
+  p.groups = G;
+  p.kb_total = (Kpad + kGemmBK - 1) / kGemmBK;
+  p.y_direct = y;
+  p.cx = static_cast<const __nv_bfloat16*>(x);
+  p.cH = H; p.cW = W; p.cC = C; p.cCg = cg; p.cK = k; p.cS = stride; p.cP = pad;
+  p.cHo = Ho; p.cWo = Wo;
+  CUtensorMap mw, my, mr;
+  if (swap) {
+    if (!make_bf16_map(&mw, w, G, coutg, Kpad, kGemmBK, kGemmBM, 0, 0) ||
+        !make_bf16_map(&my, y, G, pix, coutg, kOutBlock, bn, Cout, coutg))
+      return NF_ERR_UNSUPPORTED;
+    p.rows_a = coutg;
+    p.rows_b = int(pix);
+  } else {
+    if (!make_bf16_map(&mw, w, G, coutg, Kpad, kGemmBK, bn, 0, 0)) return NF_ERR_UNSUPPORTED;
+    if (bn >= 64 && !make_bf16_map(&my, y, G, pix, coutg, kOutBlock, kGemmBM, Cout, coutg))
+      return NF_ERR_UNSUPPORTED;
+    if (bn < 64) my = mw;  // unused: narrow tiles store from registers
+    p.rows_a = int(pix);
+    p.rows_b = coutg;
+  }
+  mr = my;
+  if (residual && bn >= 64 &&
+      !(swap ? make_bf16_map(&mr, residual, G, pix, coutg, kOutBlock, bn, Cout, coutg)
+             : make_bf16_map(&mr, residual, G, pix, coutg, kOutBlock, kGemmBM, Cout, coutg)))
+    return NF_ERR_UNSUPPORTED;
+  p.tiles_a = (p.rows_a + kGemmBM - 1) / kGemmBM;
+  p.tiles_b = (p.rows_b + bn - 1) / bn;
+  const int64_t tiles = int64_t(G) * p.tiles_a * p.tiles_b;
+  p.splits = conv_splits(tiles, p.kb_total, bn, ws ? ws_bytes : 0);
+  p.kb_per_split = (p.kb_total + p.splits - 1) / p.splits;
+  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  if (tiles * p.splits > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
+  p.units = int(tiles * p.splits);
+  p.counters = static_cast<unsigned*>(ws);
+  p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
+  const int grid = p.units < kNumSMs ? p.units : kNumSMs;
+  const bool r = relu != 0;
+  // The weights map is the only TMA operand; it sits in the slot its
+  // orientation reads (A when swapped, B otherwise).
+#define NF_CV(BNV, SW, GA) return launch_conv<BNV, SW, GA>(r, mw, mw, my, mr, p, grid, stream)
+  if (swap) {
+    if (bn == 64) NF_CV(64, true, 16);
+    if (bn == 128) NF_CV(128, true, 16);
+    NF_CV(256, true, 16);
+  }
+  if (gather == 8) {
+    if (bn == 16) NF_CV(16, false, 8);
+    if (bn == 32) NF_CV(32, false, 8);
+    NF_CV(64, false, 8);
+  }
+  if (bn == 16) NF_CV(16, false, 16);
+  if (bn == 32) NF_CV(32, false, 16);
+  if (bn == 64) NF_CV(64, false, 16);
+  if (bn == 128) NF_CV(128, false, 16);
+  NF_CV(256, false, 16);
+#undef NF_CV
+}
+
+}  // namespace nf

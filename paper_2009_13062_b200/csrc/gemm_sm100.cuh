@@ -1,0 +1,667 @@
+// Merged Linear on the 5th-gen tensor cores: a persistent, per-instance
+// ("grouped") bf16 GEMM. tcgen05.mma accumulates in TMEM (two accumulator
+// buffers, so one tile's epilogue overlaps the next tile's main loop), TMA
+// streams operands through an mbarrier ring that runs continuously across
+// tiles, and the fused epilogue y = act(acc + bias + residual) goes
+// tcgen05.ld -> registers -> swizzled smem -> TMA bulk-tensor store.
+//
+// Replaces the reference's merged-Linear kernel `batch_matmul`
+// (pkg/src/modelmerge/engine.py:215-235) for instance-packed shapes
+// x (G, T, K) . W[g] -> y (G, T, N).
+//
+// D[i, j] = sum_k A[g, i, k] * B[g, j, k] over 128 x BN tiles, both operands
+// K-major (G, rows, K). Orientation:
+//   * normal  (SWAP=false): A = activations (i = token), B = weights (j = out
+//     feature) — large T, tensor-bound merges.
+//   * swapped (SWAP=true):  A = weights (i = out feature), B = activations
+//     (j = token) — small T (batch-1 serving): the MMA's 128-row side is
+//     filled by weight rows, so each weight byte is streamed once.
+// Work units are (instance, A tile, B tile, K split). A grid of
+// min(units, #SMs) CTAs walks them round-robin. K splits raise parallelism
+// for low-tile-count shapes: each split writes an fp32 partial to an L2
+// workspace, and the last arriver (per-tile semaphore) sums the partials in
+// split order (deterministic), runs the epilogue and re-arms the semaphore.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
+// issuer (one lane), warps 2..5 = epilogue (TMEM lane quarter = warp % 4).
+//
+// Implicit-GEMM convolution (GATHER = 16 or 8): the activation operand is
+// not a TMA tile but im2col rows gathered straight from the NHWC input by
+// four extra warps (6..9) with cp.async (16- or 8-byte channel chunks,
+// zero-filled outside the image / past the last tap) into the same
+// SWIZZLE_128B K-major layout; K = (kh, kw, c) padded to 64. Weights still
+// stream by TMA. Replaces the reference's `grouped_conv2d`
+// (engine.py:155-191) without materialising im2col in HBM.
+#pragma once
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nf {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
+constexpr int kGemmThreads = 192;
+constexpr int kGatherThreads = 128;
+constexpr int kGatherLag = 8;  // cp.async groups in flight per gather thread
+constexpr int kOutBlock = 64;  // features per 128-byte output block (bf16)
+constexpr int kMaxSplits = 8;
+#ifndef NF_GEMM_BUDGET_KB
+#define NF_GEMM_BUDGET_KB 220  // smem for the operand ring + output staging
+#endif
+constexpr int64_t kCounterBytes = 64 * 1024;  // semaphores at the workspace head
+
+#ifdef NF_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[4096];
+NF_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define NF_TRACE(slot)                                                          \
+  do {                                                                          \
+    if (blockIdx.x == 0) g_gemm_trace[(slot)] = gtimer();                       \
+  } while (0)
+#else
+#define NF_TRACE(slot) \
+  do {                 \
+  } while (0)
+#endif
+
+struct GemmParams {
+  const float* bias;     // (G, features) fp32 or nullptr
+  const void* residual;  // y-shaped bf16 or nullptr
+  int64_t out_gstride;   // elements between instances of y
+  int64_t out_ld;        // elements between tokens of y
+  int rows_a, rows_b;    // valid rows of A / B
+  int features;          // N (bias stride per instance)
+  int tiles_a, tiles_b, groups;
+  int splits, kb_total, kb_per_split, units;
+  float* ws;             // split-K partials [tile][split][128][BN]
+  unsigned* counters;    // [tile] arrival semaphores (zero between launches)
+  void* y_direct;        // BN < 64: y written from registers (no TMA store)
+  // implicit-GEMM conv geometry (GATHER kernels only)
+  const __nv_bfloat16* cx;  // NHWC input
+  int cH, cW, cC, cCg, cK, cS, cP, cHo, cWo;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr int kBBytes = BN * kGemmBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kOutBytes = BN >= 64 ? kGemmBM * BN * 2 : 0;
+  static constexpr int kStages =
+      ((BN >= 256 ? 220 : NF_GEMM_BUDGET_KB) * 1024 - kOutBytes) / kStageBytes;
+  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
+  static constexpr size_t kBytes =
+      1024 + size_t(kStages) * kStageBytes + kOutBytes + 512;
+  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert(kStages <= 32, "barrier array");
+  static_assert(kTmemCols <= 512, "TMEM overflow");
+};
+
+// Byte offset of (token row t, feature f) inside the staged output tile made
+// of 64-feature blocks, each `rows` x 128 B in the SWIZZLE_128B layout.
+NF_DEVICE uint32_t stage_offset(int t, int f, int rows) {
+  const int block = f >> 6;
+  const int within = (f & 63) * 2;
+  const int chunk = within >> 4;
+  return uint32_t(block * rows * 128 + t * 128 + (((chunk ^ (t & 7)) << 4) | (within & 15)));
+}
+
+struct UnitCoord {
+  int g, ta, tb, s, tile, kb0, kb1;
+};
+
+NF_DEVICE UnitCoord decode_unit(const GemmParams& p, int u, bool swap) {
+  UnitCoord c;
+  c.s = u % p.splits;
+  c.tile = u / p.splits;
+  // swapped: B (tokens) fastest; normal: A (token tiles) fastest, so CTAs
+  // running concurrently share one weight tile in L2.
+  if (swap) {
+    c.tb = c.tile % p.tiles_b;
+    c.ta = (c.tile / p.tiles_b) % p.tiles_a;
+    c.g = c.tile / (p.tiles_b * p.tiles_a);
+  } else {
+    c.ta = c.tile % p.tiles_a;
+    c.tb = (c.tile / p.tiles_a) % p.tiles_b;
+    c.g = c.tile / (p.tiles_a * p.tiles_b);
+  }
+  c.kb0 = c.s * p.kb_per_split;
+  c.kb1 = min(p.kb_total, c.kb0 + p.kb_per_split);
+  return c;
+}
+
+// cp.async with zero-fill: copies `src_bytes` (0 or the chunk size) and
+// fills the rest of the chunk with zeros.
+template <int BYTES>
+NF_DEVICE void cp_async_zfill(uint32_t dst, const void* src, int src_bytes) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+NF_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+NF_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER>
+__global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 1)
+    k_grouped_gemm_tc(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_y,
+                      const __grid_constant__ CUtensorMap map_r, GemmParams p) {
+  using C = GemmCfg<BN>;
+  constexpr int kStages = C::kStages;
+  // Residual tiles arrive by TMA into the output staging buffer (same
+  // swizzled layout as the result), so the epilogue adds them from smem.
+  constexpr bool kResTma = HAS_RES && BN >= 64;
+  constexpr int EC = BN < 32 ? BN : 32;  // epilogue column chunk
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * C::kABytes;
+  uint8_t* sOut = smem + kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + C::kOutBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
+  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    if (BN >= 64) tma_prefetch_desc(&map_y);
+    if (kResTma) tma_prefetch_desc(&map_r);
+    mbar_init(rbar, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], GATHER ? 1 + kGatherThreads : 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) NF_TRACE(0);
+  // Let the next kernel in the stream get scheduled as SMs free up; it waits
+  // on griddepcontrol.wait for this grid's results before reading them.
+  grid_dependents_launch();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // Weights stream once: evict-first. Activations are re-read by sibling
+      // CTAs: evict-last keeps them in L2.
+      const uint64_t hint_a = SWAP ? kEvictFirst : kEvictLast;
+      const uint64_t hint_b = SWAP ? kEvictLast : kEvictFirst;
+      constexpr uint32_t kTx = GATHER ? (SWAP ? C::kABytes : C::kBBytes) : C::kStageBytes;
+      auto load_w = [&](int stage, const UnitCoord& c, int kb) {
+        if (SWAP)
+          tma_load_3d(sA + stage * C::kABytes, &map_a, &full[stage], kb * kGemmBK,
+                      c.ta * kGemmBM, c.g, hint_a);
+        else
+          tma_load_3d(sB + stage * C::kBBytes, &map_b, &full[stage], kb * kGemmBK, c.tb * BN,
+                      c.g, hint_b);
+      };
+      auto load_x = [&](int stage, const UnitCoord& c, int kb) {
+        if (GATHER) return;  // gathered by warps 6..9
+        if (SWAP)
+          tma_load_3d(sB + stage * C::kBBytes, &map_b, &full[stage], kb * kGemmBK, c.tb * BN,
+                      c.g, hint_b);
+        else
+          tma_load_3d(sA + stage * C::kABytes, &map_a, &full[stage], kb * kGemmBK,
+                      c.ta * kGemmBM, c.g, hint_a);
+      };
+      int it = 0;
+      int u = blockIdx.x;
+      int pre = 0;
+      if (u < p.units) {
+        // Under programmatic dependent launch the weights do not depend on
+        // the previous kernel but the activations do: request the first
+        // ring's worth of weight tiles before the dependency wait.
+        const UnitCoord c = decode_unit(p, u, SWAP);
+        pre = min(kStages, c.kb1 - c.kb0);
+        for (int i = 0; i < pre; ++i) {
+          mbar_arrive_expect_tx(&full[i], kTx);
+          load_w(i, c, c.kb0 + i);
+        }
+        if (!GATHER) grid_dependency_wait();
+        for (int i = 0; i < pre; ++i) load_x(i, c, c.kb0 + i);
+        it = pre;
+      } else if (!GATHER) {
+        grid_dependency_wait();
+      }
+      for (; u < p.units; u += gridDim.x) {
+        const UnitCoord c = decode_unit(p, u, SWAP);
+        for (int kb = c.kb0 + pre; kb < c.kb1; ++kb, ++it) {
+          const int stage = it % kStages;
+          mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kTx);
+          load_w(stage, c, kb);
+          load_x(stage, c, kb);
+        }
+        pre = 0;
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc_bf16_f32(kGemmBM, BN);
+    int it = 0, local = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+      const UnitCoord c = decode_unit(p, u, SWAP);
+      const int acc = local & 1;
+      mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+      for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
+        const int stage = it % kStages;
+        mbar_wait(&full[stage], (it / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kGemmBK / 16; ++kk)
+            umma_f16_ss(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
+                        make_sw128_kmajor_desc(b_base + kk * 32), idesc,
+                        (kb != c.kb0 || kk != 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+        }
+        __syncwarp();
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp < 6) {
+    // ------------------------------ epilogue ------------------------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // accumulator row == TMEM lane
+    const int etid = threadIdx.x - 64;    // 0..127
+    const uint32_t stage_base = smem_u32(sOut);
+    uint32_t res_phase = 0;
+    int local = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+      const UnitCoord c = decode_unit(p, u, SWAP);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      if (etid == 0) NF_TRACE(1 + 4 * local);
+      const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+      const int m0 = c.ta * kGemmBM, n0 = c.tb * BN;
+      float* part = nullptr;
+      if (p.splits > 1) {
+        // Publish this split's fp32 partial; the last arriver reduces.
+        // Partials are stored column-major over TMEM lanes ([col][row]):
+        // each warp store covers one contiguous 128-byte line.
+        part = p.ws + (int64_t(c.tile) * p.splits) * kGemmBM * BN;
+        float* mine = part + int64_t(c.s) * kGemmBM * BN + row;
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += EC) {
+          uint32_t r[EC];
+          tmem_ld_cols<EC>(t_row + uint32_t(cc), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < EC; ++j) __stcg(mine + (cc + j) * kGemmBM, __uint_as_float(r[j]));
+        }
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (etid == 0) NF_TRACE(3 + 4 * local);
+        if (etid == 0) *last_flag = (atomicAdd(p.counters + c.tile, 1u) == unsigned(p.splits - 1));
+        named_bar_sync(1, 128);
+        if (!*last_flag) {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          continue;
+        }
+        __threadfence();
+      }
+      const __nv_bfloat16* res =
+          HAS_RES ? reinterpret_cast<const __nv_bfloat16*>(p.residual) +
+                        int64_t(c.g) * p.out_gstride
+                  : nullptr;
+      if constexpr (kResTma) {
+        // The previous unit's store has finished reading the staging buffer
+        // (bulk_wait_read0 + barrier below), so it can take this residual.
+        if (etid == 0) {
+          mbar_arrive_expect_tx(rbar, C::kOutBytes);
+          if (!SWAP) {
+#pragma unroll
+            for (int b = 0; b < BN / kOutBlock; ++b)
+              tma_load_3d(sOut + b * kGemmBM * 128, &map_r, rbar, n0 + b * kOutBlock, m0, c.g,
+                          kEvictFirst);
+          } else {
+#pragma unroll
+            for (int b = 0; b < kGemmBM / kOutBlock; ++b)
+              tma_load_3d(sOut + b * BN * 128, &map_r, rbar, m0 + b * kOutBlock, n0, c.g,
+                          kEvictFirst);
+          }
+        }
+        mbar_wait(rbar, res_phase);
+        res_phase ^= 1u;
+      }
+      const float* bias = p.bias ? p.bias + int64_t(c.g) * p.features : nullptr;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += EC) {
+        float v[EC];
+        {
+          uint32_t r[EC];
+          tmem_ld_cols<EC>(t_row + uint32_t(cc), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < EC; ++j) v[j] = __uint_as_float(r[j]);
+        }
+        if (p.splits > 1) {
+          // Deterministic reduction: splits summed in index order.
+          float sum[EC];
+#pragma unroll
+          for (int j = 0; j < EC; ++j) sum[j] = 0.f;
+          for (int s2 = 0; s2 < p.splits; ++s2) {
+            if (s2 == c.s) {
+#pragma unroll
+              for (int j = 0; j < EC; ++j) sum[j] += v[j];
+            } else {
+              const float* src = part + int64_t(s2) * kGemmBM * BN + row + cc * kGemmBM;
+#pragma unroll
+              for (int j = 0; j < EC; ++j) sum[j] += __ldcg(src + j * kGemmBM);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < EC; ++j) v[j] = sum[j];
+        }
+        if (!SWAP) {
+          // Thread = token row; EC consecutive features n0+cc ...
+          const int tok = m0 + row;
+          const int f0 = n0 + cc;
+          if (bias) {
+            if (f0 + EC <= p.rows_b) {
+#pragma unroll
+              for (int j = 0; j < EC; j += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + f0 + j));
+                v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < EC; ++j)
+                if (f0 + j < p.rows_b) v[j] += __ldg(bias + f0 + j);
+            }
+          }
+          if constexpr (kResTma) {
+#pragma unroll
+            for (int q = 0; q < EC / 8; ++q) {
+              uint32_t w4[4];
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
+                           : "r"(stage_base + stage_offset(row, cc + 8 * q, kGemmBM)));
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
+                v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xffff0000u);
+              }
+            }
+          } else if (HAS_RES && tok < p.rows_a) {
+            const __nv_bfloat16* rp = res + int64_t(tok) * p.out_ld + f0;
+#pragma unroll
+            for (int q = 0; q < EC / 4; ++q)
+              if (f0 + 4 * q + 4 <= p.rows_b) {
+                const uint2 u2 = *reinterpret_cast<const uint2*>(rp + 4 * q);
+                v[4 * q] += __uint_as_float(u2.x << 16);
+                v[4 * q + 1] += __uint_as_float(u2.x & 0xffff0000u);
+                v[4 * q + 2] += __uint_as_float(u2.y << 16);
+                v[4 * q + 3] += __uint_as_float(u2.y & 0xffff0000u);
+              }
+          }
+#pragma unroll
+          for (int j = 0; j < EC; ++j) v[j] = act_t<ACT>(v[j]);
+          if constexpr (BN >= 64) {
+#pragma unroll
+            for (int q = 0; q < EC / 8; ++q)
+              st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM),
+                           pack_bf16x2(v[8 * q], v[8 * q + 1]),
+                           pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                           pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
+                           pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+          } else if (tok < p.rows_a) {
+            // Narrow tiles (grouped convs with 4..32 channels per group):
+            // each thread writes its row's features straight to HBM.
+            __nv_bfloat16* yp = reinterpret_cast<__nv_bfloat16*>(p.y_direct) +
+                                int64_t(c.g) * p.out_gstride + int64_t(tok) * p.out_ld + f0;
+#pragma unroll
+            for (int q = 0; q < EC / 4; ++q)
+              if (f0 + 4 * q + 4 <= p.rows_b) {
+                uint2 u2;
+                u2.x = pack_bf16x2(v[4 * q], v[4 * q + 1]);
+                u2.y = pack_bf16x2(v[4 * q + 2], v[4 * q + 3]);
+                *reinterpret_cast<uint2*>(yp + 4 * q) = u2;
+              }
+          }
+        } else {
+          // Thread = feature row; 32 consecutive tokens. Neighbouring lanes
+          // (features f, f^1) swap one value so each lane stores a packed
+          // bf16 pair of adjacent features: 16 32-bit smem stores per chunk.
+          const int feat = m0 + row;
+          const float b = (bias && feat < p.rows_a) ? __ldg(bias + feat) : 0.0f;
+#pragma unroll
+          for (int j = 0; j < EC; ++j) {
+            v[j] += b;
+            if constexpr (kResTma) {
+              uint16_t h;
+              asm volatile("ld.shared.u16 %0, [%1];"
+                           : "=h"(h)
+                           : "r"(stage_base + stage_offset(cc + j, row, BN)));
+              v[j] += __uint_as_float(uint32_t(h) << 16);
+            }
+            v[j] = act_t<ACT>(v[j]);
+          }
+          if constexpr (kResTma) __syncwarp();  // partner lanes read before the pair stores
+          const bool odd = lane & 1;
+          const int feven = row & ~1;
+#pragma unroll
+          for (int j = 0; j < EC; j += 2) {
+            const float send = odd ? v[j] : v[j + 1];
+            const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+            const uint32_t packed = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
+            const int t = cc + j + (odd ? 1 : 0);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage_base + stage_offset(t, feven, BN)),
+                         "r"(packed)
+                         : "memory");
+          }
+        }
+      }
+      // All TMEM reads of this buffer are done: hand it back to the MMA warp.
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if constexpr (BN >= 64) {
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (etid == 0) {
+          if (!SWAP) {
+#pragma unroll
+            for (int b = 0; b < BN / kOutBlock; ++b)
+              tma_store_3d(&map_y, sOut + b * kGemmBM * 128, n0 + b * kOutBlock, m0, c.g);
+          } else {
+#pragma unroll
+            for (int b = 0; b < kGemmBM / kOutBlock; ++b)
+              tma_store_3d(&map_y, sOut + b * BN * 128, m0 + b * kOutBlock, n0, c.g);
+          }
+          bulk_commit();
+          if (p.splits > 1) p.counters[c.tile] = 0u;  // re-arm for the next launch
+          bulk_wait_read0();                          // staging reusable
+          NF_TRACE(4 + 4 * local);
+        }
+        named_bar_sync(1, 128);
+      } else {
+        if (p.splits > 1) {
+          named_bar_sync(1, 128);
+          if (etid == 0) p.counters[c.tile] = 0u;
+        }
+      }
+    }
+  } else if constexpr (GATHER != 0) {
+    // ------------------------ im2col gather (conv) ------------------------
+    constexpr int R = SWAP ? BN : kGemmBM;  // activation rows per tile
+    constexpr int CPR = 128 / GATHER;       // chunks per 128-byte row
+    constexpr int RPP = kGatherThreads / CPR;
+    constexpr int PASSES = R / RPP;
+    constexpr int CE = GATHER / 2;           // channels per chunk
+    // Arrivals trail the issue by LAG iterations; LAG < kStages or the
+    // producer would wait on a slot whose fill it has not yet published.
+    constexpr int LAG = kGatherLag < kStages - 1 ? kGatherLag : kStages - 1;
+    const int gt = threadIdx.x - kGemmThreads;
+    const int j = gt % CPR;
+    const int r0 = gt / CPR;
+    const uint32_t act_smem = smem_u32(SWAP ? sB : sA);
+    constexpr uint32_t kActBytes = SWAP ? C::kBBytes : C::kABytes;
+    // swizzled byte offset of chunk j within a row r (SWIZZLE_128B)
+    const uint32_t jb = uint32_t(j * GATHER);
+    const int taps = p.cK * p.cK;
+    const int rows = SWAP ? p.rows_b : p.rows_a;
+    grid_dependency_wait();
+    int it = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const UnitCoord c = decode_unit(p, u, SWAP);
+      const int row0 = SWAP ? c.tb * BN : c.ta * kGemmBM;
+      const __nv_bfloat16* xg = p.cx + int64_t(c.g) * p.cCg;
+      int pix_off[PASSES], ih0[PASSES], iw0[PASSES];
+#pragma unroll
+      for (int i = 0; i < PASSES; ++i) {
+        const int pix = row0 + r0 + RPP * i;
+        const int ow = pix % p.cWo;
+        const int t2 = pix / p.cWo;
+        const int oh = t2 % p.cHo;
+        const int n = t2 / p.cHo;
+        ih0[i] = pix < rows ? oh * p.cS - p.cP : -(1 << 20);
+        iw0[i] = ow * p.cS - p.cP;
+        pix_off[i] = n * p.cH * p.cW;
+      }
+      for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
+        const int stage = it % kStages;
+        mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
+        const int k0 = kb * kGemmBK + j * CE;
+        const int tap = k0 / p.cCg;
+        const int ch = k0 - tap * p.cCg;
+        const int kh = tap / p.cK;
+        const int kw = tap - kh * p.cK;
+        const bool tap_ok = tap < taps;
+        const uint32_t sbase = act_smem + uint32_t(stage) * kActBytes;
+#pragma unroll
+        for (int i = 0; i < PASSES; ++i) {
+          const int r = r0 + RPP * i;
+          const int ih = ih0[i] + kh, iw = iw0[i] + kw;
+          const bool ok = tap_ok && ih >= 0 && ih < p.cH && iw >= 0 && iw < p.cW;
+          const __nv_bfloat16* src =
+              ok ? xg + (int64_t(pix_off[i]) + ih * p.cW + iw) * p.cC + ch : p.cx;
+          const uint32_t dst =
+              sbase + uint32_t(r * 128) + ((((jb >> 4) ^ uint32_t(r & 7)) << 4) | (jb & 15));
+          cp_async_zfill<GATHER>(dst, src, ok ? GATHER : 0);
+        }
+        cp_async_commit();
+        if (it >= LAG) {
+          cp_async_wait<LAG>();
+          fence_proxy_async_smem();
+          mbar_arrive(&full[(it - LAG) % kStages]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (int back = it - LAG < 0 ? 0 : it - LAG; back < it; ++back)
+      mbar_arrive(&full[back % kStages]);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) NF_TRACE(2);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  // Resolved once; the function pointer is immutable afterwards.
+  static EncodeTiledFn fn = []() -> EncodeTiledFn {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 3-D bf16 tensor (G, rows, inner) with inner contiguous -> tensor map with
+// a (box_inner, box_rows, 1) SWIZZLE_128B box (box_inner * 2 == 128 bytes).
+bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
+                   int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
+
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0>
+static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
+                     const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER>;
+  static bool attr_done = false;  // idempotent attribute set; benign race
+  if (!attr_done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kBytes));
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads + (GATHER ? kGatherThreads : 0));
+  cfg.dynamicSmemBytes = C::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, mr, p);
+  return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
+template <int BN, bool SWAP, int ACT, int GATHER = 0>
+static int launch_tc_res(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
+                         const CUtensorMap& mr, const GemmParams& p, int grid,
+                         cudaStream_t stream) {
+  if (p.residual) return launch_tc<BN, SWAP, ACT, true, GATHER>(ma, mb, my, mr, p, grid, stream);
+  return launch_tc<BN, SWAP, ACT, false, GATHER>(ma, mb, my, mr, p, grid, stream);
+}
+
+template <int BN, bool SWAP>
+static int launch_tc_act(int act, const CUtensorMap& ma, const CUtensorMap& mb,
+                         const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
+                         int grid, cudaStream_t stream) {
+  switch (act) {
+    case NF_ACT_RELU: return launch_tc_res<BN, SWAP, NF_ACT_RELU>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_GELU: return launch_tc_res<BN, SWAP, NF_ACT_GELU>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_TANH: return launch_tc_res<BN, SWAP, NF_ACT_TANH>(ma, mb, my, mr, p, grid, stream);
+    default: return launch_tc_res<BN, SWAP, NF_ACT_NONE>(ma, mb, my, mr, p, grid, stream);
+  }
+}
+
+}  // namespace nf

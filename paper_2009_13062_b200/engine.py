@@ -179,6 +179,9 @@ class Plan:
         need = int(_lib.load().nf_linear_workspace_bytes(groups, rows, k, n))
         if need <= 0:
             return None
+        return self._ws_buffer(need)
+
+    def _ws_buffer(self, need: int) -> torch.Tensor:
         cur = getattr(self, "_ws", None)
         if cur is None or cur.numel() < need:
             # A larger shape gets a fresh buffer; earlier launches keep theirs.
@@ -465,6 +468,17 @@ class Plan:
         self._copy_step(node_id, src, out.permute(0, 3, 1, 2))
         return out
 
+    def _nhwc_padded(self, node_id: str, v: DVal, groups: int, cg: int, cg_pad: int):
+        """NHWC copy of a logical NCHW value with each group's channels
+        zero-padded from cg to cg_pad (16-byte-friendly gather rows)."""
+        src = v.t if v.split is None else self._materialize(node_id, v)
+        n, c, h, w = v.dims
+        out = self._own(torch.zeros((n, h, w, groups * cg_pad), dtype=v.dtype,
+                                    device=self.device))
+        dst = out.view(n, h, w, groups, cg_pad)[..., :cg].permute(0, 3, 4, 1, 2)
+        self._copy_step(node_id, src.reshape(n, groups, cg, h, w), dst)
+        return out
+
     def _folded_conv(self, ch, weights, dt):
         """Conv weights with BatchNorm folded in: returns (w (Cout, k, k, Cg)
         fp32 scaled, bias (Cout,) fp32)."""
@@ -519,36 +533,73 @@ class Plan:
                 "nf_grouped_conv2d", xp, wp, bp, None, rp, yp, n, c, h, wd, cout, k, s, pad,
                 groups, relu, dcode, _lib.NF_MODE_FAST, st))
             return DVal(y, (n, cout, ho, wo))
-        xn = self._nhwc(conv.id, v)
+        cg_pad = cg if cg % 4 == 0 else -(-cg // 4) * 4  # stem: 3 -> 4 channels
+        if coutg % 4:
+            cg_pad = cg  # direct kernel below reads the unpadded layout
+        if cg_pad != cg:
+            xn = self._nhwc_padded(conv.id, v, groups, cg, cg_pad)
+        else:
+            xn = self._nhwc(conv.id, v)
+        c_in = groups * cg_pad
         yn = self._alloc((n, ho, wo, cout), dt)
         rn = self._nhwc(conv.id, other) if other is not None else None
         rp = rn.data_ptr() if rn is not None else None
         pix = n * ho * wo
-        kk = k * k * cg
-        if coutg % 8 == 0 and kk >= 32:
-            kpad = -(-kk // 8) * 8
+        act = _lib.NF_ACT_RELU if relu else _lib.NF_ACT_NONE
+        if k == 1 and s == 1 and pad == 0 and cg % 8 == 0 and coutg % 8 == 0:
+            # 1x1 conv == grouped GEMM over the pixel matrix: TMA reads the
+            # NHWC rows in place (row stride C, group stride C/G).
             wkey = key + ("gemm",)
             if wkey not in self._wcache:
-                wg = wf.reshape(groups, coutg, kk)
+                self._wcache[wkey] = (wf.reshape(groups, coutg, cg).to(dt).contiguous(),
+                                      bias.view(groups, coutg).contiguous())
+            wg, bg = self._wcache[wkey]
+            xp, wp, bp, yp = xn.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
+            self._linear_w[len(self.steps)] = (wp, wg.numel() * wg.element_size())
+            ws = self._workspace(groups, pix, cg, coutg)
+            wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
+            self._emit(conv.id, lambda st: _lib.call(
+                "nf_grouped_linear_ws", xp, c, cg, wp, bp, rp, yp, cout, coutg, groups, pix,
+                cg, coutg, _lib.NF_BF16, _lib.NF_W_NK, act, _lib.NF_MODE_FAST, wsp, wsb, st))
+        elif coutg % 4 == 0:
+            # implicit GEMM: im2col rows gathered on chip (cp.async), never in HBM.
+            # Narrow groups (ResNeXt: 4..16 channels) are densified into
+            # super-groups of 32 channels with block-diagonal weights: 16-byte
+            # gather rows and a 32-wide MMA tile instead of many tiny units
+            # (at most 8x the FLOPs of a conv that is HBM-bound anyway).
+            sup = 1
+            if cg_pad == cg and cg < 32 and 32 % cg == 0 and groups % (32 // cg) == 0:
+                sup = 32 // cg
+            g_eff, cg_eff, coutg_eff = groups // sup, cg_pad * sup, coutg * sup
+            kk = k * k * cg_eff
+            kpad = -(-kk // 8) * 8
+            wkey = key + ("igemm", sup)
+            if wkey not in self._wcache:
+                w4 = wf
+                if cg_pad != cg:
+                    w4 = torch.nn.functional.pad(wf, (0, cg_pad - cg))
+                if sup > 1:
+                    blk = w4.reshape(g_eff, sup, coutg, k, k, cg)
+                    dense = torch.zeros((g_eff, sup, coutg, k, k, sup, cg), dtype=w4.dtype,
+                                        device=w4.device)
+                    for q in range(sup):
+                        dense[:, q, :, :, :, q, :] = blk[:, q]
+                    w4 = dense.reshape(cout, k, k, cg_eff)
+                wg = w4.reshape(g_eff, coutg_eff, kk)
                 if kpad != kk:
                     wg = torch.nn.functional.pad(wg, (0, kpad - kk))
-                self._wcache[wkey] = (wg.to(dt).contiguous(), bias.view(groups, coutg).contiguous())
+                self._wcache[wkey] = (wg.to(dt).contiguous(), bias.contiguous())
             wg, bg = self._wcache[wkey]
-            if k == 1 and s == 1 and pad == 0 and cg % 8 == 0:
-                xp, xld, xgs, kdim = xn.data_ptr(), c, cg, cg
-            else:
-                col = self._alloc((pix, groups, kpad), dt)
-                xsrc, colp = xn.data_ptr(), col.data_ptr()
-                self._emit(conv.id, lambda st: _lib.call(
-                    "nf_im2col_nhwc", xsrc, colp, n, h, wd, c, groups, k, s, pad, kpad,
-                    _lib.NF_BF16, st))
-                xp, xld, xgs, kdim = colp, groups * kpad, kpad, kpad
-            act = _lib.NF_ACT_RELU if relu else _lib.NF_ACT_NONE
-            wp, bp, yp = wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
+            groups = g_eff
+            need = int(_lib.load().nf_conv_workspace_bytes(n, h, wd, c_in, cout, groups, k, s,
+                                                           pad, kpad))
+            ws = self._ws_buffer(need) if need > 0 else None
+            wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
+            xp, wp, bp, yp = xn.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
             self._linear_w[len(self.steps)] = (wp, wg.numel() * wg.element_size())
             self._emit(conv.id, lambda st: _lib.call(
-                "nf_grouped_linear_ws", xp, xld, xgs, wp, bp, rp, yp, cout, coutg, groups, pix,
-                kdim, coutg, _lib.NF_BF16, _lib.NF_W_NK, act, _lib.NF_MODE_FAST, None, 0, st))
+                "nf_grouped_conv_tc", xp, wp, bp, rp, yp, n, h, wd, c_in, cout, groups, k, s,
+                pad, kpad, relu, wsp, wsb, st))
         else:
             wkey = key + ("direct",)
             if wkey not in self._wcache:

@@ -27,7 +27,12 @@ def main():
     ap.add_argument("--no-heads", action="store_true")
     ap.add_argument("--prefetch", action="store_true")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="serialise kernels (NF_PDL=0) so per-kernel durations are exact")
     args = ap.parse_args()
+    if args.no_pdl:
+        import os
+        os.environ["NF_PDL"] = "0"
     _, _, inputs, merged, mstore, _ = bench.build_workload(
         args.model, args.instances, args.batch, "bf16", 0, heads=not args.no_heads)
     plan = compile_plan(merged.graph, mstore, prefetch=args.prefetch)
