@@ -9,11 +9,14 @@ symbol checks run on CPU-only machines.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from .errors import ExecutionError, ShapeError, UnsupportedOpError
 
 LIB_PATH = Path(__file__).resolve().parent / "libnetfuse_b200.so"
+if os.environ.get("NF_LIB_PATH"):  # A/B experiments with alternative builds (tools/)
+    LIB_PATH = Path(os.environ["NF_LIB_PATH"]).resolve()
 HEADER_PATH = Path(__file__).resolve().parent.parent / "include" / "netfuse_b200.h"
 
 NF_OK, NF_ERR_SHAPE, NF_ERR_UNSUPPORTED, NF_ERR_LAUNCH = 0, 1, 2, 3

@@ -72,6 +72,7 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.out_ld = y_ld;
   p.features = int(N);
   p.groups = int(G);
+  p.y_direct = y;
   p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
   const bool swap = T <= 256;
   const int bn = pick_bn(T, N);

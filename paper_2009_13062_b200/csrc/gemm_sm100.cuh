@@ -51,7 +51,10 @@ constexpr int kMaxSplits = 8;
 constexpr int64_t kCounterBytes = 64 * 1024;  // semaphores at the workspace head
 
 #ifdef NF_GEMM_TRACE
-__device__ unsigned long long g_gemm_trace[4096];
+// Per-CTA pipeline timestamps (globaltimer ns), 8 slots per CTA:
+// 0 entry, 1 setup done, 2 first stage landed (MMA warp), 3 last MMA
+// committed, 4 first accumulator ready (epilogue), 5 epilogue done, 6 exit.
+__device__ unsigned long long g_gemm_trace[148 * 8];
 NF_DEVICE unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -59,7 +62,7 @@ NF_DEVICE unsigned long long gtimer() {
 }
 #define NF_TRACE(slot)                                                          \
   do {                                                                          \
-    if (blockIdx.x == 0) g_gemm_trace[(slot)] = gtimer();                       \
+    if (blockIdx.x < 148) g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer();     \
   } while (0)
 #else
 #define NF_TRACE(slot) \
@@ -78,20 +81,44 @@ struct GemmParams {
   int splits, kb_total, kb_per_split, units;
   float* ws;             // split-K partials [tile][split][128][BN]
   unsigned* counters;    // [tile] arrival semaphores (zero between launches)
-  void* y_direct;        // BN < 64: y written from registers (no TMA store)
+  void* y_direct;        // y for tiles stored straight from registers (!kStaged)
   // implicit-GEMM conv geometry (GATHER kernels only)
   const __nv_bfloat16* cx;  // NHWC input
   int cH, cW, cC, cCg, cK, cS, cP, cHo, cWo;
 };
 
-template <int BN>
+#ifndef NF_GEMM_LITE_KB
+#define NF_GEMM_LITE_KB 100  // swapped (weight-streaming) tiles: 2 CTAs per SM
+#endif
+
+// Output path of a tile configuration: staged = registers -> swizzled smem ->
+// TMA store (wide normal tiles, swapped 256-token tiles); otherwise the
+// epilogue stores straight from registers (narrow normal tiles; swapped
+// tiles, where a warp's lanes are consecutive features of one token, so the
+// stores coalesce without staging).
+// Direct swapped stores measured slower (4 us vs 1.8 us per 128x128 tile
+// epilogue on B200) than staging + TMA store, so they are opt-in.
+#ifndef NF_GEMM_DIRECT_SWAP
+#define NF_GEMM_DIRECT_SWAP 0
+#endif
+template <int BN, bool SWAP>
+struct GemmOut {
+  static constexpr bool kStaged = BN >= 64 && !(NF_GEMM_DIRECT_SWAP && SWAP && BN <= 128);
+};
+
+template <int BN, bool SWAP>
 struct GemmCfg {
+  static constexpr bool kStaged = GemmOut<BN, SWAP>::kStaged;
   static constexpr int kABytes = kGemmBM * kGemmBK * 2;
   static constexpr int kBBytes = BN * kGemmBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kOutBytes = BN >= 64 ? kGemmBM * BN * 2 : 0;
-  static constexpr int kStages =
-      ((BN >= 256 ? 220 : NF_GEMM_BUDGET_KB) * 1024 - kOutBytes) / kStageBytes;
+  static constexpr int kOutBytes = kStaged ? kGemmBM * BN * 2 : 0;
+  // Swapped tiles stream weights at batch 1: a small footprint lets the next
+  // kernel's CTA (programmatic dependent launch) sit beside this one and
+  // prefetch its own weights while this one drains.
+  static constexpr int kBudgetKB =
+      BN >= 256 ? 220 : (SWAP && !kStaged ? NF_GEMM_LITE_KB : NF_GEMM_BUDGET_KB);
+  static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr size_t kBytes =
       1024 + size_t(kStages) * kStageBytes + kOutBytes + 512;
@@ -156,11 +183,11 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
                       const __grid_constant__ CUtensorMap map_b,
                       const __grid_constant__ CUtensorMap map_y,
                       const __grid_constant__ CUtensorMap map_r, GemmParams p) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, SWAP>;
   constexpr int kStages = C::kStages;
   // Residual tiles arrive by TMA into the output staging buffer (same
   // swizzled layout as the result), so the epilogue adds them from smem.
-  constexpr bool kResTma = HAS_RES && BN >= 64;
+  constexpr bool kResTma = HAS_RES && C::kStaged;
   constexpr int EC = BN < 32 ? BN : 32;  // epilogue column chunk
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -178,11 +205,12 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) NF_TRACE(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
-    if (BN >= 64) tma_prefetch_desc(&map_y);
+    if (C::kStaged) tma_prefetch_desc(&map_y);
     if (kResTma) tma_prefetch_desc(&map_r);
     mbar_init(rbar, 1);
     for (int s = 0; s < kStages; ++s) {
@@ -200,7 +228,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (threadIdx.x == 0) NF_TRACE(0);
+  if (threadIdx.x == 0) NF_TRACE(1);
   // Let the next kernel in the stream get scheduled as SMs free up; it waits
   // on griddepcontrol.wait for this grid's results before reading them.
   grid_dependents_launch();
@@ -273,6 +301,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
         const int stage = it % kStages;
         mbar_wait(&full[stage], (it / kStages) & 1);
         tc_fence_after();
+        if (lane == 0 && it == 0) NF_TRACE(2);
         if (lane == 0) {
           const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
           const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
@@ -288,6 +317,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
       if (lane == 0) umma_commit(&tfull[acc]);
       __syncwarp();
     }
+    if (lane == 0) NF_TRACE(3);
   } else if (warp < 6) {
     // ------------------------------ epilogue ------------------------------
     const int quarter = warp & 3;
@@ -301,7 +331,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
-      if (etid == 0) NF_TRACE(1 + 4 * local);
+      if (etid == 0 && local == 0) NF_TRACE(4);
       const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
       const int m0 = c.ta * kGemmBM, n0 = c.tb * BN;
       float* part = nullptr;
@@ -321,7 +351,6 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
         }
         __threadfence();
         named_bar_sync(1, 128);
-        if (etid == 0) NF_TRACE(3 + 4 * local);
         if (etid == 0) *last_flag = (atomicAdd(p.counters + c.tile, 1u) == unsigned(p.splits - 1));
         named_bar_sync(1, 128);
         if (!*last_flag) {
@@ -428,7 +457,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
           }
 #pragma unroll
           for (int j = 0; j < EC; ++j) v[j] = act_t<ACT>(v[j]);
-          if constexpr (BN >= 64) {
+          if constexpr (C::kStaged) {
 #pragma unroll
             for (int q = 0; q < EC / 8; ++q)
               st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM),
@@ -459,6 +488,12 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
 #pragma unroll
           for (int j = 0; j < EC; ++j) {
             v[j] += b;
+            if constexpr (HAS_RES && !C::kStaged) {
+              // lanes = consecutive features of one token: coalesced
+              const int tok = n0 + cc + j;
+              if (feat < p.rows_a && tok < p.rows_b)
+                v[j] += __bfloat162float(res[int64_t(tok) * p.out_ld + feat]);
+            }
             if constexpr (kResTma) {
               uint16_t h;
               asm volatile("ld.shared.u16 %0, [%1];"
@@ -477,16 +512,28 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
             const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
             const uint32_t packed = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
             const int t = cc + j + (odd ? 1 : 0);
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage_base + stage_offset(t, feven, BN)),
-                         "r"(packed)
-                         : "memory");
+            if constexpr (C::kStaged) {
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage_base +
+                                                             stage_offset(t, feven, BN)),
+                           "r"(packed)
+                           : "memory");
+            } else {
+              // even lanes: token t, odd lanes: token t+1; each half-warp
+              // writes 64 contiguous bytes of one token row.
+              const int tok = n0 + t;
+              const int f = m0 + feven;
+              if (tok < p.rows_b && f < p.rows_a)
+                *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(p.y_direct) +
+                                             int64_t(c.g) * p.out_gstride +
+                                             int64_t(tok) * p.out_ld + f) = packed;
+            }
           }
         }
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if constexpr (BN >= 64) {
+      if constexpr (C::kStaged) {
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (etid == 0) {
@@ -502,7 +549,6 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
           bulk_commit();
           if (p.splits > 1) p.counters[c.tile] = 0u;  // re-arm for the next launch
           bulk_wait_read0();                          // staging reusable
-          NF_TRACE(4 + 4 * local);
         }
         named_bar_sync(1, 128);
       } else {
@@ -512,6 +558,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
         }
       }
     }
+    if (etid == 0) NF_TRACE(5);
   } else if constexpr (GATHER != 0) {
     // ------------------------ im2col gather (conv) ------------------------
     constexpr int R = SWAP ? BN : kGemmBM;  // activation rows per tile
@@ -586,7 +633,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) NF_TRACE(2);
+  if (threadIdx.x == 0) NF_TRACE(6);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
@@ -623,7 +670,7 @@ bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, 
 template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, SWAP>;
   auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER>;
   static bool attr_done = false;  // idempotent attribute set; benign race
   if (!attr_done) {

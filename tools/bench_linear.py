@@ -85,9 +85,13 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--shapes", default="", help="extra G,T,K,N;G,T,K,N;... to time")
     args = ap.parse_args()
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, device="cuda")
-    for name, shp in SHAPES.items():
+    shapes = dict(SHAPES)
+    if args.shapes:
+        shapes = {f"g{s}": tuple(int(v) for v in s.split(",")) for s in args.shapes.split(";")}
+    for name, shp in shapes.items():
         if args.only and name not in args.only.split(","):
             continue
         print(json.dumps(run(name, *shp, args.reps, flush)))

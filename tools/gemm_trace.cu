@@ -1,50 +1,60 @@
-// Standalone instrumented run of the tcgen05 grouped GEMM: timestamps
-// (globaltimer, ns) of CTA (0,0,0)'s pipeline events.
+// Per-CTA pipeline timeline of the tcgen05 grouped GEMM (globaltimer ns,
+// relative to the end of a stamp kernel launched just before it, PDL off).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DNF_GEMM_TRACE \
 //        -I include -I paper_2009_13062_b200/csrc tools/gemm_trace.cu -o build/gemm_trace -lcuda
+//   NF_PDL=0 build/gemm_trace G T K N
 #include "../paper_2009_13062_b200/csrc/gemm_sm100.cu"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 
+__device__ unsigned long long g_stamp;
+__global__ void stamp_kernel() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_stamp = t;
+}
+
 int main(int argc, char** argv) {
   int G = argc > 1 ? atoi(argv[1]) : 8, T = argc > 2 ? atoi(argv[2]) : 128;
-  int K = argc > 3 ? atoi(argv[3]) : 3072, N = argc > 4 ? atoi(argv[4]) : 768;
+  int K = argc > 3 ? atoi(argv[3]) : 768, N = argc > 4 ? atoi(argv[4]) : 2304;
   size_t nx = size_t(G) * T * K, nw = size_t(G) * N * K, ny = size_t(G) * T * N;
-  void *x, *w, *y;
+  void *x, *w, *y, *flush;
   cudaMalloc(&x, nx * 2);
   cudaMalloc(&w, nw * 2);
   cudaMalloc(&y, ny * 2);
+  cudaMalloc(&flush, 256 << 20);
   cudaMemset(x, 0, nx * 2);
   cudaMemset(w, 0, nw * 2);
   int64_t ws_bytes = nf::linear_workspace_bytes(G, T, K, N);
   void* ws = nullptr;
   if (ws_bytes) { cudaMalloc(&ws, ws_bytes); cudaMemset(ws, 0, ws_bytes); }
-  printf("workspace %lld bytes\n", (long long)ws_bytes);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  const char* names[7] = {"entry", "setup", "first_stage", "last_mma", "acc0_ready", "epi_done",
+                          "exit"};
   for (int it = 0; it < 3; ++it) {
-    cudaEventRecord(e0);
-    int st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, y, N, int64_t(T) * N,
-                                   G, T, K, N, NF_BF16, 0, ws, ws_bytes, 0);
-    cudaEventRecord(e1);
+    cudaMemset(flush, it, 256 << 20);
+    stamp_kernel<<<1, 1>>>();
+    int st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, y, N,
+                                   int64_t(T) * N, G, T, K, N, NF_BF16, 0, ws, ws_bytes, 0);
     cudaError_t e = cudaDeviceSynchronize();
-    float ms;
-    cudaEventElapsedTime(&ms, e0, e1);
-    printf("iter %d status %d err %s  %.2f us\n", it, st, cudaGetErrorString(e), ms * 1e3);
+    if (st || e) { printf("status %d err %s\n", st, cudaGetErrorString(e)); return 1; }
+    if (it < 2) continue;
+    std::vector<unsigned long long> tr(148 * 8);
+    unsigned long long t0;
+    cudaMemcpyFromSymbol(tr.data(), nf::g_gemm_trace, sizeof(unsigned long long) * 148 * 8);
+    cudaMemcpyFromSymbol(&t0, g_stamp, sizeof(t0));
+    printf("G=%d T=%d K=%d N=%d workspace=%lld\n", G, T, K, N, (long long)ws_bytes);
+    for (int s = 0; s < 7; ++s) {
+      std::vector<double> v;
+      for (int b = 0; b < 148; ++b)
+        if (tr[b * 8 + s] > t0 && tr[b * 8 + s] - t0 < 100000000ull) v.push_back((tr[b * 8 + s] - t0) * 1e-3);
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      printf("  %-12s n=%3zu  min %7.2f  med %7.2f  max %7.2f us\n", names[s], v.size(), v[0],
+             v[v.size() / 2], v.back());
+    }
   }
-  std::vector<unsigned long long> tr(4096);
-  cudaMemcpyFromSymbol(tr.data(), nf::g_gemm_trace, sizeof(unsigned long long) * 4096);
-  unsigned long long t0 = tr[0];
-  int num_kb = (K + 63) / 64;
-  printf("end=%lld\n", (long long)(tr[2] - t0));
-  for (int l = 0; l < 4; ++l)
-    if (tr[1 + 4 * l] > t0)
-      printf("unit %d: acc ready %lld  partial published %lld  stored %lld\n", l,
-             (long long)(tr[1 + 4 * l] - t0), tr[3 + 4 * l] > t0 ? (long long)(tr[3 + 4 * l] - t0) : -1LL,
-             tr[4 + 4 * l] > t0 ? (long long)(tr[4 + 4 * l] - t0) : -1LL);
-  (void)num_kb;
   return 0;
 }
