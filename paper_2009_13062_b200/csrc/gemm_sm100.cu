@@ -42,15 +42,50 @@ static int choose_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) 
   return s < 1 ? 1 : s;
 }
 
-int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
-  const int bn = pick_bn(T, N);
-  const int64_t tiles_a = T <= 256 ? (N + kGemmBM - 1) / kGemmBM : (T + kGemmBM - 1) / kGemmBM;
-  const int64_t tiles_b = T <= 256 ? (T + bn - 1) / bn : (N + bn - 1) / bn;
-  const int64_t tiles = G * tiles_a * tiles_b;
+// CTA pairs (cta_group::2): large-T tensor-bound tiles (128x256 per CTA,
+// 256x256 per pair: each SM loads half of B) and batch-1 weight-streaming
+// tiles (each SM loads 128 weight rows and half of the tokens). NF_GEMM_PAIR=0
+// disables them (A/B knob, read once).
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NF_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+struct LinearPlan {
+  bool swap, pair;
+  int bn;
+  int64_t tiles_a, tiles_b, tiles;  // tiles_a counts pair tiles (256 rows) when pair
+  int splits;
+};
+
+static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_t ws_bytes) {
+  LinearPlan L;
+  L.swap = T <= 256;
+  L.bn = pick_bn(T, N);
+  // Measured (tools/gemm_trace.cu): pairs cut the MMA's operand stalls on
+  // 128x256 tensor-bound tiles (4-5 stages of 32 KB per CTA instead of 3 of
+  // 48 KB); on batch-1 weight-streaming tiles they only add cluster-launch
+  // latency, so swapped tiles stay single-CTA.
+  L.pair = pair_enabled() && !L.swap && L.bn == 256;
+  const int64_t rows_a = L.swap ? N : T, rows_b = L.swap ? T : N;
+  const int rows_per_a = L.pair ? 2 * kGemmBM : kGemmBM;
+  L.tiles_a = (rows_a + rows_per_a - 1) / rows_per_a;
+  L.tiles_b = (rows_b + L.bn - 1) / L.bn;
+  L.tiles = G * L.tiles_a * L.tiles_b;
   const int kb_total = int((K + kGemmBK - 1) / kGemmBK);
-  const int s = choose_splits(tiles, kb_total, bn, INT64_MAX);
-  if (s <= 1) return 0;
-  return kCounterBytes + tiles * s * int64_t(kGemmBM) * bn * 4;
+  // split-K sizing works on per-CTA tiles (a pair unit occupies two SMs)
+  L.splits = choose_splits(L.pair ? 2 * L.tiles : L.tiles, kb_total, L.bn, ws_bytes);
+  return L;
+}
+
+int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
+  const LinearPlan L = plan_linear(G, T, K, N, INT64_MAX);
+  if (L.splits <= 1) return 0;
+  const int64_t cta_tiles = L.pair ? 2 * L.tiles : L.tiles;
+  return kCounterBytes + cta_tiles * L.splits * int64_t(kGemmBM) * L.bn * 4;
 }
 
 // Entry used by the C ABI. x rows at x + g*x_gs + t*x_ld (bf16); w (G, N, K)
@@ -74,19 +109,21 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.groups = int(G);
   p.y_direct = y;
   p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
-  const bool swap = T <= 256;
-  const int bn = pick_bn(T, N);
+  const LinearPlan L = plan_linear(G, T, K, N, ws ? ws_bytes : 0);
+  const bool swap = L.swap;
+  const int bn = L.bn;
+  const int bbox = L.pair ? bn / 2 : bn;  // B rows each CTA loads
   CUtensorMap ma, mb, my, mr;
   if (swap) {
     if (!make_bf16_map(&ma, w, G, N, K, kGemmBK, kGemmBM, 0, 0) ||
-        !make_bf16_map(&mb, x, G, T, K, kGemmBK, bn, x_ld, x_gs) ||
+        !make_bf16_map(&mb, x, G, T, K, kGemmBK, bbox, x_ld, x_gs) ||
         !make_bf16_map(&my, y, G, T, N, kOutBlock, bn, y_ld, y_gs))
       return NF_ERR_UNSUPPORTED;
     p.rows_a = int(N);
     p.rows_b = int(T);
   } else {
     if (!make_bf16_map(&ma, x, G, T, K, kGemmBK, kGemmBM, x_ld, x_gs) ||
-        !make_bf16_map(&mb, w, G, N, K, kGemmBK, bn, 0, 0) ||
+        !make_bf16_map(&mb, w, G, N, K, kGemmBK, bbox, 0, 0) ||
         !make_bf16_map(&my, y, G, T, N, kOutBlock, kGemmBM, y_ld, y_gs))
       return NF_ERR_UNSUPPORTED;
     p.rows_a = int(T);
@@ -97,16 +134,21 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
       !(swap ? make_bf16_map(&mr, residual, G, T, N, kOutBlock, bn, y_ld, y_gs)
              : make_bf16_map(&mr, residual, G, T, N, kOutBlock, kGemmBM, y_ld, y_gs)))
     return NF_ERR_UNSUPPORTED;
-  p.tiles_a = (p.rows_a + kGemmBM - 1) / kGemmBM;
-  p.tiles_b = (p.rows_b + bn - 1) / bn;
-  const int64_t tiles = G * p.tiles_a * int64_t(p.tiles_b);
-  p.splits = choose_splits(tiles, p.kb_total, bn, ws ? ws_bytes : 0);
+  p.tiles_a = int(L.tiles_a);
+  p.tiles_b = int(L.tiles_b);
+  const int64_t tiles = L.tiles;
+  p.splits = L.splits;
   p.kb_per_split = (p.kb_total + p.splits - 1) / p.splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
-  if (tiles * p.splits > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
+  if (tiles * p.splits * 2 > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
   p.units = int(tiles * p.splits);
   p.counters = static_cast<unsigned*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
+  if (L.pair) {
+    const int clusters = p.units < kNumSMs / 2 ? p.units : kNumSMs / 2;
+    const int grid = 2 * clusters;
+    return launch_tc_act<256, false, true>(act, ma, mb, my, mr, p, grid, stream);
+  }
   const int grid = p.units < kNumSMs ? p.units : kNumSMs;
 #define NF_TC(BNV, SW) return launch_tc_act<BNV, SW>(act, ma, mb, my, mr, p, grid, stream)
   if (swap) {

@@ -40,7 +40,14 @@ namespace nf {
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B row
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 192;  // TMA warp + MMA warp + 4 epilogue warps
+// Wide tiles get 8 epilogue warps (two per TMEM lane quarter, each taking
+// half of the columns): the GELU / residual epilogue of a 128x256 tile then
+// keeps up with the next tile's main loop.
+template <int BN>
+constexpr int epi_warps() { return BN >= 128 ? 8 : 4; }
+template <int BN, int GATHER>
+constexpr int gemm_threads() { return 64 + 32 * epi_warps<BN>() + (GATHER ? 128 : 0); }
 constexpr int kGatherThreads = 128;
 constexpr int kGatherLag = 8;  // cp.async groups in flight per gather thread
 constexpr int kOutBlock = 64;  // features per 128-byte output block (bf16)
@@ -64,7 +71,17 @@ NF_DEVICE unsigned long long gtimer() {
   do {                                                                          \
     if (blockIdx.x < 148) g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer();     \
   } while (0)
+// Stall accounting (ns spent in mbarrier waits, per CTA and role):
+// 0 producer<-empty, 1 mma<-full, 2 mma<-tempty, 3 epilogue<-tfull, 4 epilogue busy
+__device__ unsigned long long g_gemm_wait[148 * 8];
+#define NF_WAIT_BEGIN() const unsigned long long nf_w0_ = gtimer()
+#define NF_WAIT_END(slot)                                                       \
+  do {                                                                          \
+    if (blockIdx.x < 148) g_gemm_wait[blockIdx.x * 8 + (slot)] += gtimer() - nf_w0_; \
+  } while (0)
 #else
+#define NF_WAIT_BEGIN() do {} while (0)
+#define NF_WAIT_END(slot) do {} while (0)
 #define NF_TRACE(slot) \
   do {                 \
   } while (0)
@@ -106,18 +123,19 @@ struct GemmOut {
   static constexpr bool kStaged = BN >= 64 && !(NF_GEMM_DIRECT_SWAP && SWAP && BN <= 128);
 };
 
-template <int BN, bool SWAP>
+template <int BN, bool SWAP, bool PAIR = false>
 struct GemmCfg {
   static constexpr bool kStaged = GemmOut<BN, SWAP>::kStaged;
   static constexpr int kABytes = kGemmBM * kGemmBK * 2;
-  static constexpr int kBBytes = BN * kGemmBK * 2;
+  static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * kGemmBK * 2;  // pair: half of B each
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = kStaged ? kGemmBM * BN * 2 : 0;
   // Swapped tiles stream weights at batch 1: a small footprint lets the next
   // kernel's CTA (programmatic dependent launch) sit beside this one and
   // prefetch its own weights while this one drains.
   static constexpr int kBudgetKB =
-      BN >= 256 ? 220 : (SWAP && !kStaged ? NF_GEMM_LITE_KB : NF_GEMM_BUDGET_KB);
+      BN >= 256 ? (PAIR ? 225 : 220)
+                : (SWAP && !kStaged ? NF_GEMM_LITE_KB : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr size_t kBytes =
@@ -177,14 +195,19 @@ NF_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "me
 template <int N>
 NF_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER>
-__global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 1)
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER, bool PAIR>
+__global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     k_grouped_gemm_tc(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
                       const __grid_constant__ CUtensorMap map_y,
                       const __grid_constant__ CUtensorMap map_r, GemmParams p) {
-  using C = GemmCfg<BN, SWAP>;
+  using C = GemmCfg<BN, SWAP, PAIR>;
   constexpr int kStages = C::kStages;
+  static_assert(!(PAIR && GATHER), "CTA pairs take TMA operands only");
+  constexpr int kRowsA = PAIR ? 2 * kGemmBM : kGemmBM;  // A rows per unit
+  constexpr int kEpiWarps = epi_warps<BN>();
+  constexpr int kEpiThreads = 32 * kEpiWarps;
+  constexpr int kColsPerThread = BN * 4 / kEpiWarps;  // columns each epilogue thread drains
   // Residual tiles arrive by TMA into the output staging buffer (same
   // swizzled layout as the result), so the epilogue adds them from smem.
   constexpr bool kResTma = HAS_RES && C::kStaged;
@@ -206,6 +229,11 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) NF_TRACE(0);
+  // A pair walks the unit list together: cluster index / cluster count.
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int ubase = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int ustride = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -219,13 +247,17 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], PAIR ? 2 : kEpiThreads);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_slot, C::kTmemCols);
+    else tmem_alloc(tmem_slot, C::kTmemCols);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // peer signals the leader's barriers after this
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) NF_TRACE(1);
@@ -239,26 +271,34 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
       // CTAs: evict-last keeps them in L2.
       const uint64_t hint_a = SWAP ? kEvictFirst : kEvictLast;
       const uint64_t hint_b = SWAP ? kEvictLast : kEvictFirst;
-      constexpr uint32_t kTx = GATHER ? (SWAP ? C::kABytes : C::kBBytes) : C::kStageBytes;
+      // Pair: the leader's full barrier counts both CTAs' bytes.
+      constexpr uint32_t kTx = GATHER ? (SWAP ? C::kABytes : C::kBBytes)
+                                      : (PAIR ? 2 : 1) * C::kStageBytes;
+      auto tload = [&](uint8_t* dst, const CUtensorMap* map, int stage, int c0, int c1, int c2,
+                       uint64_t hint) {
+        if constexpr (PAIR) tma_load_3d_pair(dst, map, &full[stage], c0, c1, c2, hint);
+        else tma_load_3d(dst, map, &full[stage], c0, c1, c2, hint);
+      };
+      auto arm = [&](int stage) {
+        if (leader) mbar_arrive_expect_tx(&full[stage], kTx);
+      };
+      auto a_row = [&](const UnitCoord& c) { return c.ta * kRowsA + int(rank) * kGemmBM; };
+      auto b_row = [&](const UnitCoord& c) { return c.tb * BN + (PAIR ? int(rank) * (BN / 2) : 0); };
       auto load_w = [&](int stage, const UnitCoord& c, int kb) {
         if (SWAP)
-          tma_load_3d(sA + stage * C::kABytes, &map_a, &full[stage], kb * kGemmBK,
-                      c.ta * kGemmBM, c.g, hint_a);
+          tload(sA + stage * C::kABytes, &map_a, stage, kb * kGemmBK, a_row(c), c.g, hint_a);
         else
-          tma_load_3d(sB + stage * C::kBBytes, &map_b, &full[stage], kb * kGemmBK, c.tb * BN,
-                      c.g, hint_b);
+          tload(sB + stage * C::kBBytes, &map_b, stage, kb * kGemmBK, b_row(c), c.g, hint_b);
       };
       auto load_x = [&](int stage, const UnitCoord& c, int kb) {
         if (GATHER) return;  // gathered by warps 6..9
         if (SWAP)
-          tma_load_3d(sB + stage * C::kBBytes, &map_b, &full[stage], kb * kGemmBK, c.tb * BN,
-                      c.g, hint_b);
+          tload(sB + stage * C::kBBytes, &map_b, stage, kb * kGemmBK, b_row(c), c.g, hint_b);
         else
-          tma_load_3d(sA + stage * C::kABytes, &map_a, &full[stage], kb * kGemmBK,
-                      c.ta * kGemmBM, c.g, hint_a);
+          tload(sA + stage * C::kABytes, &map_a, stage, kb * kGemmBK, a_row(c), c.g, hint_a);
       };
       int it = 0;
-      int u = blockIdx.x;
+      int u = ubase;
       int pre = 0;
       if (u < p.units) {
         // Under programmatic dependent launch the weights do not depend on
@@ -267,7 +307,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
         const UnitCoord c = decode_unit(p, u, SWAP);
         pre = min(kStages, c.kb1 - c.kb0);
         for (int i = 0; i < pre; ++i) {
-          mbar_arrive_expect_tx(&full[i], kTx);
+          arm(i);
           load_w(i, c, c.kb0 + i);
         }
         if (!GATHER) grid_dependency_wait();
@@ -276,12 +316,16 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
       } else if (!GATHER) {
         grid_dependency_wait();
       }
-      for (; u < p.units; u += gridDim.x) {
+      for (; u < p.units; u += ustride) {
         const UnitCoord c = decode_unit(p, u, SWAP);
         for (int kb = c.kb0 + pre; kb < c.kb1; ++kb, ++it) {
           const int stage = it % kStages;
-          mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[stage], kTx);
+          {
+            NF_WAIT_BEGIN();
+            mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
+            NF_WAIT_END(0);
+          }
+          arm(stage);
           load_w(stage, c, kb);
           load_x(stage, c, kb);
         }
@@ -289,60 +333,97 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc_bf16_f32(kGemmBM, BN);
+    constexpr uint32_t idesc = make_idesc_bf16_f32(kRowsA, BN);
     int it = 0, local = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+    // Pair: only the leader issues (M=256 over both CTAs' smem / TMEM).
+    for (int u = leader ? ubase : p.units; u < p.units; u += ustride, ++local) {
       const UnitCoord c = decode_unit(p, u, SWAP);
       const int acc = local & 1;
-      mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+      {
+        NF_WAIT_BEGIN();
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        if (lane == 0) NF_WAIT_END(2);
+      }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
       for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
         const int stage = it % kStages;
-        mbar_wait(&full[stage], (it / kStages) & 1);
+        {
+          NF_WAIT_BEGIN();
+          mbar_wait(&full[stage], (it / kStages) & 1);
+          if (lane == 0) NF_WAIT_END(1);
+        }
         tc_fence_after();
         if (lane == 0 && it == 0) NF_TRACE(2);
         if (lane == 0) {
           const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
           const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
-          for (int kk = 0; kk < kGemmBK / 16; ++kk)
-            umma_f16_ss(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
-                        make_sw128_kmajor_desc(b_base + kk * 32), idesc,
-                        (kb != c.kb0 || kk != 0) ? 1u : 0u);
-          umma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          for (int kk = 0; kk < kGemmBK / 16; ++kk) {
+            if constexpr (PAIR)
+              umma_f16_ss_pair(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
+                               make_sw128_kmajor_desc(b_base + kk * 32), idesc,
+                               (kb != c.kb0 || kk != 0) ? 1u : 0u);
+            else
+              umma_f16_ss(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
+                          make_sw128_kmajor_desc(b_base + kk * 32), idesc,
+                          (kb != c.kb0 || kk != 0) ? 1u : 0u);
+          }
+          // frees the smem slot (both CTAs' halves) once these MMAs retire
+          if constexpr (PAIR) umma_commit_pair(&empty[stage]);
+          else umma_commit(&empty[stage]);
         }
         __syncwarp();
       }
-      if (lane == 0) umma_commit(&tfull[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) umma_commit_pair(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
+      }
       __syncwarp();
     }
     if (lane == 0) NF_TRACE(3);
-  } else if (warp < 6) {
+  } else if (warp < 2 + kEpiWarps) {
     // ------------------------------ epilogue ------------------------------
-    const int quarter = warp & 3;
+    const int quarter = warp & 3;         // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;  // accumulator row == TMEM lane
-    const int etid = threadIdx.x - 64;    // 0..127
+    const int etid = threadIdx.x - 64;    // 0 .. kEpiThreads-1
+    const int col0 = ((warp - 2) >> 2) * kColsPerThread;  // this thread's column range
     const uint32_t stage_base = smem_u32(sOut);
     uint32_t res_phase = 0;
     int local = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+    // Hand an accumulator buffer back to the MMA issuer (the leader's barrier
+    // collects one arrival per CTA in pair mode).
+    auto release_acc = [&](int acc) {
+      tc_fence_before();
+      if constexpr (PAIR) {
+        named_bar_sync(1, kEpiThreads);
+        if (etid == 0) mbar_arrive_leader(&tempty[acc]);
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
+    };
+    for (int u = ubase; u < p.units; u += ustride, ++local) {
       const UnitCoord c = decode_unit(p, u, SWAP);
       const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      {
+        NF_WAIT_BEGIN();
+        mbar_wait(&tfull[acc], (local >> 1) & 1);
+        if (etid == 0) NF_WAIT_END(3);
+      }
       tc_fence_after();
       if (etid == 0 && local == 0) NF_TRACE(4);
       const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-      const int m0 = c.ta * kGemmBM, n0 = c.tb * BN;
+      const int m0 = c.ta * kRowsA + int(rank) * kGemmBM, n0 = c.tb * BN;
+      const int wtile = PAIR ? c.tile * 2 + int(rank) : c.tile;  // this CTA's 128-row tile
       float* part = nullptr;
       if (p.splits > 1) {
         // Publish this split's fp32 partial; the last arriver reduces.
         // Partials are stored column-major over TMEM lanes ([col][row]):
         // each warp store covers one contiguous 128-byte line.
-        part = p.ws + (int64_t(c.tile) * p.splits) * kGemmBM * BN;
+        part = p.ws + (int64_t(wtile) * p.splits) * kGemmBM * BN;
         float* mine = part + int64_t(c.s) * kGemmBM * BN + row;
 #pragma unroll 1
-        for (int cc = 0; cc < BN; cc += EC) {
+        for (int cc = col0; cc < col0 + kColsPerThread; cc += EC) {
           uint32_t r[EC];
           tmem_ld_cols<EC>(t_row + uint32_t(cc), r);
           tmem_ld_wait();
@@ -350,12 +431,11 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
           for (int j = 0; j < EC; ++j) __stcg(mine + (cc + j) * kGemmBM, __uint_as_float(r[j]));
         }
         __threadfence();
-        named_bar_sync(1, 128);
-        if (etid == 0) *last_flag = (atomicAdd(p.counters + c.tile, 1u) == unsigned(p.splits - 1));
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
+        if (etid == 0) *last_flag = (atomicAdd(p.counters + wtile, 1u) == unsigned(p.splits - 1));
+        named_bar_sync(1, kEpiThreads);
         if (!*last_flag) {
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          release_acc(acc);
           continue;
         }
         __threadfence();
@@ -386,7 +466,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
       }
       const float* bias = p.bias ? p.bias + int64_t(c.g) * p.features : nullptr;
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += EC) {
+      for (int cc = col0; cc < col0 + kColsPerThread; cc += EC) {
         float v[EC];
         {
           uint32_t r[EC];
@@ -531,11 +611,10 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
         }
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      release_acc(acc);
       if constexpr (C::kStaged) {
         fence_proxy_async_smem();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
         if (etid == 0) {
           if (!SWAP) {
 #pragma unroll
@@ -547,14 +626,14 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
               tma_store_3d(&map_y, sOut + b * BN * 128, m0 + b * kOutBlock, n0, c.g);
           }
           bulk_commit();
-          if (p.splits > 1) p.counters[c.tile] = 0u;  // re-arm for the next launch
+          if (p.splits > 1) p.counters[wtile] = 0u;  // re-arm for the next launch
           bulk_wait_read0();                          // staging reusable
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1, kEpiThreads);
       } else {
         if (p.splits > 1) {
-          named_bar_sync(1, 128);
-          if (etid == 0) p.counters[c.tile] = 0u;
+          named_bar_sync(1, kEpiThreads);
+          if (etid == 0) p.counters[wtile] = 0u;
         }
       }
     }
@@ -569,7 +648,7 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
     // Arrivals trail the issue by LAG iterations; LAG < kStages or the
     // producer would wait on a slot whose fill it has not yet published.
     constexpr int LAG = kGatherLag < kStages - 1 ? kGatherLag : kStages - 1;
-    const int gt = threadIdx.x - kGemmThreads;
+    const int gt = threadIdx.x - (64 + kEpiThreads);
     const int j = gt % CPR;
     const int r0 = gt / CPR;
     const uint32_t act_smem = smem_u32(SWAP ? sB : sA);
@@ -633,10 +712,12 @@ __global__ void __launch_bounds__(kGemmThreads + (GATHER ? kGatherThreads : 0), 
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the leader's MMAs into the peer's TMEM are done
   if (threadIdx.x == 0) NF_TRACE(6);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::kTmemCols);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, C::kTmemCols);
+    else tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
@@ -667,11 +748,11 @@ inline EncodeTiledFn encode_fn() {
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0>
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0, bool PAIR = false>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
-  using C = GemmCfg<BN, SWAP>;
-  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER>;
+  using C = GemmCfg<BN, SWAP, PAIR>;
+  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR>;
   static bool attr_done = false;  // idempotent attribute set; benign race
   if (!attr_done) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kBytes));
@@ -679,35 +760,47 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads + (GATHER ? kGatherThreads : 0));
+  cfg.blockDim = dim3(gemm_threads<BN, GATHER>());
   cfg.dynamicSmemBytes = C::kBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (PAIR) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled();
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, mr, p);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 
-template <int BN, bool SWAP, int ACT, int GATHER = 0>
+template <int BN, bool SWAP, int ACT, int GATHER = 0, bool PAIR = false>
 static int launch_tc_res(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                          const CUtensorMap& mr, const GemmParams& p, int grid,
                          cudaStream_t stream) {
-  if (p.residual) return launch_tc<BN, SWAP, ACT, true, GATHER>(ma, mb, my, mr, p, grid, stream);
-  return launch_tc<BN, SWAP, ACT, false, GATHER>(ma, mb, my, mr, p, grid, stream);
+  if (p.residual)
+    return launch_tc<BN, SWAP, ACT, true, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
+  return launch_tc<BN, SWAP, ACT, false, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
 }
 
-template <int BN, bool SWAP>
+template <int BN, bool SWAP, bool PAIR = false>
 static int launch_tc_act(int act, const CUtensorMap& ma, const CUtensorMap& mb,
                          const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
                          int grid, cudaStream_t stream) {
   switch (act) {
-    case NF_ACT_RELU: return launch_tc_res<BN, SWAP, NF_ACT_RELU>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_GELU: return launch_tc_res<BN, SWAP, NF_ACT_GELU>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_TANH: return launch_tc_res<BN, SWAP, NF_ACT_TANH>(ma, mb, my, mr, p, grid, stream);
-    default: return launch_tc_res<BN, SWAP, NF_ACT_NONE>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_RELU: return launch_tc_res<BN, SWAP, NF_ACT_RELU, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_GELU: return launch_tc_res<BN, SWAP, NF_ACT_GELU, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_TANH: return launch_tc_res<BN, SWAP, NF_ACT_TANH, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
+    default: return launch_tc_res<BN, SWAP, NF_ACT_NONE, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
   }
 }
 

@@ -20,7 +20,10 @@ def _call_linear(x, w_nk, bias, residual, y, act, mode, dtype_code, w_layout=_li
 
 
 @pytest.mark.parametrize("G,T,K,N", [(2, 128, 768, 768), (3, 64, 256, 384), (2, 512, 512, 1024),
-                                     (1, 200, 320, 200), (4, 16, 128, 96), (2, 300, 192, 130)])
+                                     (1, 200, 320, 200), (4, 16, 128, 96), (2, 300, 192, 130),
+                                     # CTA-pair tiles: persistent loop, partial pair tiles
+                                     (8, 1024, 768, 1024), (3, 700, 256, 512),
+                                     (8, 128, 3072, 768), (5, 100, 512, 1000)])
 @pytest.mark.parametrize("act", [_lib.NF_ACT_NONE, _lib.NF_ACT_GELU])
 def test_tc_linear_bf16_vs_torch(G, T, K, N, act):
     torch.manual_seed(0)

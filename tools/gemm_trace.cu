@@ -46,6 +46,16 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(tr.data(), nf::g_gemm_trace, sizeof(unsigned long long) * 148 * 8);
     cudaMemcpyFromSymbol(&t0, g_stamp, sizeof(t0));
     printf("G=%d T=%d K=%d N=%d workspace=%lld\n", G, T, K, N, (long long)ws_bytes);
+    {
+      std::vector<unsigned long long> wt(148 * 8);
+      cudaMemcpyFromSymbol(wt.data(), nf::g_gemm_wait, sizeof(unsigned long long) * 148 * 8);
+      const char* wn[4] = {"prod<-empty", "mma<-full", "mma<-tempty", "epi<-tfull"};
+      for (int s = 0; s < 4; ++s) {
+        double tot = 0, mx = 0;
+        for (int b = 0; b < 148; ++b) { tot += wt[b * 8 + s]; mx = std::max(mx, double(wt[b * 8 + s])); }
+        printf("  wait %-12s mean %8.2f us  max %8.2f us (summed over 3 runs)\n", wn[s], tot / 148 * 1e-3, mx * 1e-3);
+      }
+    }
     for (int s = 0; s < 7; ++s) {
       std::vector<double> v;
       for (int b = 0; b < 148; ++b)
