@@ -154,6 +154,16 @@ NF_DEVICE void tma_load_4d(void* smem_dst, const CUtensorMap* map, uint64_t* bar
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (TMA engine, no tensor map), completing
+// `bytes` (multiple of 16, 16-byte aligned both sides) on an mbarrier.
+NF_DEVICE void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // TMA bulk-tensor store smem -> global (bulk-group completion).
 NF_DEVICE void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
   asm volatile(

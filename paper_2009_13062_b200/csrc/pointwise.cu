@@ -306,6 +306,157 @@ __global__ void __launch_bounds__(256) k_group_norm(const T* __restrict__ x,
   }
 }
 
+// Streaming variant for many rows (bf16): each warp walks a contiguous range
+// of (row, group) units; lane 0 keeps kNormDepth units of x (and residual) in
+// flight with 1-D TMA bulk copies into a per-warp shared-memory ring, so the
+// registers hold only the affine (kept until the per-instance affine block
+// changes) and the row being reduced. HBM-bound: 2 reads + 1 write.
+constexpr int kNormDepth = 4;
+constexpr int kNormWarps = 8;
+constexpr int kNormRowBytes = 1536;  // Cg <= 768 bf16
+
+template <int Q>
+__global__ void __launch_bounds__(kNormWarps * 32, 2)
+    k_group_norm_tma(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
+                     const float* __restrict__ gamma, const float* __restrict__ beta,
+                     __nv_bfloat16* __restrict__ y, NormGeom g, int units_per_warp) {
+  constexpr int V = 8;
+  extern __shared__ __align__(128) uint8_t nsm[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int warp_id = int(blockIdx.x) * kNormWarps + wib;
+  const bool has_res = res != nullptr;
+  uint8_t* ring = nsm + size_t(wib) * kNormDepth * 2 * kNormRowBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(nsm + size_t(kNormWarps) * kNormDepth * 2 *
+                                               kNormRowBytes) + wib * kNormDepth;
+  const int G = int(g.G), R2 = int(g.R2);
+  const int units = int(g.R1) * R2 * G;
+  const int Cg = int(g.Cg);
+  const int nchunks = Cg / V;
+  const uint32_t row_bytes = uint32_t(Cg) * 2u;
+  const int u0 = warp_id * units_per_warp;
+  const int u1 = min(units, u0 + units_per_warp);
+  if (lane == 0)
+    for (int d = 0; d < kNormDepth; ++d) mbar_init(&bars[d], 1);
+  fence_barrier_init();
+  __syncwarp();
+  grid_dependents_launch();
+  auto base_of = [&](int u) {
+    const int row = u / G, grp = u - (u / G) * G;
+    const int r1 = row / R2, r2 = row - r1 * R2;
+    return int64_t(r1) * g.s1 + int64_t(r2) * g.s2 + int64_t(grp) * g.sg;
+  };
+  auto aff_of = [&](int u) {
+    const int row = u / G, grp = u - (u / G) * G;
+    return (g.rows_per_affine > 0 ? int64_t(row / int(g.rows_per_affine)) : 0) * g.G * g.Cg +
+           int64_t(grp) * Cg;
+  };
+  float ga[Q * V], be[Q * V];
+  int64_t aff_cur = -1;
+  auto load_affine = [&](int64_t aff) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < nchunks) {
+#pragma unroll
+        for (int e = 0; e < V; e += 4) {
+          const float4 a4 = __ldg(reinterpret_cast<const float4*>(gamma + aff + ch * V + e));
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + aff + ch * V + e));
+          ga[q * V + e] = a4.x; ga[q * V + e + 1] = a4.y; ga[q * V + e + 2] = a4.z;
+          ga[q * V + e + 3] = a4.w;
+          be[q * V + e] = b4.x; be[q * V + e + 1] = b4.y; be[q * V + e + 2] = b4.z;
+          be[q * V + e + 3] = b4.w;
+        }
+      }
+    }
+    aff_cur = aff;
+  };
+  if (u0 < u1) load_affine(aff_of(u0));  // a weight: before the dependency wait
+  grid_dependency_wait();
+  if (u0 >= u1) return;
+  auto issue = [&](int u) {
+    const int slot = (u - u0) % kNormDepth;
+    const int64_t b = base_of(u);
+    uint8_t* dst = ring + size_t(slot) * 2 * kNormRowBytes;
+    mbar_arrive_expect_tx(&bars[slot], has_res ? 2 * row_bytes : row_bytes);
+    bulk_load_1d(dst, x + b, row_bytes, &bars[slot]);
+    if (has_res) bulk_load_1d(dst + kNormRowBytes, res + b, row_bytes, &bars[slot]);
+  };
+  if (lane == 0)
+    for (int u = u0; u < min(u1, u0 + kNormDepth); ++u) issue(u);
+  for (int u = u0; u < u1; ++u) {
+    const int k = u - u0;
+    const int slot = k % kNormDepth;
+    mbar_wait(&bars[slot], uint32_t(k / kNormDepth) & 1u);
+    const uint8_t* sx = ring + size_t(slot) * 2 * kNormRowBytes;
+    uint4 ux[Q], ur[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < nchunks) {
+        ux[q] = *reinterpret_cast<const uint4*>(sx + ch * 16);
+        if (has_res) ur[q] = *reinterpret_cast<const uint4*>(sx + kNormRowBytes + ch * 16);
+      }
+    }
+    __syncwarp();  // every lane has its chunks: the slot can be refilled
+    if (lane == 0 && u + kNormDepth < u1) {
+      fence_proxy_async_smem();  // generic reads of the slot before the async refill
+      issue(u + kNormDepth);
+    }
+    const int64_t aff = aff_of(u);
+    if (aff != aff_cur) load_affine(aff);
+    // one pass: sum and sum of squares (fp32; |x| ~ O(1) activations)
+    float v[Q * V];
+    float sum = 0.f, sq = 0.f;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (lane + 32 * q < nchunks) {
+        const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&ux[q]);
+        const __nv_bfloat162* pr = reinterpret_cast<const __nv_bfloat162*>(&ur[q]);
+#pragma unroll
+        for (int e = 0; e < V / 2; ++e) {
+          float2 t = __bfloat1622float2(px[e]);
+          if (has_res) {
+            const float2 r2 = __bfloat1622float2(pr[e]);
+            t.x = __fadd_rn(t.x, r2.x);
+            t.y = __fadd_rn(t.y, r2.y);
+          }
+          v[q * V + 2 * e] = t.x;
+          v[q * V + 2 * e + 1] = t.y;
+          sum += t.x + t.y;
+          sq = fmaf(t.x, t.x, fmaf(t.y, t.y, sq));
+        }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    }
+    const float inv_c = 1.0f / float(Cg);
+    const float mean = sum * inv_c;
+    const float var = fmaxf(fmaf(-mean, mean, sq * inv_c), 0.f);
+    const float rstd = rsqrtf(var + g.eps);
+    const int64_t b = base_of(u);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < nchunks) {
+        uint4 uo;
+        uint32_t* po = reinterpret_cast<uint32_t*>(&uo);
+#pragma unroll
+        for (int e = 0; e < V / 2; ++e) {
+          const int i0 = q * V + 2 * e;
+          const float a0 = ga[i0] * rstd, a1 = ga[i0 + 1] * rstd;
+          po[e] = pack_bf16x2(fmaf(v[i0] - mean, a0, be[i0]), fmaf(v[i0 + 1] - mean, a1, be[i0 + 1]));
+        }
+        *reinterpret_cast<uint4*>(y + b + int64_t(ch) * V) = uo;
+      }
+    }
+  }
+}
+constexpr size_t kNormTmaSmem =
+    size_t(kNormWarps) * kNormDepth * 2 * kNormRowBytes + kNormWarps * kNormDepth * 8;
+
 int group_norm(const void* x, const void* residual, const float* gamma, const float* beta,
                void* y, const NormGeomC& gc, int dtype, cudaStream_t s) {
   NormGeom g{gc.R1, gc.R2, gc.s1, gc.s2, gc.G, gc.Cg, gc.sg, gc.sc, gc.rows_per_affine, gc.eps};
@@ -324,7 +475,23 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     auto* pr = static_cast<const __nv_bfloat16*>(residual);
     auto* py = static_cast<__nv_bfloat16*>(y);
     const int q = int((g.Cg / 8 + 31) / 32);
-    if (vec && q == 1) launch_pdl(k_group_norm_vec<__nv_bfloat16, 1>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
+    if (vec && q <= 3 && units >= 4 * 148 * 16) {
+      // enough rows for each warp of 2 resident blocks per SM to stream several
+      static bool attr_done = false;
+      if (!attr_done) {
+        cudaFuncSetAttribute(k_group_norm_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNormTmaSmem));
+        cudaFuncSetAttribute(k_group_norm_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNormTmaSmem));
+        cudaFuncSetAttribute(k_group_norm_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNormTmaSmem));
+        attr_done = true;
+      }
+      const int warps = 148 * 2 * kNormWarps;
+      const int per = int((units + warps - 1) / warps);
+      const int nw = int((units + per - 1) / per);
+      const int sgrid = (nw + kNormWarps - 1) / kNormWarps;
+      if (q == 1) launch_pdl(k_group_norm_tma<1>, dim3(sgrid), dim3(kNormWarps * 32), kNormTmaSmem, s, px, pr, gamma, beta, py, g, per);
+      else if (q == 2) launch_pdl(k_group_norm_tma<2>, dim3(sgrid), dim3(kNormWarps * 32), kNormTmaSmem, s, px, pr, gamma, beta, py, g, per);
+      else launch_pdl(k_group_norm_tma<3>, dim3(sgrid), dim3(kNormWarps * 32), kNormTmaSmem, s, px, pr, gamma, beta, py, g, per);
+    } else if (vec && q == 1) launch_pdl(k_group_norm_vec<__nv_bfloat16, 1>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else if (vec && q == 2) launch_pdl(k_group_norm_vec<__nv_bfloat16, 2>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else if (vec && q == 3) launch_pdl(k_group_norm_vec<__nv_bfloat16, 3>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else if (vec) launch_pdl(k_group_norm_vec<__nv_bfloat16, 4>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);

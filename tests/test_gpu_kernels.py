@@ -143,6 +143,19 @@ def test_group_norm_layouts_and_residual(dtype):
     assert normwise(got, want) < (2e-2 if dtype == torch.bfloat16 else 1e-5)
 
 
+def test_group_norm_streaming_many_rows():
+    """Enough rows for the streaming (contiguous row range per warp) kernel."""
+    rng = np.random.default_rng(8)
+    x = OK.bf16_round(rng.uniform(-1, 1, (4, 1024, 4 * 768)).astype(np.float32))
+    r = OK.bf16_round(rng.uniform(-1, 1, x.shape).astype(np.float32))
+    gam = rng.uniform(.5, 1.5, 4 * 768).astype(np.float32)
+    bet = rng.uniform(-.5, .5, 4 * 768).astype(np.float32)
+    want = OK.group_norm(x + r, gam, bet, groups=4, eps=1e-12)
+    got = host(GK.group_norm(cuda(x, torch.bfloat16), cuda(gam), cuda(bet), groups=4, eps=1e-12,
+                             residual=cuda(r, torch.bfloat16)))
+    assert normwise(got, want) < 2e-2
+
+
 def test_softmax_axes_and_stability():
     x = np.random.default_rng(1).uniform(-30, 30, (3, 17, 40)).astype(np.float32)
     for ax in (-1, 1, 0):
