@@ -57,10 +57,26 @@ NF_DEVICE float apply_act(float v, int act) {
   }
 }
 
+// GELU for the bf16 tensor-core epilogues: the tanh form on MUFU.TANH (one
+// SFU op instead of erf's exp + reciprocal). |gelu_tanh - gelu_erf| <= 4.8e-4
+// over the reals (at x ~ 2.7, i.e. 2e-4 relative), and tanh.approx adds
+// <= 2^-11 relative: both far below the bf16 output rounding (2^-9), so the
+// result is the erf GELU at bf16 precision. fp32 / exact paths use gelu_erf.
+NF_DEVICE float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+NF_DEVICE float gelu_bf16_epilogue(float x) {
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_approx(u), hx);
+}
+
 template <int ACT>
 NF_DEVICE float act_t(float v) {
   if constexpr (ACT == NF_ACT_RELU) return fmaxf(v, 0.0f);
-  else if constexpr (ACT == NF_ACT_GELU) return gelu_erf(v);
+  else if constexpr (ACT == NF_ACT_GELU) return gelu_bf16_epilogue(v);
   else if constexpr (ACT == NF_ACT_TANH) return tanhf(v);
   else return v;
 }

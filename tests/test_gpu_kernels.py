@@ -107,7 +107,8 @@ def test_grouped_conv_exact_criterion1_generator(seed):
         assert packed[:, j * c_out:(j + 1) * c_out].tobytes() == solo.tobytes()
 
 
-@pytest.mark.parametrize("bt,s,h", [(8, 128, 12), (3, 77, 4), (2, 128, 2), (5, 16, 3)])
+@pytest.mark.parametrize("bt,s,h", [(8, 128, 12), (3, 77, 4), (2, 128, 2), (5, 16, 3),
+                                    (64, 128, 12), (100, 77, 4)])  # persistent kernel
 def test_attention_tensor_core_vs_oracle(bt, s, h):
     rng = np.random.default_rng(bt * s + h)
     d = 64 * h

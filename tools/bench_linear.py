@@ -22,6 +22,9 @@ SHAPES = {
     "xlnet_b4_ff1": (32, 512, 768, 3072),
     "xlnet_b4_ff2": (32, 512, 3072, 768),
     "bert_b8_ff1": (32, 1024, 768, 3072),
+    "bert_b8_ff1_gelu": (32, 1024, 768, 3072),
+    "bert_b8_qkv": (32, 1024, 768, 2304),
+    "bert_b8_ff2": (32, 1024, 3072, 768),
 }
 
 
