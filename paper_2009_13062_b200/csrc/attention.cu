@@ -562,8 +562,16 @@ __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restr
 // ---------------------------------------------------------------------------
 constexpr int kRelPitch = 68;                           // words per staged row
 constexpr int kRelStageBytes = 4 * 32 * kRelPitch * 4;  // 34816 B (4 warps)
-constexpr size_t kRelSmem = 1024 + 2 * kTileBytes + 4096 + kTileBytes + 2 * kTileBytes +
-                            (128 + 256 + 128) * 4 + 64;
+inline bool rel_persistent() {
+  static const bool on = [] {
+    const char* e = getenv("NF_REL_PERSISTENT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+constexpr size_t kRelBufBytes = 2 * kTileBytes + 4096 + kTileBytes + 2 * kTileBytes;
+template <int NBUF>
+constexpr size_t rel_smem() { return 1024 + NBUF * kRelBufBytes + (128 + 256 + 128) * 4 + 64; }
 
 // positional keys r viewed as 4-D (dh, H, 2S, Bt); box (64, 1, 128, 1).
 bool make_r_map(CUtensorMap* map, const void* r, int64_t Bt, int64_t S, int64_t H) {
@@ -596,41 +604,37 @@ __device__ __forceinline__ float bias_dot_row(const uint8_t* tile, int row, cons
   return acc;
 }
 
-__global__ void __launch_bounds__(128, 2)
+template <int NBUF>
+__global__ void __launch_bounds__(128, NBUF == 1 ? 2 : 1)
     k_rel_attention_tc(const __grid_constant__ CUtensorMap map_qkv,
                        const __grid_constant__ CUtensorMap map_r, const float* __restrict__ rwb,
                        const float* __restrict__ rrb, __nv_bfloat16* __restrict__ out, int H,
-                       int seqs_per_bias, float scale_log2) {
+                       int seqs_per_bias, int units, float scale_log2) {
+  // NBUF == 2: persistent over units with the next unit's tiles loading into
+  // the other buffer while this one computes (one CTA per SM).
   constexpr int S = kAttnS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kTileBytes;
-  uint8_t* sStage = sQ;  // Q | K | 4 KB pad, reused after the raw MMA retired
-  uint8_t* sV = sK + kTileBytes + 4096;
-  uint8_t* sKR = sV + kTileBytes;  // 256 rows; later P (128 x 128, 2 k-blocks)
-  float* sBw = reinterpret_cast<float*>(sKR + 2 * kTileBytes);
+  float* sBw = reinterpret_cast<float*>(smem + NBUF * kRelBufBytes);
   float* sCr = sBw + 128;
   float* sRb = sCr + 256;  // r_w_bias | r_r_bias of this (instance, head)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sRb + 128);
-  uint64_t* bar_load = bars;
-  uint64_t* bar_s = bars + 1;
-  uint64_t* bar_bd = bars + 2;
-  uint64_t* bar_o = bars + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* bar_load = bars;  // [2]
+  uint64_t* bar_s = bars + 2;
+  uint64_t* bar_bd = bars + 3;
+  uint64_t* bar_o = bars + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
-  const int bt = blockIdx.x / H;
-  const int h = blockIdx.x % H;
-  const int inst = bt / seqs_per_bias;
 
   if (tid == 0) {
     tma_prefetch_desc(&map_qkv);
     tma_prefetch_desc(&map_r);
-    mbar_init(bar_load, 1);
+    mbar_init(&bar_load[0], 1);
+    mbar_init(&bar_load[1], 1);
     mbar_init(bar_s, 1);
     mbar_init(bar_bd, 1);
     mbar_init(bar_o, 1);
@@ -643,19 +647,41 @@ __global__ void __launch_bounds__(128, 2)
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
 
+  auto issue = [&](int u, int buf) {
+    uint8_t* q = smem + buf * kRelBufBytes;
+    uint8_t* k = q + kTileBytes;
+    uint8_t* v = k + kTileBytes + 4096;
+    uint8_t* kr = v + kTileBytes;
+    const int bt = u / H, h = u % H;
+    mbar_arrive_expect_tx(&bar_load[buf], 5 * kTileBytes);
+    tma_load_4d(q, &map_qkv, &bar_load[buf], 0, h, 0, bt, kEvictFirst);
+    tma_load_4d(k, &map_qkv, &bar_load[buf], 0, H + h, 0, bt, kEvictFirst);
+    tma_load_4d(v, &map_qkv, &bar_load[buf], 0, 2 * H + h, 0, bt, kEvictFirst);
+    tma_load_4d(kr, &map_r, &bar_load[buf], 0, h, 0, bt, kEvictFirst);
+    tma_load_4d(kr + kTileBytes, &map_r, &bar_load[buf], 0, h, S, bt, kEvictFirst);
+  };
   if (tid == 0) {
     grid_dependency_wait();
-    mbar_arrive_expect_tx(bar_load, 5 * kTileBytes);
-    tma_load_4d(sQ, &map_qkv, bar_load, 0, h, 0, bt, kEvictFirst);
-    tma_load_4d(sK, &map_qkv, bar_load, 0, H + h, 0, bt, kEvictFirst);
-    tma_load_4d(sV, &map_qkv, bar_load, 0, 2 * H + h, 0, bt, kEvictFirst);
-    tma_load_4d(sKR, &map_r, bar_load, 0, h, 0, bt, kEvictFirst);
-    tma_load_4d(sKR + kTileBytes, &map_r, bar_load, 0, h, S, bt, kEvictFirst);
+    if (int(blockIdx.x) < units) issue(blockIdx.x, 0);
   }
   grid_dependents_launch();
+
+  int it = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+  const int buf = NBUF == 2 ? (it & 1) : 0;
+  const uint32_t ph = uint32_t(it) & 1u;
+  uint8_t* sQ = smem + buf * kRelBufBytes;
+  uint8_t* sK = sQ + kTileBytes;
+  uint8_t* sStage = sQ;  // Q | K | 4 KB pad, reused after the raw MMA retired
+  uint8_t* sV = sK + kTileBytes + 4096;
+  uint8_t* sKR = sV + kTileBytes;  // 256 rows; later P (128 x 128, 2 k-blocks)
+  const int bt = u / H;
+  const int h = u % H;
+  const int inst = bt / seqs_per_bias;
+  if (NBUF == 2 && tid == 0 && u + int(gridDim.x) < units) issue(u + gridDim.x, buf ^ 1);
   const float* bw_src = rwb + (int64_t(inst) * H + h) * kAttnD;
   const float* br_src = rrb + (int64_t(inst) * H + h) * kAttnD;
-  mbar_wait(bar_load, 0);
+  mbar_wait(&bar_load[buf], NBUF == 2 ? (uint32_t(it >> 1) & 1u) : ph);
 
   if (tid == 0) {
     tc_fence_after();
@@ -680,7 +706,7 @@ __global__ void __launch_bounds__(128, 2)
   sCr[tid] = bias_dot_row(sKR, tid, sRb + 64);
   sCr[tid + 128] = bias_dot_row(sKR, tid + 128, sRb + 64);
 
-  mbar_wait(bar_s, 0);
+  mbar_wait(bar_s, ph);
   tc_fence_after();
   uint32_t r[4][32];  // AC row of this query
 #pragma unroll
@@ -706,7 +732,7 @@ __global__ void __launch_bounds__(128, 2)
     for (int j = 0; j < 32; ++j)
       r[c][j] = __float_as_uint(__uint_as_float(r[c][j]) + sBw[c * 32 + j]);
 
-  mbar_wait(bar_bd, 0);
+  mbar_wait(bar_bd, ph);
   tc_fence_after();
   // Rel-shift through the per-warp staging window.
   const uint32_t stage_w = smem_u32(sStage) + uint32_t(warp * 32 * kRelPitch * 4);
@@ -788,7 +814,7 @@ __global__ void __launch_bounds__(128, 2)
     }
     umma_commit(bar_o);
   }
-  mbar_wait(bar_o, 0);
+  mbar_wait(bar_o, ph);
   tc_fence_after();
   {
     uint32_t o[2][32];
@@ -811,7 +837,9 @@ __global__ void __launch_bounds__(128, 2)
       }
   }
   tc_fence_before();
-  __syncthreads();
+  __syncthreads();  // TMEM, smem and bias vectors free for the next unit
+  if (NBUF == 1 && tid == 0 && u + int(gridDim.x) < units) issue(u + gridDim.x, 0);
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
@@ -835,24 +863,26 @@ int rel_attention(const void* qkv, const void* r, const float* rwb, const float*
     if (!make_qkv_map(&mq, qkv, Bt, S, H) || !make_r_map(&mr, r, Bt, S, H)) return NF_ERR_LAUNCH;
     static bool attr_done = false;
     if (!attr_done) {
-      cudaFuncSetAttribute(k_rel_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(kRelSmem));
+      cudaFuncSetAttribute(k_rel_attention_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(rel_smem<1>()));
+      cudaFuncSetAttribute(k_rel_attention_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(rel_smem<2>()));
       attr_done = true;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(Bt * H));
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = kRelSmem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled();
+    const int units = int(Bt * H);
     const float scale_log2 = scale * 1.4426950408889634f;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_rel_attention_tc, mq, mr, rwb, rrb,
-                                       static_cast<__nv_bfloat16*>(out), int(H),
-                                       int(seqs_per_bias), scale_log2);
+    cudaError_t e;
+    // The persistent double-buffered variant (NBUF = 2, one CTA per SM)
+    // measured slower (92 vs 79 us per XLNet-base layer at 1536 units) than
+    // two single-buffered CTAs per SM, whose chains overlap each other.
+    if (units > 2 * kNumSMs && rel_persistent())
+      e = launch_pdl(k_rel_attention_tc<2>, dim3(kNumSMs), dim3(128), rel_smem<2>(), stream, mq,
+                     mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
+                     units, scale_log2);
+    else
+      e = launch_pdl(k_rel_attention_tc<1>, dim3(units), dim3(128), rel_smem<1>(), stream, mq,
+                     mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
+                     units, scale_log2);
     return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
   }
   const int64_t warps = Bt * H * S;
