@@ -31,13 +31,23 @@ static int pick_bn(int64_t T, int64_t N) {
 
 // Split-K factor: enough units to cover the SMs when the tile count is low,
 // with at least 4 K blocks per split and a workspace that fits.
+// Minimum K blocks per split (debug knob NF_SPLITK_MINKB, read once).
+static int splitk_min_kb() {
+  static const int v = [] {
+    const char* e = getenv("NF_SPLITK_MINKB");
+    return e ? atoi(e) : 16;
+  }();
+  return v < 1 ? 1 : v;
+}
+
 static int choose_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) {
   if (ws_bytes <= kCounterBytes || tiles >= 100 || tiles > kCounterBytes / 4) return 1;
   int s = int(kNumSMs / tiles);
   s = s < kMaxSplits ? s : kMaxSplits;
   // Each split adds a partial write + reduction to the critical path; only
   // worth it when every split still streams a long K range.
-  s = s < kb_total / 64 ? s : kb_total / 64;
+  const int cap = kb_total / splitk_min_kb();
+  s = s < cap ? s : cap;
   while (s > 1 && tiles * s * int64_t(kGemmBM) * bn * 4 > ws_bytes - kCounterBytes) --s;
   return s < 1 ? 1 : s;
 }

@@ -133,9 +133,12 @@ struct GemmCfg {
   // Swapped tiles stream weights at batch 1: a small footprint lets the next
   // kernel's CTA (programmatic dependent launch) sit beside this one and
   // prefetch its own weights while this one drains.
+#ifndef NF_GEMM_SWAP_KB
+#define NF_GEMM_SWAP_KB NF_GEMM_BUDGET_KB
+#endif
   static constexpr int kBudgetKB =
       BN >= 256 ? (PAIR ? 225 : 220)
-                : (SWAP && !kStaged ? NF_GEMM_LITE_KB : NF_GEMM_BUDGET_KB);
+                : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr size_t kBytes =
