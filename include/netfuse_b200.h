@@ -135,6 +135,18 @@ int nf_grouped_conv_tc(const void* x, const void* w, const float* bias, const vo
 int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups, int kernel,
                                 int stride, int pad, int kpad);
 
+/*
+ * Fused merged QKV projection + attention for batch-1 encoders (the merged
+ * graph's BatchMatMul(qkv) -> Attention pair: reference `batch_matmul`,
+ * engine.py:215-235, then the attention restatement). x (G, S=128, D) bf16
+ * rows at x + g*x_gs + t*x_ld; w (G, 3D, D) K-major bf16 (q | k | v output
+ * features); bias (G, 3D) fp32 or NULL; out (G, S, D) bf16 context of heads
+ * of 64. One CTA per (instance, head); QKV never reaches HBM.
+ */
+int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
+                     void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
+                     float scale, void* stream);
+
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream);

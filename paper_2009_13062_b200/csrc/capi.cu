@@ -161,6 +161,14 @@ int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups
   return nf::conv_workspace_bytes(N, H, W, C, Cout, groups, kernel, stride, pad, kpad);
 }
 
+int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
+                     void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
+                     float scale, void* stream) {
+  if (!x || !w || !out) return NF_ERR_SHAPE;
+  return nf::qkv_attention_tc(x, x_ld, x_gs, w, bias, out, groups, seq, d_model, heads, scale,
+                              static_cast<cudaStream_t>(stream));
+}
+
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream) {
   if (!x || !y || N < 1 || H < 1 || W < 1 || C < 1) return NF_ERR_SHAPE;

@@ -64,6 +64,11 @@ int conv_nhwc_direct(const void* x, const void* w, const float* bias, const void
 int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int k, int stride,
               int pad, int dtype, cudaStream_t s);
 
+// qkv_attention.cu — fused QKV projection + attention, batch 1, S = 128.
+int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
+                     void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
+                     cudaStream_t stream);
+
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,
               float scale, int dtype, int mode, cudaStream_t stream);

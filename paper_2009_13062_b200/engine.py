@@ -331,6 +331,17 @@ class Plan:
             ins = [self.vals[parse_ref(r)[0]] for r in node.inputs]
             for v in ins:
                 self._flush_deferred(v.t, keep_for=node)
+            attn = self._qkv_attention_pair(node, ins, weights, users, outputs)
+            if attn is not None:
+                try:
+                    out = self._lower_qkv_attention(node, attn, ins[0], weights)
+                except (ShapeError, UnsupportedOpError) as exc:
+                    raise ExecutionError(node.id, exc) from exc
+                self.vals[attn.id] = out
+                done.add(attn.id)
+                self.op_invocations += 2
+                self.dispatch_count += 2
+                continue
             try:
                 act_user = None
                 if self.fuse and node.kind in (OpKind.MATMUL, OpKind.BATCH_MATMUL):
@@ -851,6 +862,51 @@ class Plan:
             "nf_grouped_linear_ws", xp, k_in, rows * k_in, wp, bp, None, yp, n_out,
             rows * n_out, groups, rows, k_in, n_out, dcode, layout, act, mcode, wsp, wsb, st))
         return DVal(y, node.output_spec.dims)
+
+    def _qkv_attention_pair(self, node, ins, weights, users, outputs):
+        """A batch-1 QKV projection whose only consumer is an Attention over
+        128-token sequences of 64-wide heads: run both as one fused launch
+        (nf_qkv_attention) so the per-head Q/K/V stay on chip."""
+        if not self.fuse or self.mcode != _lib.NF_MODE_FAST:
+            return None
+        if node.kind not in (OpKind.MATMUL, OpKind.BATCH_MATMUL) or node.id in outputs:
+            return None
+        us = users.get(node.id, [])
+        if len(us) != 1 or us[0].kind is not OpKind.ATTENTION or us[0].attrs.get("scale"):
+            return None
+        attn = us[0]
+        v = ins[0]
+        if v.split is not None or v.dtype != torch.bfloat16:
+            return None
+        wsrc = weights[node.weights[0]]
+        if wsrc.data.dtype != torch.bfloat16:
+            return None
+        groups = wsrc.spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
+        d = wsrc.spec.dims[-2]
+        heads = attn.attrs["heads"]
+        x = v.t
+        if (wsrc.spec.dims[-1] != 3 * d or d != 64 * heads or x.shape[-1] != d
+                or x.numel() != groups * 128 * d or x.shape[-2] != 128):
+            return None
+        return attn
+
+    def _lower_qkv_attention(self, node, attn, v, weights):
+        x = self._materialize(node.id, v)
+        wname = node.weights[0]
+        groups = weights[wname].spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
+        d = weights[wname].spec.dims[-2]
+        heads = attn.attrs["heads"]
+        w = self._w(weights, wname, "linear_nk", x.dtype)
+        bias = self._w(weights, node.weights[1], "vec_f32", x.dtype) if len(node.weights) > 1 \
+            else None
+        y = self._alloc(attn.output_spec.dims, x.dtype)
+        scale = 1.0 / math.sqrt(d // heads)
+        xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, \
+            y.data_ptr()
+        self._linear_w[len(self.steps)] = (wp, w.numel() * w.element_size())
+        self._emit(attn.id, lambda st: _lib.call("nf_qkv_attention", xp, d, 128 * d, wp, bp, yp,
+                                                 groups, 128, d, heads, float(scale), st))
+        return DVal(y, attn.output_spec.dims)
 
     def _attention(self, node, v):
         x = self._materialize(node.id, v)

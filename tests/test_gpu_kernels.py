@@ -118,6 +118,27 @@ def test_attention_tensor_core_vs_oracle(bt, s, h):
     assert normwise(host(got), want) < 2e-2
 
 
+@pytest.mark.parametrize("g,h", [(8, 12), (3, 2), (40, 12)])
+def test_fused_qkv_attention_vs_oracle(g, h):
+    """nf_qkv_attention = batch_matmul(x, Wqkv) + bias -> attention, S=128."""
+    from paper_2009_13062_b200 import _lib
+    rng = np.random.default_rng(g * 7 + h)
+    d = 64 * h
+    x = OK.bf16_round(rng.uniform(-1, 1, (g, 128, d)).astype(np.float32))
+    w = OK.bf16_round((rng.uniform(-1, 1, (g, d, 3 * d)) / np.sqrt(d)).astype(np.float32))
+    b = rng.uniform(-0.1, 0.1, (g, 3 * d)).astype(np.float32)
+    qkv = OK.bf16_round(np.einsum("gtk,gkn->gtn", x, w) + b[:, None, :])
+    want = np.stack([OK.attention(qkv[j], heads=h) for j in range(g)])
+    xt = cuda(x, torch.bfloat16)
+    wt = cuda(np.ascontiguousarray(np.swapaxes(w, 1, 2)), torch.bfloat16)
+    bt = cuda(b)
+    y = torch.empty(g, 128, d, dtype=torch.bfloat16, device="cuda")
+    _lib.call("nf_qkv_attention", xt.data_ptr(), d, 128 * d, wt.data_ptr(), bt.data_ptr(),
+              y.data_ptr(), g, 128, d, h, 1.0 / 8.0, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert normwise(host(y), want) < 2e-2
+
+
 def test_attention_simt_f32_and_long_sequences():
     rng = np.random.default_rng(11)
     for shape, h in (((2, 3, 40, 3 * 48), 3), ((1, 200, 3 * 128), 2)):

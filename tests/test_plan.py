@@ -22,11 +22,22 @@ def test_bert_glue_is_zero_copy():
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
     # only the per-model output copies remain
     assert _copies(plan) == 3
-    # per layer: qkv, attn, proj, ln(+residual add), ff1(+gelu), ff2, ln(+add)
-    assert len(plan.steps) == 2 * 7 + 3
+    # per layer: qkv+attn (one fused launch at batch 1), proj, ln(+residual add),
+    # ff1(+gelu), ff2, ln(+add)
+    assert len(plan.steps) == 2 * 6 + 3
+    ids = [nid for nid, _, _ in plan.steps]
+    assert "merged::l00.attn" in ids and "merged::l00.qkv" not in ids
     assert not any("res" in nid for nid, _, _ in plan.steps)
     with pytest.raises(UnsupportedOpError):
         plan.launch()
+
+
+def test_qkv_attention_fusion_needs_batch_one():
+    graph, stores = W.build_zoo("bert-2l", num_models=2, batch=2, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    ids = [nid for nid, _, _ in plan.steps]
+    assert "merged::l00.qkv" in ids and "merged::l00.attn" in ids
 
 
 def test_gelu_fused_into_linear_epilogue():
