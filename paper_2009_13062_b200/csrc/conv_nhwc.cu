@@ -167,6 +167,56 @@ __global__ void k_pool_nhwc(const T* __restrict__ x, T* __restrict__ y, int N, i
   }
 }
 
+// bf16, C % 8 == 0: one thread per (pixel, 8-channel group) with 16-byte
+// loads / stores and 32-bit indexing (HBM-bound). Max is order-free; the mean
+// sums in the same row-major window order as the scalar kernel.
+template <bool MAXP>
+__global__ void k_pool_nhwc_v8(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                               int N, int H, int W, int C8, int Ho, int Wo, int k, int stride,
+                               int pad) {
+  pdl_enter();
+  const int total = N * Ho * Wo * C8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = i % C8;
+    const int pix = i / C8;
+    const int wo = pix % Wo;
+    const int t = pix / Wo;
+    const int ho = t % Ho;
+    const int n = t / Ho;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = MAXP ? -INFINITY : 0.f;
+    for (int r = 0; r < k; ++r) {
+      const int h = ho * stride - pad + r;
+      for (int q = 0; q < k; ++q) {
+        const int w = wo * stride - pad + q;
+        if (h >= 0 && h < H && w >= 0 && w < W) {
+          const uint4 u = *reinterpret_cast<const uint4*>(
+              x + ((int64_t(n) * H + h) * W + w) * (C8 * 8) + c8 * 8);
+          const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(p2[e]);
+            acc[2 * e] = MAXP ? fmaxf(acc[2 * e], f.x) : __fadd_rn(acc[2 * e], f.x);
+            acc[2 * e + 1] = MAXP ? fmaxf(acc[2 * e + 1], f.y) : __fadd_rn(acc[2 * e + 1], f.y);
+          }
+        } else if (!MAXP) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], 0.f);
+        }
+      }
+    }
+    uint4 o;
+    uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+    const float inv_den = float(k * k);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      po[e] = MAXP ? pack_bf16x2(acc[2 * e], acc[2 * e + 1])
+                   : pack_bf16x2(__fdiv_rn(acc[2 * e], inv_den), __fdiv_rn(acc[2 * e + 1], inv_den));
+    *reinterpret_cast<uint4*>(y + int64_t(pix) * (C8 * 8) + c8 * 8) = o;
+  }
+}
+
 int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int k, int stride,
               int pad, int dtype, cudaStream_t s) {
   if (k < 1 || stride < 1 || pad < 0 || 2 * pad > k) return NF_ERR_SHAPE;
@@ -186,7 +236,21 @@ int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int 
       launch_pdl(k_pool_nhwc<T, false>, dim3(unsigned(blocks)), dim3(256), 0, s, px, py, N, H,   \
                  W, C, Ho, Wo, k, stride, pad);                                                    \
   } while (0)
-  if (dtype == NF_BF16) NF_PN(__nv_bfloat16);
+  const bool v8 = dtype == NF_BF16 && C % 8 == 0 && int64_t(N) * H * W * C < (int64_t(1) << 31) &&
+                  ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  if (v8) {
+    const int64_t work = int64_t(N) * Ho * Wo * (C / 8);
+    int64_t b8 = (work + 255) / 256;
+    if (b8 > int64_t(kNumSMs) * 16) b8 = int64_t(kNumSMs) * 16;
+    auto* px = static_cast<const __nv_bfloat16*>(x);
+    auto* py = static_cast<__nv_bfloat16*>(y);
+    if (kind == NF_POOL_MAX)
+      launch_pdl(k_pool_nhwc_v8<true>, dim3(unsigned(b8)), dim3(256), 0, s, px, py, N, H, W,
+                 C / 8, Ho, Wo, k, stride, pad);
+    else
+      launch_pdl(k_pool_nhwc_v8<false>, dim3(unsigned(b8)), dim3(256), 0, s, px, py, N, H, W,
+                 C / 8, Ho, Wo, k, stride, pad);
+  } else if (dtype == NF_BF16) NF_PN(__nv_bfloat16);
   else if (dtype == NF_F32) NF_PN(float);
   else return NF_ERR_UNSUPPORTED;
 #undef NF_PN

@@ -123,7 +123,14 @@ struct GemmOut {
   static constexpr bool kStaged = BN >= 64 && !(NF_GEMM_DIRECT_SWAP && SWAP && BN <= 128);
 };
 
-template <int BN, bool SWAP, bool PAIR = false>
+#ifndef NF_GEMM_GATHER_KB
+#define NF_GEMM_GATHER_KB NF_GEMM_BUDGET_KB
+#endif
+#ifndef NF_GATHER_CA
+#define NF_GATHER_CA 0
+#endif
+
+template <int BN, bool SWAP, bool PAIR = false, int GATHER = 0>
 struct GemmCfg {
   static constexpr bool kStaged = GemmOut<BN, SWAP>::kStaged;
   static constexpr int kABytes = kGemmBM * kGemmBK * 2;
@@ -136,9 +143,13 @@ struct GemmCfg {
 #ifndef NF_GEMM_SWAP_KB
 #define NF_GEMM_SWAP_KB NF_GEMM_BUDGET_KB
 #endif
+  // Gather (implicit-GEMM conv) kernels may trade ring depth for L1: the
+  // 3x3 taps re-read each input pixel up to 9 times.
+  static constexpr int kMinKB = (3 * kStageBytes + kOutBytes + 1023) / 1024;
   static constexpr int kBudgetKB =
-      BN >= 256 ? (PAIR ? 225 : 220)
-                : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
+      GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
+      : BN >= 256 ? (PAIR ? 225 : 220)
+                  : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
   static constexpr size_t kBytes =
@@ -186,9 +197,14 @@ NF_DEVICE UnitCoord decode_unit(const GemmParams& p, int u, bool swap) {
 template <int BYTES>
 NF_DEVICE void cp_async_zfill(uint32_t dst, const void* src, int src_bytes) {
   if constexpr (BYTES == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                 "r"(src_bytes)
-                 : "memory");
+    if (NF_GATHER_CA)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                   "r"(src_bytes)
+                   : "memory");
+    else
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                   "r"(src_bytes)
+                   : "memory");
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
                  "r"(src_bytes)
@@ -204,7 +220,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                       const __grid_constant__ CUtensorMap map_b,
                       const __grid_constant__ CUtensorMap map_y,
                       const __grid_constant__ CUtensorMap map_r, GemmParams p) {
-  using C = GemmCfg<BN, SWAP, PAIR>;
+  using C = GemmCfg<BN, SWAP, PAIR, GATHER>;
   constexpr int kStages = C::kStages;
   static_assert(!(PAIR && GATHER), "CTA pairs take TMA operands only");
   constexpr int kRowsA = PAIR ? 2 * kGemmBM : kGemmBM;  // A rows per unit
@@ -754,7 +770,7 @@ bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, 
 template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0, bool PAIR = false>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
-  using C = GemmCfg<BN, SWAP, PAIR>;
+  using C = GemmCfg<BN, SWAP, PAIR, GATHER>;
   auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR>;
   static bool attr_done = false;  // idempotent attribute set; benign race
   if (!attr_done) {

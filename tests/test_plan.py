@@ -20,11 +20,11 @@ def test_bert_glue_is_zero_copy():
     kinds = [merged.graph.node_map()[nid].kind for nid, _, _ in plan.steps
              if nid in merged.graph.node_map()]
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
-    # only the per-model output copies remain
-    assert _copies(plan) == 3
+    # outputs are views of plan-owned buffers: no copy launch at all
+    assert _copies(plan) == 0
     # per layer: qkv+attn (one fused launch at batch 1), proj, ln(+residual add),
     # ff1(+gelu), ff2, ln(+add)
-    assert len(plan.steps) == 2 * 6 + 3
+    assert len(plan.steps) == 2 * 6
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.attn" in ids and "merged::l00.qkv" not in ids
     assert not any("res" in nid for nid, _, _ in plan.steps)
