@@ -13,11 +13,36 @@
 // channel groups waste at most 4x of a tiny MMA), or, for few pixels and
 // wide groups (ResNet layer3/4 at batch 1), weights on the 128-row side
 // (swapped) plus split-K so the weight stream covers every SM.
+#include <algorithm>
+
 #include "gemm_sm100.cuh"
 
 namespace nf {
 
 namespace {
+
+// NF_CONV_HALO=0 forces the per-tap cp.async gather (A/B knob, read once).
+bool halo_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NF_CONV_HALO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// 4-D NHWC box for the halo gather: (cg channels, halo_w columns, halo_h rows, 1 image).
+bool make_halo_map(CUtensorMap* map, const void* x, int N, int H, int W, int C, int cg,
+                   int halo_w, int halo_h) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(N)};
+  cuuint64_t strides[3] = {cuuint64_t(C) * 2, cuuint64_t(W) * C * 2, cuuint64_t(H) * W * C * 2};
+  cuuint32_t box[4] = {cuuint32_t(cg), cuuint32_t(halo_w), cuuint32_t(halo_h), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 int conv_pick(int64_t pix, int64_t coutg, bool* swap) {
   *swap = pix <= 256 && coutg >= 128;
@@ -78,6 +103,15 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   bool swap;
   const int bn = conv_pick(pix, coutg, &swap);
   if (gather == 8 && (swap || bn > 64)) return NF_ERR_UNSUPPORTED;
+  // Halo gather: one image, pixels on M, 16..64-channel groups, a halo that
+  // fits two buffers next to the operand ring.
+  const int rows_out = std::min(Ho, (kGemmBM - 1 + Wo - 1) / Wo + 1);
+  const int halo_h = (rows_out - 1) * stride + k;
+  const int halo_w = (Wo - 1) * stride + k;
+  const int64_t halo_raw = int64_t(cg) * 2 * halo_w * halo_h;
+  const int64_t halo_bytes = (halo_raw + 1023) / 1024 * 1024;
+  const bool halo = halo_enabled() && !swap && N == 1 && (cg == 16 || cg == 32 || cg == 64) &&
+                    bn <= 64 && halo_h <= 256 && halo_w <= 256 && halo_bytes <= 48 * 1024;
 
   GemmParams p{};
   p.bias = bias;
@@ -91,7 +125,13 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   p.cx = static_cast<const __nv_bfloat16*>(x);
   p.cH = H; p.cW = W; p.cC = C; p.cCg = cg; p.cK = k; p.cS = stride; p.cP = pad;
   p.cHo = Ho; p.cWo = Wo;
-  CUtensorMap mw, my, mr;
+  CUtensorMap mw, my, mr, mh;
+  if (halo) {
+    if (!make_halo_map(&mh, x, N, H, W, C, cg, halo_w, halo_h)) return NF_ERR_UNSUPPORTED;
+    p.halo_w = halo_w;
+    p.halo_bytes = int(halo_bytes);
+    p.halo_tx = uint32_t(halo_raw);
+  }
   if (swap) {
     if (!make_bf16_map(&mw, w, G, coutg, Kpad, kGemmBK, kGemmBM, 0, 0) ||
         !make_bf16_map(&my, y, G, pix, coutg, kOutBlock, bn, Cout, coutg))
@@ -126,6 +166,13 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   // The weights map is the only TMA operand; it sits in the slot its
   // orientation reads (A when swapped, B otherwise).
 #define NF_CV(BNV, SW, GA) return launch_conv<BNV, SW, GA>(r, mw, mw, my, mr, p, grid, stream)
+#define NF_CH(BNV) return launch_conv<BNV, false, 1>(r, mh, mw, my, mr, p, grid, stream)
+  if (halo) {
+    if (bn == 16) NF_CH(16);
+    if (bn == 32) NF_CH(32);
+    NF_CH(64);
+  }
+#undef NF_CH
   if (swap) {
     if (bn == 64) NF_CV(64, true, 16);
     if (bn == 128) NF_CV(128, true, 16);

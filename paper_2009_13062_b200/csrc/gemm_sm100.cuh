@@ -102,6 +102,8 @@ struct GemmParams {
   // implicit-GEMM conv geometry (GATHER kernels only)
   const __nv_bfloat16* cx;  // NHWC input
   int cH, cW, cC, cCg, cK, cS, cP, cHo, cWo;
+  int halo_w, halo_bytes;    // GATHER == 1: halo box width, bytes per buffer (1 KB aligned)
+  uint32_t halo_tx;          // bytes one halo TMA box delivers
 };
 
 #ifndef NF_GEMM_LITE_KB
@@ -129,6 +131,9 @@ struct GemmOut {
 #ifndef NF_GATHER_CA
 #define NF_GATHER_CA 0
 #endif
+#ifndef NF_GEMM_HALO_KB
+#define NF_GEMM_HALO_KB 120  // operand ring of halo-gather convs (2 halo buffers follow)
+#endif
 
 template <int BN, bool SWAP, bool PAIR = false, int GATHER = 0>
 struct GemmCfg {
@@ -147,7 +152,8 @@ struct GemmCfg {
   // 3x3 taps re-read each input pixel up to 9 times.
   static constexpr int kMinKB = (3 * kStageBytes + kOutBytes + 1023) / 1024;
   static constexpr int kBudgetKB =
-      GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
+      GATHER == 1 ? (NF_GEMM_HALO_KB > kMinKB ? NF_GEMM_HALO_KB : kMinKB)
+      : GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
       : BN >= 256 ? (PAIR ? 225 : 220)
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
@@ -242,7 +248,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
+  uint64_t* hbar = rbar + 1;  // [2] halo buffers (GATHER == 1)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hbar + 2);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -260,6 +267,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     if (C::kStaged) tma_prefetch_desc(&map_y);
     if (kResTma) tma_prefetch_desc(&map_r);
     mbar_init(rbar, 1);
+    mbar_init(&hbar[0], 1);
+    mbar_init(&hbar[1], 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], GATHER ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
@@ -657,6 +666,73 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       }
     }
     if (etid == 0) NF_TRACE(5);
+  } else if constexpr (GATHER == 1) {
+    // --------------------- halo im2col (conv, pixels on M) ---------------------
+    // One TMA box per 128-pixel tile: cg channels x halo_w columns x the
+    // input rows the tile's taps touch (zero-filled outside the image), double
+    // buffered across units; each k-block's im2col rows are then built with
+    // 16-byte shared-memory copies (every input pixel leaves HBM / L2 once
+    // per tile instead of once per tap).
+    const int gt = threadIdx.x - (64 + kEpiThreads);
+    const int j = gt & 7;   // 16-byte chunk of the 128-byte operand row
+    const int rb = gt >> 3; // rows rb + 16 * i
+    uint8_t* halo = sOut + C::kOutBytes + 1024;
+    const int taps = p.cK * p.cK;
+    const int rows = p.rows_a;
+    const int hw = p.halo_w;
+    auto issue_halo = [&](int u, int hb) {
+      const UnitCoord c = decode_unit(p, u, false);
+      const int oh_lo = (c.ta * kGemmBM) / p.cWo;
+      mbar_arrive_expect_tx(&hbar[hb], p.halo_tx);
+      tma_load_4d(halo + hb * p.halo_bytes, &map_a, &hbar[hb], c.g * p.cCg, -p.cP,
+                  oh_lo * p.cS - p.cP, 0, kEvictNormal);
+    };
+    grid_dependency_wait();
+    if (gt == 0 && int(blockIdx.x) < p.units) issue_halo(blockIdx.x, 0);
+    int it = 0, local = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+      const int hb = local & 1;
+      if (gt == 0 && u + int(gridDim.x) < p.units) {
+        fence_proxy_async_smem();  // generic reads of that buffer (previous unit) done
+        issue_halo(u + gridDim.x, hb ^ 1);
+      }
+      const UnitCoord c = decode_unit(p, u, false);
+      const int p0 = c.ta * kGemmBM;
+      const int oh_lo = p0 / p.cWo;
+      int hoff[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int pix = p0 + rb + 16 * i;
+        const int oh = pix / p.cWo, ow = pix - (pix / p.cWo) * p.cWo;
+        hoff[i] = pix < rows ? ((oh - oh_lo) * p.cS * hw + ow * p.cS) : -1;
+      }
+      const uint32_t hsrc = smem_u32(halo + hb * p.halo_bytes);
+      mbar_wait(&hbar[hb], uint32_t(local >> 1) & 1u);
+      for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
+        const int stage = it % kStages;
+        mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
+        const int k0 = kb * kGemmBK + j * 8;
+        const int tap = k0 / p.cCg;
+        const int ch = k0 - tap * p.cCg;
+        const int kh = tap / p.cK;
+        const int tap_off = kh * hw + (tap - kh * p.cK);
+        const bool tap_ok = tap < taps;
+        const uint32_t sbase = smem_u32(sA + stage * C::kABytes);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = rb + 16 * i;
+          uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+          if (tap_ok && hoff[i] >= 0)
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                         : "r"(hsrc + uint32_t(((hoff[i] + tap_off) * p.cCg + ch) * 2)));
+          st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v0, v1, v2, v3);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&full[stage]);
+      }
+      named_bar_sync(2, kGatherThreads);  // everyone is done with halo buffer hb
+    }
   } else if constexpr (GATHER != 0) {
     // ------------------------ im2col gather (conv) ------------------------
     constexpr int R = SWAP ? BN : kGemmBM;  // activation rows per tile
@@ -774,13 +850,14 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR>;
   static bool attr_done = false;  // idempotent attribute set; benign race
   if (!attr_done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kBytes));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GATHER == 1 ? 232448 : int(C::kBytes));
     attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(gemm_threads<BN, GATHER>());
-  cfg.dynamicSmemBytes = C::kBytes;
+  cfg.dynamicSmemBytes = C::kBytes + (GATHER == 1 ? 1024 + 2 * size_t(p.halo_bytes) : 0);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;

@@ -23,6 +23,11 @@ CASES = [
     (1, 7, 7, 2, 512, 512, 3, 1, 1, True, False),     # swapped, split-K, residual
     (2, 56, 56, 2, 256, 512, 1, 2, 0, False, False),  # 1x1 stride-2 downsample
     (3, 9, 11, 3, 24, 40, 3, 2, 1, True, True),       # ragged: odd sizes, coutg % 8 != 0
+    # halo gather (one image, 16..64-channel groups)
+    (1, 56, 56, 128, 32, 32, 3, 1, 1, False, True),   # ResNeXt layer1 32-channel super-groups
+    (1, 56, 56, 64, 32, 32, 3, 2, 1, False, True),    # stride 2: 13-row halo
+    (1, 9, 11, 4, 16, 16, 3, 1, 1, True, True),       # ragged rows, residual
+    (1, 20, 20, 3, 64, 48, 3, 1, 1, False, False),    # 64-channel groups, coutg 48
 ]
 
 
