@@ -30,6 +30,14 @@ bool halo_enabled() {
   return on;
 }
 
+bool halo_stem() {
+  static const bool on = [] {
+    const char* e = getenv("NF_CONV_HALO_STEM");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // 4-D NHWC box for the halo gather: (cg channels, halo_w columns, halo_h rows, 1 image).
 bool make_halo_map(CUtensorMap* map, const void* x, int N, int H, int W, int C, int cg,
                    int halo_w, int halo_h) {
@@ -108,9 +116,13 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   const int rows_out = std::min(Ho, (kGemmBM - 1 + Wo - 1) / Wo + 1);
   const int halo_h = (rows_out - 1) * stride + k;
   const int halo_w = (Wo - 1) * stride + k;
-  const int64_t halo_raw = int64_t(cg) * 2 * halo_w * halo_h;
+  const int halo_cpp = cg < 8 ? 8 : cg;  // TMA boxes need 16-byte rows
+  const int64_t halo_raw = int64_t(halo_cpp) * 2 * halo_w * halo_h;
   const int64_t halo_bytes = (halo_raw + 1023) / 1024 * 1024;
-  const bool halo = halo_enabled() && !swap && N == 1 && (cg == 16 || cg == 32 || cg == 64) &&
+  // (4-channel groups work too — the padded stem — but measured slower than
+  // the 8-byte cp.async gather: a 7x7/s2 halo is barely smaller than 49 taps.)
+  const bool halo = halo_enabled() && !swap && N == 1 &&
+                    (cg == 16 || cg == 32 || cg == 64 || (cg == 4 && halo_stem())) &&
                     bn <= 64 && halo_h <= 256 && halo_w <= 256 && halo_bytes <= 48 * 1024;
 
   GemmParams p{};
@@ -127,8 +139,9 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   p.cHo = Ho; p.cWo = Wo;
   CUtensorMap mw, my, mr, mh;
   if (halo) {
-    if (!make_halo_map(&mh, x, N, H, W, C, cg, halo_w, halo_h)) return NF_ERR_UNSUPPORTED;
+    if (!make_halo_map(&mh, x, N, H, W, C, halo_cpp, halo_w, halo_h)) return NF_ERR_UNSUPPORTED;
     p.halo_w = halo_w;
+    p.halo_cpp = halo_cpp;
     p.halo_bytes = int(halo_bytes);
     p.halo_tx = uint32_t(halo_raw);
   }

@@ -103,6 +103,7 @@ struct GemmParams {
   const __nv_bfloat16* cx;  // NHWC input
   int cH, cW, cC, cCg, cK, cS, cP, cHo, cWo;
   int halo_w, halo_bytes;    // GATHER == 1: halo box width, bytes per buffer (1 KB aligned)
+  int halo_cpp;              // channels per halo pixel (cg, or 8 for cg == 4: 16-byte boxes)
   uint32_t halo_tx;          // bytes one halo TMA box delivers
 };
 
@@ -684,7 +685,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       const UnitCoord c = decode_unit(p, u, false);
       const int oh_lo = (c.ta * kGemmBM) / p.cWo;
       mbar_arrive_expect_tx(&hbar[hb], p.halo_tx);
-      tma_load_4d(halo + hb * p.halo_bytes, &map_a, &hbar[hb], c.g * p.cCg, -p.cP,
+      // the box's first channel must sit on a 16-byte boundary: 4-channel
+      // groups start at the even-group boundary and index +4 inside the pixel
+      tma_load_4d(halo + hb * p.halo_bytes, &map_a, &hbar[hb], (c.g * p.cCg) & ~7, -p.cP,
                   oh_lo * p.cS - p.cP, 0, kEvictNormal);
     };
     grid_dependency_wait();
@@ -706,26 +709,48 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         const int oh = pix / p.cWo, ow = pix - (pix / p.cWo) * p.cWo;
         hoff[i] = pix < rows ? ((oh - oh_lo) * p.cS * hw + ow * p.cS) : -1;
       }
-      const uint32_t hsrc = smem_u32(halo + hb * p.halo_bytes);
+      const uint32_t hsrc = smem_u32(halo + hb * p.halo_bytes) + uint32_t(((c.g * p.cCg) & 7) * 2);
       mbar_wait(&hbar[hb], uint32_t(local >> 1) & 1u);
       for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
         const int stage = it % kStages;
         mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
+        // chunk j = K elements [k0, k0+8): one tap when cg >= 8, two 4-channel
+        // taps (8-byte halves) when cg == 4 (the padded stem)
         const int k0 = kb * kGemmBK + j * 8;
-        const int tap = k0 / p.cCg;
-        const int ch = k0 - tap * p.cCg;
-        const int kh = tap / p.cK;
-        const int tap_off = kh * hw + (tap - kh * p.cK);
-        const bool tap_ok = tap < taps;
+        int off[2];
+        bool okh[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int kx = k0 + hh * 4;
+          const int tap = kx / p.cCg;
+          const int ch = kx - tap * p.cCg;
+          const int kh = tap / p.cK;
+          off[hh] = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp + ch;
+          okh[hh] = tap < taps;
+        }
         const uint32_t sbase = smem_u32(sA + stage * C::kABytes);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = rb + 16 * i;
           uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-          if (tap_ok && hoff[i] >= 0)
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                         : "r"(hsrc + uint32_t(((hoff[i] + tap_off) * p.cCg + ch) * 2)));
+          if (hoff[i] >= 0) {
+            const uint32_t pix = hsrc + uint32_t(hoff[i] * p.halo_cpp * 2);
+            if (p.cCg >= 8) {
+              if (okh[0])
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                             : "r"(pix + uint32_t(off[0] * 2)));
+            } else {
+              if (okh[0])
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
+                             : "=r"(v0), "=r"(v1)
+                             : "r"(pix + uint32_t(off[0] * 2)));
+              if (okh[1])
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
+                             : "=r"(v2), "=r"(v3)
+                             : "r"(pix + uint32_t(off[1] * 2)));
+            }
+          }
           st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v0, v1, v2, v3);
         }
         fence_proxy_async_smem();

@@ -53,6 +53,9 @@ _ACT_OF = {OpKind.RELU: _lib.NF_ACT_RELU, OpKind.GELU: _lib.NF_ACT_GELU,
 _EW_OF = {OpKind.ADD: _lib.NF_EW_ADD, OpKind.MUL: _lib.NF_EW_MUL, OpKind.RELU: _lib.NF_EW_RELU,
           OpKind.TANH: _lib.NF_EW_TANH, OpKind.GELU: _lib.NF_EW_GELU}
 _MODES = {"fast": _lib.NF_MODE_FAST, "exact": _lib.NF_MODE_EXACT}
+# Channels per densified super-group for narrow grouped convs (ResNeXt);
+# NF_SUPER_GROUP overrides (A/B knob).
+_SUPER_GROUP = int(__import__("os").environ.get("NF_SUPER_GROUP", "64"))
 
 
 @dataclass
@@ -584,8 +587,9 @@ class Plan:
             # gather rows and a 32-wide MMA tile instead of many tiny units
             # (at most 8x the FLOPs of a conv that is HBM-bound anyway).
             sup = 1
-            if cg_pad == cg and cg < 32 and 32 % cg == 0 and groups % (32 // cg) == 0:
-                sup = 32 // cg
+            sg = _SUPER_GROUP
+            if cg_pad == cg and cg < sg and sg % cg == 0 and groups % (sg // cg) == 0:
+                sup = sg // cg
             g_eff, cg_eff, coutg_eff = groups // sup, cg_pad * sup, coutg * sup
             kk = k * k * cg_eff
             kpad = -(-kk // 8) * 8
