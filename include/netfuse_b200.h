@@ -136,6 +136,19 @@ int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups
                                 int stride, int pad, int kpad);
 
 /*
+ * Merged Linear + residual + LayerNorm (batch-1 encoders): the merged graph's
+ * BatchMatMul -> Add -> GroupNorm(groups = instances) chain (reference
+ * batch_matmul engine.py:215-235, add 322-325, group_norm 263-284) as one
+ * launch: y = LN(x W^T + bias + residual) over the n output features of each
+ * of the rows (<= 128) tokens, gamma/beta (groups, n) fp32, n <= 1024.
+ * x / residual / y rows at base + g*gs + t*ld (bf16), w (groups, n, k) bf16.
+ */
+int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const float* bias, const void* residual, const float* gamma,
+                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
+                         int64_t groups, int64_t rows, int64_t k, int64_t n, void* stream);
+
+/*
  * Fused merged QKV projection + attention for batch-1 encoders (the merged
  * graph's BatchMatMul(qkv) -> Attention pair: reference `batch_matmul`,
  * engine.py:215-235, then the attention restatement). x (G, S=128, D) bf16

@@ -49,6 +49,8 @@ SIGNATURES: dict[str, list] = {
     "nf_pool2d_nhwc": [_p, _p] + [_i] * 9 + [_p],
     "nf_grouped_conv_tc": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _i64, _p],
     "nf_conv_workspace_bytes": [_i] * 10,
+    "nf_grouped_linear_ln": [_p, _i64, _i64, _p, _p, _p, _p, _p, _f, _p, _i64, _i64, _i64, _i64,
+                             _i64, _i64, _p],
     "nf_qkv_attention": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],

@@ -161,6 +161,15 @@ int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups
   return nf::conv_workspace_bytes(N, H, W, C, Cout, groups, kernel, stride, pad, kpad);
 }
 
+int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const float* bias, const void* residual, const float* gamma,
+                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
+                         int64_t groups, int64_t rows, int64_t k, int64_t n, void* stream) {
+  if (!x || !w || !y || !gamma || !beta) return NF_ERR_SHAPE;
+  return nf::grouped_linear_ln_tc(x, x_ld, x_gs, w, bias, residual, gamma, beta, eps, y, y_ld,
+                                  y_gs, groups, rows, k, n, static_cast<cudaStream_t>(stream));
+}
+
 int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
                      float scale, void* stream) {

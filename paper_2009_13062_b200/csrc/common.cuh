@@ -139,6 +139,36 @@ NF_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with cluster-scope acquire: remote (DSMEM) writes released by peer
+// CTAs' mbarrier arrivals are visible after it returns.
+NF_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC;\n\t"
+      "bra LAB_WAITC;\n\t"
+      "DONEC:\n\t"
+      "}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+// float2 store into the same-offset shared memory of cluster CTA `rank`.
+NF_DEVICE void st_cluster_f2(const void* local, uint32_t rank, float a, float b) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(remote), "f"(a), "f"(b) : "memory");
+}
+// Release-arrive on the same-offset mbarrier of cluster CTA `rank`.
+NF_DEVICE void mbar_arrive_remote(uint64_t* local_bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+NF_DEVICE void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor) loads with an L2 cache-policy hint
 // ---------------------------------------------------------------------------

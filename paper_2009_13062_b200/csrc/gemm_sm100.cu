@@ -173,3 +173,54 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
 }
 
 }  // namespace nf
+
+namespace nf {
+
+// Merged Linear + residual + LayerNorm over the N output features (batch-1
+// encoders: T <= 128 tokens per instance, N <= 1024): swapped 128x128 tiles,
+// one cluster of N/128 CTAs per instance exchanging per-token partial sums
+// over DSMEM. y = LN(x W^T + bias + residual) with per-instance gamma/beta
+// (G, N). Replaces the merged graph's BatchMatMul -> Add -> GroupNorm chain
+// (reference batch_matmul engine.py:215-235, add 322-325, group_norm 263-284).
+int grouped_linear_ln_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const float* bias, const void* residual, const float* gamma,
+                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
+                         int64_t G, int64_t T, int64_t K, int64_t N, cudaStream_t stream) {
+  if (K % 8 || N % 8 || T < 1 || T > 128 || N > 8 * kGemmBM || !gamma || !beta)
+    return NF_ERR_UNSUPPORTED;
+  if (G > 65535) return NF_ERR_UNSUPPORTED;
+  GemmParams p{};
+  p.bias = bias;
+  p.residual = residual;
+  p.out_gstride = y_gs;
+  p.out_ld = y_ld;
+  p.features = int(N);
+  p.groups = int(G);
+  p.y_direct = y;
+  p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
+  p.ln_gamma = gamma;
+  p.ln_beta = beta;
+  p.ln_eps = eps;
+  p.ln_cluster = int((N + kGemmBM - 1) / kGemmBM);
+  CUtensorMap ma, mb, my, mr;
+  if (!make_bf16_map(&ma, w, G, N, K, kGemmBK, kGemmBM, 0, 0) ||
+      !make_bf16_map(&mb, x, G, T, K, kGemmBK, 128, x_ld, x_gs) ||
+      !make_bf16_map(&my, y, G, T, N, kOutBlock, 128, y_ld, y_gs))
+    return NF_ERR_UNSUPPORTED;
+  mr = my;
+  if (residual && !make_bf16_map(&mr, residual, G, T, N, kOutBlock, 128, y_ld, y_gs))
+    return NF_ERR_UNSUPPORTED;
+  p.rows_a = int(N);
+  p.rows_b = int(T);
+  p.tiles_a = p.ln_cluster;
+  p.tiles_b = 1;
+  p.splits = 1;
+  p.kb_per_split = p.kb_total;
+  p.units = int(G) * p.tiles_a;
+  const int grid = p.units;  // one unit per CTA: clusters are whole instances
+  if (residual)
+    return launch_tc<128, true, NF_ACT_NONE, true, 0, false, true>(ma, mb, my, mr, p, grid, stream);
+  return launch_tc<128, true, NF_ACT_NONE, false, 0, false, true>(ma, mb, my, my, p, grid, stream);
+}
+
+}  // namespace nf

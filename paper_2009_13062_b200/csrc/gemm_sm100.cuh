@@ -105,6 +105,12 @@ struct GemmParams {
   int halo_w, halo_bytes;    // GATHER == 1: halo box width, bytes per buffer (1 KB aligned)
   int halo_cpp;              // channels per halo pixel (cg, or 8 for cg == 4: 16-byte boxes)
   uint32_t halo_tx;          // bytes one halo TMA box delivers
+  // LNF kernels: y = LayerNorm over the N output features of each token
+  // (one cluster of N/128 CTAs per instance), per-instance affine (G, N)
+  const float* ln_gamma;
+  const float* ln_beta;
+  float ln_eps;
+  int ln_cluster;
 };
 
 #ifndef NF_GEMM_LITE_KB
@@ -221,7 +227,7 @@ NF_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "me
 template <int N>
 NF_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER, bool PAIR>
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER, bool PAIR, bool LNF = false>
 __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     k_grouped_gemm_tc(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
@@ -250,7 +256,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
   uint64_t* hbar = rbar + 1;  // [2] halo buffers (GATHER == 1)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hbar + 2);
+  uint64_t* lnbar = hbar + 2;  // LNF: cluster partial-sum arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lnbar + 1);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -270,6 +277,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     mbar_init(rbar, 1);
     mbar_init(&hbar[0], 1);
     mbar_init(&hbar[1], 1);
+    mbar_init(lnbar, LNF ? p.ln_cluster : 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], GATHER ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR) cluster_sync();  // peer signals the leader's barriers after this
+  if constexpr (PAIR || LNF) cluster_sync();  // peers signal our barriers after this
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) NF_TRACE(1);
@@ -411,6 +419,154 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       __syncwarp();
     }
     if (lane == 0) NF_TRACE(3);
+  } else if (LNF && warp < 2 + kEpiWarps) {
+    // ------------- epilogue + LayerNorm over a cluster's features -------------
+    // Swapped tile (thread = feature row, columns = tokens), one unit per CTA;
+    // the cluster's CL CTAs hold the CL*128 features of one instance. Pass 1:
+    // v = acc + bias + residual, per-token sum / sum of squares over this
+    // CTA's features (warp transpose-reduce + smem); partials go to every
+    // cluster CTA through DSMEM; pass 2 re-reads TMEM and writes
+    // gamma * (v - mean) * rstd + beta.
+    static_assert(!LNF || (SWAP && BN == 128 && !PAIR && GATHER == 0), "LN epilogue config");
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int etid = threadIdx.x - 64;
+    const int col0 = ((warp - 2) >> 2) * kColsPerThread;  // 64 tokens per thread
+    const uint32_t stage_base = smem_u32(sOut);
+    float* sred = reinterpret_cast<float*>(sOut + C::kOutBytes + 1024);  // [4][128][2]
+    float2* sclu = reinterpret_cast<float2*>(sred + 4 * 128 * 2);      // [8][128]
+    float2* sstat = sclu + 8 * 128;                                      // [128]
+    const uint32_t crank = cluster_ctarank();
+    const int CL = p.ln_cluster;
+    const UnitCoord c = decode_unit(p, blockIdx.x, true);
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    if (etid == 0) NF_TRACE(4);
+    const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16);
+    const int m0 = c.ta * kGemmBM;
+    const int feat = m0 + row;
+    const bool fok = feat < p.rows_a;
+    const int64_t fidx = int64_t(c.g) * p.features + feat;
+    const float bf = (p.bias && fok) ? __ldg(p.bias + fidx) : 0.f;
+    // The residual tile arrives by TMA in the output staging layout (the same
+    // smem the result is staged in); per-element global loads here would
+    // serialise on L2 latency.
+    if constexpr (HAS_RES) {
+      if (etid == 0) {
+        mbar_arrive_expect_tx(rbar, C::kOutBytes);
+#pragma unroll
+        for (int b = 0; b < kGemmBM / kOutBlock; ++b)
+          tma_load_3d(sOut + b * BN * 128, &map_r, rbar, m0 + b * kOutBlock, 0, c.g, kEvictFirst);
+      }
+      mbar_wait(rbar, 0);
+    }
+    auto load_v = [&](int cc, float (&v)[32]) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_row + uint32_t(cc), r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float x = __uint_as_float(r[j]) + bf;
+        if constexpr (HAS_RES) {
+          uint16_t h;
+          asm volatile("ld.shared.u16 %0, [%1];"
+                       : "=h"(h)
+                       : "r"(stage_base + stage_offset(cc + j, row, BN)));
+          x += __uint_as_float(uint32_t(h) << 16);
+        }
+        v[j] = fok ? x : 0.f;
+      }
+    };
+#pragma unroll 1
+    for (int cc = col0; cc < col0 + kColsPerThread; cc += 32) {
+      float s1[32], s2[32];
+      load_v(cc, s1);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) s2[j] = s1[j] * s1[j];
+      // transpose-reduce: lane l ends with the warp's sums for token cc + l
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+          const float a1 = upper ? s1[i] : s1[i + o], k1 = upper ? s1[i + o] : s1[i];
+          const float a2 = upper ? s2[i] : s2[i + o], k2 = upper ? s2[i + o] : s2[i];
+          s1[i] = k1 + __shfl_xor_sync(0xffffffffu, a1, o);
+          s2[i] = k2 + __shfl_xor_sync(0xffffffffu, a2, o);
+        }
+      }
+      sred[(quarter * 128 + cc + lane) * 2] = s1[0];
+      sred[(quarter * 128 + cc + lane) * 2 + 1] = s2[0];
+    }
+    named_bar_sync(1, kEpiThreads);
+    if (etid < 128) {
+      const int t = etid;
+      float cs = 0.f, cq = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cs += sred[(q * 128 + t) * 2];
+        cq += sred[(q * 128 + t) * 2 + 1];
+      }
+      for (int r = 0; r < CL; ++r) st_cluster_f2(&sclu[crank * 128 + t], uint32_t(r), cs, cq);
+    }
+    named_bar_sync(1, kEpiThreads);
+    if (etid == 0) {
+      fence_acq_rel_cluster();
+      for (int r = 0; r < CL; ++r) mbar_arrive_remote(lnbar, uint32_t(r));
+    }
+    if (etid == 0) NF_TRACE(2);
+    mbar_wait_cluster(lnbar, 0);
+    if (etid == 0) NF_TRACE(7);
+    if (etid < 128) {
+      const int t = etid;
+      float ts = 0.f, tq = 0.f;
+      for (int r = 0; r < CL; ++r) {
+        const float2 pr = sclu[r * 128 + t];
+        ts += pr.x;
+        tq += pr.y;
+      }
+      const float inv_n = 1.0f / float(p.rows_a);
+      const float mean = ts * inv_n;
+      const float var = fmaxf(fmaf(-mean, mean, tq * inv_n), 0.f);
+      sstat[t] = make_float2(mean, rsqrtf(var + p.ln_eps));
+    }
+    named_bar_sync(1, kEpiThreads);
+    const float gf = fok ? __ldg(p.ln_gamma + fidx) : 0.f;
+    const float btf = fok ? __ldg(p.ln_beta + fidx) : 0.f;
+#pragma unroll 1
+    for (int cc = col0; cc < col0 + kColsPerThread; cc += 32) {
+      float v[32];
+      load_v(cc, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float2 st = sstat[cc + j];
+        v[j] = fmaf((v[j] - st.x) * st.y, gf, btf);
+      }
+      __syncwarp();  // partner lanes read their residuals before the pair stores
+      const bool odd = lane & 1;
+      const int feven = row & ~1;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float send = odd ? v[j] : v[j + 1];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        const uint32_t packed = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
+        const int t = cc + j + (odd ? 1 : 0);
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage_base + stage_offset(t, feven, BN)),
+                     "r"(packed)
+                     : "memory");
+      }
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    named_bar_sync(1, kEpiThreads);
+    if (etid == 0) {
+#pragma unroll
+      for (int b = 0; b < kGemmBM / kOutBlock; ++b)
+        tma_store_3d(&map_y, sOut + b * BN * 128, m0 + b * kOutBlock, 0, c.g);
+      bulk_commit();
+      bulk_wait0();
+      NF_TRACE(5);
+    }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------ epilogue ------------------------------
     const int quarter = warp & 3;         // TMEM lane quarter this warp may access
@@ -868,21 +1024,23 @@ inline EncodeTiledFn encode_fn() {
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0, bool PAIR = false>
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0, bool PAIR = false,
+          bool LNF = false>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
   using C = GemmCfg<BN, SWAP, PAIR, GATHER>;
-  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR>;
+  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR, LNF>;
   static bool attr_done = false;  // idempotent attribute set; benign race
   if (!attr_done) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         GATHER == 1 ? 232448 : int(C::kBytes));
+                         (GATHER == 1 || LNF) ? 232448 : int(C::kBytes));
     attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(gemm_threads<BN, GATHER>());
-  cfg.dynamicSmemBytes = C::kBytes + (GATHER == 1 ? 1024 + 2 * size_t(p.halo_bytes) : 0);
+  cfg.dynamicSmemBytes = C::kBytes + (GATHER == 1 ? 1024 + 2 * size_t(p.halo_bytes) : 0) +
+                         (LNF ? 1024 + 16 * 1024 : 0);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -891,9 +1049,9 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  if (PAIR) {
+  if (PAIR || LNF) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.x = PAIR ? 2 : p.ln_cluster;
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;

@@ -13,6 +13,10 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream);
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
+int grouped_linear_ln_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const float* bias, const void* residual, const float* gamma,
+                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
+                         int64_t G, int64_t T, int64_t K, int64_t N, cudaStream_t stream);
 
 // linear_simt.cu — CUDA-core grouped linear (exact reference order or FMA).
 int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,

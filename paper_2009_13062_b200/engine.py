@@ -149,6 +149,8 @@ class Plan:
         self._linear_w: dict[int, tuple[int, int]] = {}  # step index -> (weight ptr, bytes)
         self.prefetch = prefetch
         self._add_into_norm: dict[str, str] = {}
+        self._ln_done: set[str] = set()  # norms computed by a Linear epilogue
+        self._add_passthrough: dict[str, tuple[str, str]] = {}  # add -> (linear side, residual)
         self._cuda_graph: torch.cuda.CUDAGraph | None = None
         self.dispatch_count = 0
         self.op_invocations = 0
@@ -334,6 +336,31 @@ class Plan:
             ins = [self.vals[parse_ref(r)[0]] for r in node.inputs]
             for v in ins:
                 self._flush_deferred(v.t, keep_for=node)
+            ln_chain = self._linear_ln_chain(node, ins, weights, users, outputs)
+            if ln_chain is not None:
+                add, norm = ln_chain
+                try:
+                    out = self._lower_linear_ln(node, add, norm, ins[0], weights)
+                except (ShapeError, UnsupportedOpError) as exc:
+                    raise ExecutionError(node.id, exc) from exc
+                self.vals[node.id] = out
+                self._ln_done.add(norm.id)
+                self.op_invocations += 1
+                self.dispatch_count += 1
+                continue
+            if node.id in self._add_passthrough:
+                # residual added in the producing Linear's epilogue: the Add is
+                # its (glue-viewed) output
+                self.vals[node.id] = self.vals[self._add_passthrough[node.id][0]]
+                self.op_invocations += 1
+                self.dispatch_count += 1
+                continue
+            if node.id in self._ln_done:
+                # normalised in the producing Linear's epilogue (cluster LN)
+                self.vals[node.id] = ins[0]
+                self.op_invocations += 1
+                self.dispatch_count += 1
+                continue
             attn = self._qkv_attention_pair(node, ins, weights, users, outputs)
             if attn is not None:
                 try:
@@ -870,6 +897,92 @@ class Plan:
         self._emit(node.id, lambda st: _lib.call(
             "nf_grouped_linear_ws", xp, k_in, rows * k_in, wp, bp, None, yp, n_out,
             rows * n_out, groups, rows, k_in, n_out, dcode, layout, act, mcode, wsp, wsb, st))
+        return DVal(y, node.output_spec.dims)
+
+    def _linear_ln_chain(self, node, ins, weights, users, outputs):
+        """Batch-1 merged Linear -> Add(residual) -> [glue views] -> norm over
+        each instance's output features: one launch with the residual add and
+        the LayerNorm in the GEMM epilogue (a cluster of N/128 CTAs per
+        instance shares the row statistics over DSMEM)."""
+        if not self.fuse or self.mcode != _lib.NF_MODE_FAST:
+            return None
+        if node.kind not in (OpKind.MATMUL, OpKind.BATCH_MATMUL) or node.id in outputs:
+            return None
+        # Linear -> [glue views] -> Add: the merger may re-lay the Linear's
+        # batch-packed output out channel-packed for the Add (merger.py:237-301)
+        cur, near = node, node.id
+        while True:
+            us = users.get(cur.id, [])
+            if len(us) != 1 or cur.id in outputs:
+                return None
+            if us[0].kind in (OpKind.RESHAPE, OpKind.TRANSPOSE):
+                cur = us[0]
+                near = cur.id
+                continue
+            break
+        if us[0].kind is not OpKind.ADD or us[0].id not in self._add_into_norm:
+            return None
+        add = us[0]
+        refs = [parse_ref(r)[0] for r in add.inputs]
+        if len(refs) != 2 or refs.count(near) != 1:
+            return None
+        norm = self.graph.node_map()[self._add_into_norm[add.id]]
+        v = ins[0]
+        if v.split is not None or v.dtype != torch.bfloat16:
+            return None
+        wsrc = weights[node.weights[0]]
+        if wsrc.data.dtype != torch.bfloat16:
+            return None
+        groups = wsrc.spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
+        k_in, n_out = wsrc.spec.dims[-2], wsrc.spec.dims[-1]
+        rows = v.t.numel() // max(groups * k_in, 1)
+        ngroups = norm.attrs.get("groups", 1)
+        if ngroups != groups or rows > 128 or n_out > 1024 or n_out % 8 or k_in % 8:
+            return None
+        nspec = norm.output_spec
+        if nspec.dims[channel_axis(len(nspec.dims))] != groups * n_out:
+            return None
+        other_id = refs[1] if refs[0] == near else refs[0]
+        if other_id not in self.vals or self.vals[other_id].dtype != torch.bfloat16:
+            return None
+        self._add_passthrough[add.id] = (near, other_id)
+        return add, norm
+
+    def _lower_linear_ln(self, node, add, norm, v, weights):
+        x = self._materialize(node.id, v)
+        wname = node.weights[0]
+        groups = weights[wname].spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
+        k_in, n_out = weights[wname].spec.dims[-2], weights[wname].spec.dims[-1]
+        rows = x.numel() // (groups * k_in)
+        other = self.vals[self._add_passthrough[add.id][1]]
+        r_t = None
+        if other.split is not None:
+            # channel-packed value kept model-major: (instance, token, channel)
+            # rows are already where the kernel reads them if the storage is
+            # dense with the model axis outermost and channels contiguous
+            t = other.t
+            a = other.split
+            if (_dense_block(t) and t.stride(a + 1) == 1 and t.stride(a) == rows * n_out
+                    and t.numel() == groups * rows * n_out):
+                r_t = t
+        if r_t is None:
+            r_t = self._materialize(node.id, other)
+        if r_t.numel() != groups * rows * n_out:
+            raise ShapeError("residual does not match the linear output")
+        w = self._w(weights, wname, "linear_nk", x.dtype)
+        bias = self._w(weights, node.weights[1], "vec_f32", x.dtype) if len(node.weights) > 1 \
+            else None
+        gam = self._w(weights, norm.weights[0], "vec_f32", x.dtype)
+        bet = self._w(weights, norm.weights[1], "vec_f32", x.dtype)
+        y = self._alloc(node.output_spec.dims, x.dtype)
+        eps = float(norm.attrs["eps"])
+        xp, wp, bp, rp, yp = x.data_ptr(), w.data_ptr(), \
+            bias.data_ptr() if bias is not None else None, r_t.data_ptr(), y.data_ptr()
+        gp, bt = gam.data_ptr(), bet.data_ptr()
+        self._linear_w[len(self.steps)] = (wp, w.numel() * w.element_size())
+        self._emit(node.id, lambda st: _lib.call(
+            "nf_grouped_linear_ln", xp, k_in, rows * k_in, wp, bp, rp, gp, bt, eps, yp, n_out,
+            rows * n_out, groups, rows, k_in, n_out, st))
         return DVal(y, node.output_spec.dims)
 
     def _qkv_attention_pair(self, node, ins, weights, users, outputs):

@@ -22,9 +22,9 @@ def test_bert_glue_is_zero_copy():
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
     # outputs are views of plan-owned buffers: no copy launch at all
     assert _copies(plan) == 0
-    # per layer: qkv+attn (one fused launch at batch 1), proj, ln(+residual add),
-    # ff1(+gelu), ff2, ln(+add)
-    assert len(plan.steps) == 2 * 6
+    # per layer at batch 1: qkv+attn, proj+add+ln (cluster LN epilogue),
+    # ff1(+gelu), ff2+add+ln
+    assert len(plan.steps) == 2 * 4
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.attn" in ids and "merged::l00.qkv" not in ids
     assert not any("res" in nid for nid, _, _ in plan.steps)

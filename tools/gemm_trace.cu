@@ -31,14 +31,25 @@ int main(int argc, char** argv) {
   int64_t ws_bytes = nf::linear_workspace_bytes(G, T, K, N);
   void* ws = nullptr;
   if (ws_bytes) { cudaMalloc(&ws, ws_bytes); cudaMemset(ws, 0, ws_bytes); }
-  const char* names[7] = {"entry", "setup", "first_stage", "last_mma", "acc0_ready", "epi_done",
-                          "exit"};
+  const char* names[8] = {"entry", "setup", "first_stage|ln_partials", "last_mma", "acc0_ready",
+                          "epi_done", "exit", "ln_stats"};
   const bool warm = getenv("NF_TRACE_WARM") != nullptr;  // keep operands L2-resident
   for (int it = 0; it < 3; ++it) {
     if (!warm) cudaMemset(flush, it, 256 << 20);
     stamp_kernel<<<1, 1>>>();
-    int st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, y, N,
-                                   int64_t(T) * N, G, T, K, N, NF_BF16, 0, ws, ws_bytes, 0);
+    int st;
+    if (getenv("NF_TRACE_LN")) {
+      static float* gb = nullptr;
+      if (!gb) {
+        cudaMalloc(&gb, size_t(G) * N * 4 * 2);
+        cudaMemset(gb, 0, size_t(G) * N * 4 * 2);
+      }
+      st = nf::grouped_linear_ln_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, gb, gb + size_t(G) * N,
+                                    1e-5f, y, N, int64_t(T) * N, G, T, K, N, 0);
+    } else {
+      st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, y, N,
+                                 int64_t(T) * N, G, T, K, N, NF_BF16, 0, ws, ws_bytes, 0);
+    }
     cudaError_t e = cudaDeviceSynchronize();
     if (st || e) { printf("status %d err %s\n", st, cudaGetErrorString(e)); return 1; }
     if (it < 2) continue;
@@ -57,7 +68,7 @@ int main(int argc, char** argv) {
         printf("  wait %-12s mean %8.2f us  max %8.2f us (summed over 3 runs)\n", wn[s], tot / 148 * 1e-3, mx * 1e-3);
       }
     }
-    for (int s = 0; s < 7; ++s) {
+    for (int s = 0; s < 8; ++s) {
       std::vector<double> v;
       for (int b = 0; b < 148; ++b)
         if (tr[b * 8 + s] > t0 && tr[b * 8 + s] - t0 < 100000000ull) v.push_back((tr[b * 8 + s] - t0) * 1e-3);
