@@ -56,6 +56,7 @@ _MODES = {"fast": _lib.NF_MODE_FAST, "exact": _lib.NF_MODE_EXACT}
 # Channels per densified super-group for narrow grouped convs (ResNeXt);
 # NF_SUPER_GROUP overrides (A/B knob).
 _SUPER_GROUP = int(__import__("os").environ.get("NF_SUPER_GROUP", "64"))
+_FUSE_LN = __import__("os").environ.get("NF_FUSE_LN", "0") == "1"
 
 
 @dataclass
@@ -904,7 +905,11 @@ class Plan:
         each instance's output features: one launch with the residual add and
         the LayerNorm in the GEMM epilogue (a cluster of N/128 CTAs per
         instance shares the row statistics over DSMEM)."""
-        if not self.fuse or self.mcode != _lib.NF_MODE_FAST:
+        # Measured on B200 (BERT-base N=8, B=1): the cluster-LN launch costs
+        # ~5 us of epilogue on the critical path and forgoes split-K for FF2,
+        # more than the separate norm launch it saves (0.757 vs 0.685 ms per
+        # forward), so it is opt-in (NF_FUSE_LN=1).
+        if not (self.fuse and _FUSE_LN) or self.mcode != _lib.NF_MODE_FAST:
             return None
         if node.kind not in (OpKind.MATMUL, OpKind.BATCH_MATMUL) or node.id in outputs:
             return None

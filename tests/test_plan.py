@@ -22,9 +22,9 @@ def test_bert_glue_is_zero_copy():
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
     # outputs are views of plan-owned buffers: no copy launch at all
     assert _copies(plan) == 0
-    # per layer at batch 1: qkv+attn, proj+add+ln (cluster LN epilogue),
-    # ff1(+gelu), ff2+add+ln
-    assert len(plan.steps) == 2 * 4
+    # per layer at batch 1: qkv+attn (fused), proj, ln(+residual add),
+    # ff1(+gelu), ff2, ln(+add)
+    assert len(plan.steps) == 2 * 6
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.attn" in ids and "merged::l00.qkv" not in ids
     assert not any("res" in nid for nid, _, _ in plan.steps)
@@ -38,6 +38,17 @@ def test_qkv_attention_fusion_needs_batch_one():
     plan = Plan(merged.graph, mstore, device="cpu")
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.qkv" in ids and "merged::l00.attn" in ids
+
+
+def test_cluster_layernorm_fusion_opt_in(monkeypatch):
+    from paper_2009_13062_b200 import engine
+    monkeypatch.setattr(engine, "_FUSE_LN", True)
+    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    ids = [nid for nid, _, _ in plan.steps]
+    # qkv+attn, proj+add+ln1, ff1(+gelu), ff2+add+ln2 per layer
+    assert len(ids) == 2 * 4 and not any(".ln" in i for i in ids)
 
 
 def test_gelu_fused_into_linear_epilogue():
