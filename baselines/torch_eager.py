@@ -133,6 +133,8 @@ def _rel_attention(qkv, r, rwb, rrb, heads, scale):
     dh = d // heads
     q, k, v = qkv.reshape(-1, s, 3, heads, dh).unbind(2)
     kr = r.reshape(-1, 2 * s, heads, dh)
+    if kr.shape[0] != q.shape[0]:  # positional keys shared by an instance's sequences
+        kr = kr.repeat_interleave(q.shape[0] // kr.shape[0], dim=0)
     rw = rwb.reshape(heads, dh).to(qkv.dtype)
     rr = rrb.reshape(heads, dh).to(qkv.dtype)
     ac = torch.einsum("bihd,bjhd->bhij", q + rw, k)

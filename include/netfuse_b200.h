@@ -247,14 +247,16 @@ int nf_attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, i
 /*
  * XLNet relative attention (extension; transformers XLNetRelativeAttention.
  * rel_attn_core, attn_type "bi", no segment term / mask): qkv (Bt, S, 3*H*dh),
- * r (Bt, 2S, H*dh) projected positional keys, r_w_bias / r_r_bias fp32
+ * r (Bt/seqs_per_r, 2S, H*dh) projected positional keys (one per
+ * seqs_per_r consecutive sequences: the positional embedding is the same for
+ * every sequence of an instance), r_w_bias / r_r_bias fp32
  * (Bt/seqs_per_bias, H, dh) per instance; out (Bt, S, H*dh) with
  * score_ij = ((q_i + r_w_bias) . k_j + (q_i + r_r_bias) . kr_{S-i+j}) * scale.
  */
 int nf_rel_attention(const void* qkv, const void* r, const float* r_w_bias,
                      const float* r_r_bias, void* out, int64_t Bt, int64_t S, int64_t H,
-                     int64_t dh, int64_t seqs_per_bias, float scale, int dtype, int mode,
-                     void* stream);
+                     int64_t dh, int64_t seqs_per_bias, int64_t seqs_per_r, float scale,
+                     int dtype, int mode, void* stream);
 
 /*
  * Inference batch norm == reference `batch_norm_inference`

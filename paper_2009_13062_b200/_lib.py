@@ -58,7 +58,8 @@ SIGNATURES: dict[str, list] = {
     "nf_group_norm": [_p, _p, _p, _p, _p] + [_i64] * 9 + [_f, _i, _p],
     "nf_softmax": [_p, _p] + [_i64] * 6 + [_i, _p],
     "nf_attention": [_p, _p, _i64, _i64, _i64, _i64, _f, _i, _i, _p],
-    "nf_rel_attention": [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _f, _i, _i, _p],
+    "nf_rel_attention": [_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _f, _i, _i,
+                         _p],
     "nf_batch_norm": [_p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _f, _i, _p],
     "nf_pool2d": [_p, _p, _i64, _i64, _i, _i, _i, _i, _i, _i, _i, _p],
 }

@@ -488,7 +488,7 @@ template <typename T>
 __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restrict__ r,
                                      const float* __restrict__ rwb, const float* __restrict__ rrb,
                                      T* __restrict__ out, int64_t Bt, int S, int H, int dh,
-                                     int seqs_per_bias, float scale) {
+                                     int seqs_per_bias, int seqs_per_r, float scale) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -501,7 +501,7 @@ __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restr
     const int64_t b = u / (int64_t(S) * H);
     const int64_t inst = b / seqs_per_bias;
     const T* base = qkv + b * S * 3 * D;
-    const T* rb = r + b * 2 * S * D + int64_t(h) * dh;
+    const T* rb = r + (b / seqs_per_r) * 2 * S * D + int64_t(h) * dh;
     const T* q = base + int64_t(i) * 3 * D + int64_t(h) * dh;
     const float* bw = rwb + (inst * H + h) * dh;
     const float* br = rrb + (inst * H + h) * dh;
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(128, NBUF == 1 ? 2 : 1)
     k_rel_attention_tc(const __grid_constant__ CUtensorMap map_qkv,
                        const __grid_constant__ CUtensorMap map_r, const float* __restrict__ rwb,
                        const float* __restrict__ rrb, __nv_bfloat16* __restrict__ out, int H,
-                       int seqs_per_bias, int units, float scale_log2) {
+                       int seqs_per_bias, int seqs_per_r, int units, float scale_log2) {
   // NBUF == 2: persistent over units with the next unit's tiles loading into
   // the other buffer while this one computes (one CTA per SM).
   constexpr int S = kAttnS;
@@ -657,8 +657,9 @@ __global__ void __launch_bounds__(128, NBUF == 1 ? 2 : 1)
     tma_load_4d(q, &map_qkv, &bar_load[buf], 0, h, 0, bt, kEvictFirst);
     tma_load_4d(k, &map_qkv, &bar_load[buf], 0, H + h, 0, bt, kEvictFirst);
     tma_load_4d(v, &map_qkv, &bar_load[buf], 0, 2 * H + h, 0, bt, kEvictFirst);
-    tma_load_4d(kr, &map_r, &bar_load[buf], 0, h, 0, bt, kEvictFirst);
-    tma_load_4d(kr + kTileBytes, &map_r, &bar_load[buf], 0, h, S, bt, kEvictFirst);
+    // sequences of one instance share its projected positional keys
+    tma_load_4d(kr, &map_r, &bar_load[buf], 0, h, 0, bt / seqs_per_r, kEvictLast);
+    tma_load_4d(kr + kTileBytes, &map_r, &bar_load[buf], 0, h, S, bt / seqs_per_r, kEvictLast);
   };
   if (tid == 0) {
     grid_dependency_wait();
@@ -850,8 +851,9 @@ __global__ void __launch_bounds__(128, NBUF == 1 ? 2 : 1)
 
 int rel_attention(const void* qkv, const void* r, const float* rwb, const float* rrb, void* out,
                   int64_t Bt, int64_t S, int64_t H, int64_t dh, int64_t seqs_per_bias,
-                  float scale, int dtype, int mode, cudaStream_t stream) {
-  if (Bt < 1 || S < 1 || H < 1 || dh < 1 || seqs_per_bias < 1 || Bt % seqs_per_bias)
+                  int64_t seqs_per_r, float scale, int dtype, int mode, cudaStream_t stream) {
+  if (Bt < 1 || S < 1 || H < 1 || dh < 1 || seqs_per_bias < 1 || Bt % seqs_per_bias ||
+      seqs_per_r < 1 || Bt % seqs_per_r)
     return NF_ERR_SHAPE;
   if (dh > 128) return NF_ERR_UNSUPPORTED;
   const uintptr_t al = reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(r) |
@@ -860,7 +862,8 @@ int rel_attention(const void* qkv, const void* r, const float* rwb, const float*
   if (dtype == NF_BF16 && mode == NF_MODE_FAST && dh == kAttnD && S == kAttnS && (al & 15) == 0 &&
       Bt * H <= (int64_t(1) << 31) - 1) {
     CUtensorMap mq, mr;
-    if (!make_qkv_map(&mq, qkv, Bt, S, H) || !make_r_map(&mr, r, Bt, S, H)) return NF_ERR_LAUNCH;
+    if (!make_qkv_map(&mq, qkv, Bt, S, H) || !make_r_map(&mr, r, Bt / seqs_per_r, S, H))
+      return NF_ERR_LAUNCH;
     static bool attr_done = false;
     if (!attr_done) {
       cudaFuncSetAttribute(k_rel_attention_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -878,11 +881,11 @@ int rel_attention(const void* qkv, const void* r, const float* rwb, const float*
     if (units > 2 * kNumSMs && rel_persistent())
       e = launch_pdl(k_rel_attention_tc<2>, dim3(kNumSMs), dim3(128), rel_smem<2>(), stream, mq,
                      mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
-                     units, scale_log2);
+                     int(seqs_per_r), units, scale_log2);
     else
       e = launch_pdl(k_rel_attention_tc<1>, dim3(units), dim3(128), rel_smem<1>(), stream, mq,
                      mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
-                     units, scale_log2);
+                     int(seqs_per_r), units, scale_log2);
     return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
   }
   const int64_t warps = Bt * H * S;
@@ -891,12 +894,13 @@ int rel_attention(const void* qkv, const void* r, const float* rwb, const float*
   if (dtype == NF_F32)
     launch_pdl(k_rel_attention_simt<float>, dim3(unsigned(blocks)), dim3(256), 0, stream,
                static_cast<const float*>(qkv), static_cast<const float*>(r), rwb, rrb,
-               static_cast<float*>(out), Bt, int(S), int(H), int(dh), int(seqs_per_bias), scale);
+               static_cast<float*>(out), Bt, int(S), int(H), int(dh), int(seqs_per_bias),
+               int(seqs_per_r), scale);
   else if (dtype == NF_BF16)
     launch_pdl(k_rel_attention_simt<__nv_bfloat16>, dim3(unsigned(blocks)), dim3(256), 0, stream,
                static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(r), rwb,
                rrb, static_cast<__nv_bfloat16*>(out), Bt, int(S), int(H), int(dh),
-               int(seqs_per_bias), scale);
+               int(seqs_per_bias), int(seqs_per_r), scale);
   else
     return NF_ERR_UNSUPPORTED;
   return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;

@@ -108,11 +108,11 @@ int nf_attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, i
 
 int nf_rel_attention(const void* qkv, const void* r, const float* r_w_bias,
                      const float* r_r_bias, void* out, int64_t Bt, int64_t S, int64_t H,
-                     int64_t dh, int64_t seqs_per_bias, float scale, int dtype, int mode,
-                     void* stream) {
+                     int64_t dh, int64_t seqs_per_bias, int64_t seqs_per_r, float scale,
+                     int dtype, int mode, void* stream) {
   if (!qkv || !r || !r_w_bias || !r_r_bias || !out) return NF_ERR_SHAPE;
-  return nf::rel_attention(qkv, r, r_w_bias, r_r_bias, out, Bt, S, H, dh, seqs_per_bias, scale,
-                           dtype, mode, static_cast<cudaStream_t>(stream));
+  return nf::rel_attention(qkv, r, r_w_bias, r_r_bias, out, Bt, S, H, dh, seqs_per_bias,
+                           seqs_per_r, scale, dtype, mode, static_cast<cudaStream_t>(stream));
 }
 
 int nf_batch_norm(const void* x, const float* gamma, const float* beta, const float* mean,

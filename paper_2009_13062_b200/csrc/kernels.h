@@ -78,6 +78,6 @@ int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int6
               float scale, int dtype, int mode, cudaStream_t stream);
 int rel_attention(const void* qkv, const void* r, const float* rwb, const float* rrb, void* out,
                   int64_t Bt, int64_t S, int64_t H, int64_t dh, int64_t seqs_per_bias,
-                  float scale, int dtype, int mode, cudaStream_t stream);
+                  int64_t seqs_per_r, float scale, int dtype, int mode, cudaStream_t stream);
 
 }  // namespace nf

@@ -1061,13 +1061,17 @@ class Plan:
         rr = self._w(weights, node.weights[1], "vec_f32", x.dtype).reshape(-1, heads, dh)
         if bt % rw.shape[0]:
             raise ShapeError("bias instances do not divide the sequences")
+        br = r.numel() // (2 * s * d)  # positional-key blocks (one per instance when shared)
+        if br < 1 or bt % br:
+            raise ShapeError("positional keys do not tile the sequences")
         y = self._alloc(node.output_spec.dims, x.dtype)
         scale = node.attrs.get("scale") or 1.0 / math.sqrt(dh)
         xp, rp, yp = x.data_ptr(), r.data_ptr(), y.data_ptr()
-        wp, bp, spb = rw.data_ptr(), rr.data_ptr(), bt // rw.shape[0]
+        wp, bp, spb, spr = rw.data_ptr(), rr.data_ptr(), bt // rw.shape[0], bt // br
         dcode, mcode = K.dtype_code(x), self.mcode
         self._emit(node.id, lambda st: _lib.call("nf_rel_attention", xp, rp, wp, bp, yp, bt, s,
-                                                 heads, dh, spb, float(scale), dcode, mcode, st))
+                                                 heads, dh, spb, spr, float(scale), dcode, mcode,
+                                                 st))
         return DVal(y, node.output_spec.dims)
 
     def _norm(self, node, v, weights):

@@ -278,6 +278,9 @@ def rel_attention(qkv: torch.Tensor, r: torch.Tensor, r_w_bias: torch.Tensor,
     if qkv.shape[-1] != 3 * d or r.shape[-1] != d or r.shape[-2] != 2 * s or d % heads:
         raise ShapeError(f"rel attention operands {tuple(qkv.shape)} / {tuple(r.shape)}")
     bt = qkv.numel() // (s * 3 * d)
+    br = r.numel() // (2 * s * d)  # positional-key blocks, each shared by bt // br sequences
+    if br < 1 or bt % br:
+        raise ShapeError(f"positional keys {tuple(r.shape)} do not tile qkv {tuple(qkv.shape)}")
     rw = _f32(r_w_bias).reshape(-1, heads, dh)
     rr = _f32(r_r_bias).reshape(-1, heads, dh)
     if bt % rw.shape[0]:
@@ -286,7 +289,7 @@ def rel_attention(qkv: torch.Tensor, r: torch.Tensor, r_w_bias: torch.Tensor,
     sc = 1.0 / math.sqrt(dh) if scale is None else scale
     _lib.call("nf_rel_attention", qkv.contiguous().data_ptr(), r.contiguous().data_ptr(),
               rw.data_ptr(), rr.data_ptr(), y.data_ptr(), bt, s, heads, dh, bt // rw.shape[0],
-              float(sc), dtype_code(qkv), _MODES[mode], stream_ptr())
+              bt // br, float(sc), dtype_code(qkv), _MODES[mode], stream_ptr())
     return y
 
 

@@ -190,14 +190,15 @@ XLNET_BASE = XLNetConfig()
 def _xlnet(batch: int, dtype: str, cfg: XLNetConfig = XLNET_BASE) -> tuple[Graph, WeightPlan]:
     """XLNet-base encoder (attn_type "bi", no memory / segments / masks) on
     (B, S, 768) embeddings plus the sinusoidal relative positional embedding
-    input ``pos`` (B, 2S, 768). Per layer (transformers XLNetLayer): fused
+    input ``pos`` (1, 2S, 768), projected once per instance and shared by its
+    B sequences (transformers expands the same pos_emb over the batch). Per layer (transformers XLNetLayer): fused
     q|k|v projection (no bias), positional-key projection r, relative
     attention with per-instance r_w_bias / r_r_bias, output projection o (no
     bias), Add + LayerNorm, FF1 + GELU + FF2, Add + LayerNorm."""
     b, s, d, f, h = batch, cfg.seq, cfg.hidden, cfg.ffn, cfg.heads
     dh = d // h
     tok, qkv, wide = _spec(dtype, b, s, d), _spec(dtype, b, s, 3 * d), _spec(dtype, b, s, f)
-    rsp = _spec(dtype, b, 2 * s, d)
+    rsp = _spec(dtype, 1, 2 * s, d)  # shared by the batch: r projected once per instance
     nodes: list[OpNode] = []
     plan: WeightPlan = []
     x = "x:0"

@@ -212,15 +212,20 @@ def test_shape_errors_surface():
         GK.max_pool2d(torch.zeros(1, 1, 5, 5, device="cuda"), kernel=2, stride=2)
 
 
-@pytest.mark.parametrize("dtype,S,B,H", [(torch.float32, 33, 2, 4), (torch.bfloat16, 33, 2, 4),
-                                         (torch.bfloat16, 128, 2, 4), (torch.bfloat16, 128, 8, 12)])
-def test_rel_attention_vs_oracle(dtype, S, B, H):
+@pytest.mark.parametrize("dtype,S,B,H,shared", [(torch.float32, 33, 2, 4, False),
+                                                (torch.bfloat16, 33, 2, 4, True),
+                                                (torch.bfloat16, 128, 2, 4, False),
+                                                (torch.bfloat16, 128, 8, 12, False),
+                                                (torch.bfloat16, 128, 4, 12, True),
+                                                (torch.float32, 40, 3, 2, True)])
+def test_rel_attention_vs_oracle(dtype, S, B, H, shared):
     """S=128 bf16 takes the tcgen05 kernel (TMEM rel-shift; the 288-unit case
     runs the persistent double-buffered variant); the rest SIMT."""
     rng = np.random.default_rng(4)
     M, dh = 3, 64
     qkv = rng.uniform(-1, 1, (M, B, S, 3 * H * dh)).astype(np.float32)
-    r = rng.uniform(-1, 1, (M, B, 2 * S, H * dh)).astype(np.float32)
+    # shared: one positional-key block per instance, broadcast over its B sequences
+    r = rng.uniform(-1, 1, (M, 1 if shared else B, 2 * S, H * dh)).astype(np.float32)
     rw = rng.uniform(-.3, .3, (M, H, dh)).astype(np.float32)
     rr = rng.uniform(-.3, .3, (M, H, dh)).astype(np.float32)
     if dtype == torch.bfloat16:
