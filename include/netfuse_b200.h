@@ -158,7 +158,8 @@ int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* 
  */
 int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
-                     float scale, void* stream);
+                     float scale, const void* l2_prefetch, int64_t l2_prefetch_bytes,
+                     void* stream);
 
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
@@ -176,6 +177,20 @@ int64_t nf_linear_workspace_bytes(int64_t groups, int64_t rows, int64_t k, int64
  * split-K). Low-tile-count shapes (e.g. 8 instances x 768 features) split K
  * across otherwise idle SMs; partials reduce in split order (deterministic).
  */
+/*
+ * nf_grouped_linear_ws plus an L2 prefetch hint: once its own operand loads
+ * are issued, each CTA prefetches its share of [l2_prefetch,
+ * l2_prefetch + l2_prefetch_bytes) (the next weight-streaming launch's
+ * weights) into L2, so batch-1 plans keep HBM streaming across launches.
+ * NULL / 0 disables the hint.
+ */
+int nf_grouped_linear_ex(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const void* bias, const void* residual, void* y, int64_t y_ld,
+                         int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                         int dtype, int w_layout, int act, int mode, void* workspace,
+                         int64_t workspace_bytes, const void* l2_prefetch,
+                         int64_t l2_prefetch_bytes, void* stream);
+
 int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                          const void* bias, const void* residual, void* y, int64_t y_ld,
                          int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,

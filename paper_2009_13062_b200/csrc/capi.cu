@@ -22,11 +22,12 @@ int64_t nf_linear_workspace_bytes(int64_t groups, int64_t rows, int64_t k, int64
   return nf::linear_workspace_bytes(groups, rows, k, n);
 }
 
-int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+int nf_grouped_linear_ex(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                          const void* bias, const void* residual, void* y, int64_t y_ld,
                          int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
                          int dtype, int w_layout, int act, int mode, void* workspace,
-                         int64_t workspace_bytes, void* stream) {
+                         int64_t workspace_bytes, const void* l2_prefetch,
+                         int64_t l2_prefetch_bytes, void* stream) {
   if (!x || !w || !y || groups < 1 || rows < 1 || k < 1 || n < 1) return NF_ERR_SHAPE;
   if (x_ld < k || y_ld < n || (groups > 1 && (x_gs < 1 || y_gs < 1))) return NF_ERR_SHAPE;
   if (dtype != NF_F32 && dtype != NF_BF16) return NF_ERR_UNSUPPORTED;
@@ -36,11 +37,22 @@ int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* 
   const float* b = static_cast<const float*>(bias);
   if (mode == NF_MODE_FAST && dtype == NF_BF16 && w_layout == NF_W_NK) {
     int st = nf::grouped_linear_tc(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
-                                   n, dtype, act, workspace, workspace_bytes, s);
+                                   n, dtype, act, workspace, workspace_bytes, s, l2_prefetch,
+                                   l2_prefetch_bytes);
     if (st != NF_ERR_UNSUPPORTED) return st;
   }
   return nf::grouped_linear_simt(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
                                  n, dtype, w_layout, act, mode == NF_MODE_EXACT, s);
+}
+
+int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                         const void* bias, const void* residual, void* y, int64_t y_ld,
+                         int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                         int dtype, int w_layout, int act, int mode, void* workspace,
+                         int64_t workspace_bytes, void* stream) {
+  return nf_grouped_linear_ex(x, x_ld, x_gs, w, bias, residual, y, y_ld, y_gs, groups, rows, k, n,
+                              dtype, w_layout, act, mode, workspace, workspace_bytes, nullptr, 0,
+                              stream);
 }
 
 int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
@@ -172,10 +184,11 @@ int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* 
 
 int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
-                     float scale, void* stream) {
+                     float scale, const void* l2_prefetch, int64_t l2_prefetch_bytes,
+                     void* stream) {
   if (!x || !w || !out) return NF_ERR_SHAPE;
   return nf::qkv_attention_tc(x, x_ld, x_gs, w, bias, out, groups, seq, d_model, heads, scale,
-                              static_cast<cudaStream_t>(stream));
+                              static_cast<cudaStream_t>(stream), l2_prefetch, l2_prefetch_bytes);
 }
 
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,

@@ -210,6 +210,27 @@ NF_DEVICE void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, ui
       : "memory");
 }
 
+// L2 prefetch of a contiguous global range (bytes multiple of 16).
+NF_DEVICE void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gsrc)),
+               "r"(bytes)
+               : "memory");
+}
+// Each CTA of the grid prefetches its even share of [base, base + bytes) into
+// L2: a weight-streaming kernel warms the NEXT launch's weights once its own
+// loads are issued, so that launch's first TMA tiles hit L2.
+NF_DEVICE void prefetch_share_l2(const void* base, int64_t bytes) {
+  if (!base || bytes <= 0) return;
+  const int64_t per = ((bytes / gridDim.x) + 255) & ~int64_t(255);
+  int64_t lo = int64_t(blockIdx.x) * per;
+  const int64_t hi = lo + per < bytes ? lo + per : bytes;
+  const uint8_t* b = static_cast<const uint8_t*>(base);
+  for (; lo + 16 <= hi; lo += 65536) {
+    const int64_t n = hi - lo < 65536 ? ((hi - lo) & ~int64_t(15)) : 65536;
+    if (n > 0) bulk_prefetch_l2(b + lo, uint32_t(n));
+  }
+}
+
 // TMA bulk-tensor store smem -> global (bulk-group completion).
 NF_DEVICE void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
   asm volatile(

@@ -105,7 +105,8 @@ int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
 int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
-                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream) {
+                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
+                      const void* pf_next, int64_t pf_bytes) {
   // TMA needs 16-byte aligned row strides for x, w and y.
   if (out_dtype != NF_BF16 || K % 8 != 0 || N % 8 != 0) return NF_ERR_UNSUPPORTED;
   if (G > 65535 || T > (int64_t(1) << 30) || N > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
@@ -118,6 +119,8 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.features = int(N);
   p.groups = int(G);
   p.y_direct = y;
+  p.pf_next = pf_next;
+  p.pf_bytes = pf_bytes;
   p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
   const LinearPlan L = plan_linear(G, T, K, N, ws ? ws_bytes : 0);
   const bool swap = L.swap;

@@ -111,6 +111,10 @@ struct GemmParams {
   const float* ln_beta;
   float ln_eps;
   int ln_cluster;
+  // next weight-streaming launch's weights: prefetched into L2 by the
+  // producer once this CTA's own loads are issued (null: none)
+  const void* pf_next;
+  int64_t pf_bytes;
 };
 
 #ifndef NF_GEMM_LITE_KB
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         }
         pre = 0;
       }
+      prefetch_share_l2(p.pf_next, p.pf_bytes);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16_f32(kRowsA, BN);

@@ -11,7 +11,8 @@ namespace nf {
 int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
-                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream);
+                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
+                      const void* pf_next = nullptr, int64_t pf_bytes = 0);
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
 int grouped_linear_ln_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                          const float* bias, const void* residual, const float* gamma,
@@ -71,7 +72,7 @@ int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int 
 // qkv_attention.cu — fused QKV projection + attention, batch 1, S = 128.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream);
+                     cudaStream_t stream, const void* pf_next = nullptr, int64_t pf_bytes = 0);
 
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,

@@ -35,7 +35,8 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int chunk16) {
 __global__ void __launch_bounds__(192, 1)
     k_qkv_attention_tc(const __grid_constant__ CUtensorMap map_x,
                        const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
-                       __nv_bfloat16* __restrict__ out, int H, int kb_total, float scale_log2) {
+                       __nv_bfloat16* __restrict__ out, int H, int kb_total, float scale_log2,
+                       const void* pf_next, int64_t pf_bytes) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(192, 1)
         load_w(stage, kb);
         load_x(stage, kb);
       }
+      prefetch_share_l2(pf_next, pf_bytes);  // the next launch's weights into L2
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16_f32(128, 3 * kQD);
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(192, 1)
 // null; out (G, 128, D) bf16 context. heads * 64 == D.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, const void* pf_next, int64_t pf_bytes) {
   if (G < 1 || heads < 1 || D != heads * kQD) return NF_ERR_SHAPE;
   if (S != kQS || D % 64 || G * heads > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
@@ -274,7 +276,7 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
   const float sl2 = scale * 1.4426950408889634f;
   cudaError_t e = launch_pdl(k_qkv_attention_tc, dim3(unsigned(G * heads)), dim3(192), kQSmem,
                              stream, mx, mw, bias, static_cast<__nv_bfloat16*>(out), int(heads),
-                             int(D / 64), sl2);
+                             int(D / 64), sl2, pf_next, pf_bytes);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 

@@ -57,6 +57,7 @@ _MODES = {"fast": _lib.NF_MODE_FAST, "exact": _lib.NF_MODE_EXACT}
 # NF_SUPER_GROUP overrides (A/B knob).
 _SUPER_GROUP = int(__import__("os").environ.get("NF_SUPER_GROUP", "64"))
 _FUSE_LN = __import__("os").environ.get("NF_FUSE_LN", "0") == "1"
+_L2_PF = __import__("os").environ.get("NF_L2_PF", "0") == "1"  # measured slower (opt-in)
 
 
 @dataclass
@@ -151,6 +152,7 @@ class Plan:
         self.prefetch = prefetch
         self._add_into_norm: dict[str, str] = {}
         self._ln_done: set[str] = set()  # norms computed by a Linear epilogue
+        self._pf_sources: set[int] = set()  # launches that prefetch the next weights
         self._add_passthrough: dict[str, tuple[str, str]] = {}  # add -> (linear side, residual)
         self._cuda_graph: torch.cuda.CUDAGraph | None = None
         self.dispatch_count = 0
@@ -893,11 +895,15 @@ class Plan:
             y.data_ptr()
         dcode, mcode = K.dtype_code(x), self.mcode
         ws = self._workspace(groups, rows, k_in, n_out) if fast_tc else None
-        self._linear_w[len(self.steps)] = (w.data_ptr(), w.numel() * w.element_size())
+        idx = len(self.steps)
+        self._linear_w[idx] = (w.data_ptr(), w.numel() * w.element_size())
+        if fast_tc and rows <= 256:
+            self._pf_sources.add(idx)  # weight-streaming (batch-1) launch
         wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
         self._emit(node.id, lambda st: _lib.call(
-            "nf_grouped_linear_ws", xp, k_in, rows * k_in, wp, bp, None, yp, n_out,
-            rows * n_out, groups, rows, k_in, n_out, dcode, layout, act, mcode, wsp, wsb, st))
+            "nf_grouped_linear_ex", xp, k_in, rows * k_in, wp, bp, None, yp, n_out,
+            rows * n_out, groups, rows, k_in, n_out, dcode, layout, act, mcode, wsp, wsb,
+            *self._pf_hint(idx), st))
         return DVal(y, node.output_spec.dims)
 
     def _linear_ln_chain(self, node, ins, weights, users, outputs):
@@ -1030,10 +1036,28 @@ class Plan:
         scale = 1.0 / math.sqrt(d // heads)
         xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, \
             y.data_ptr()
-        self._linear_w[len(self.steps)] = (wp, w.numel() * w.element_size())
+        idx = len(self.steps)
+        self._linear_w[idx] = (wp, w.numel() * w.element_size())
+        self._pf_sources.add(idx)
         self._emit(attn.id, lambda st: _lib.call("nf_qkv_attention", xp, d, 128 * d, wp, bp, yp,
-                                                 groups, 128, d, heads, float(scale), st))
+                                                 groups, 128, d, heads, float(scale),
+                                                 *self._pf_hint(idx), st))
         return DVal(y, attn.output_spec.dims)
+
+    def _pf_hint(self, idx: int) -> tuple:
+        """(pointer, bytes) of the next weight-streaming launch's weights for
+        the launch at step ``idx`` to prefetch into L2 once its own loads are
+        issued (batch-1 plans: HBM keeps streaming across attention / norm
+        launches), or (None, 0)."""
+        if not _L2_PF or idx not in self._pf_sources:
+            return (None, 0)
+        later = [j for j in self._linear_w if j > idx]
+        if not later:
+            return (None, 0)
+        ptr, nbytes = self._linear_w[min(later)]
+        if nbytes > 64 * 1024 * 1024:  # keep the prefetch well inside the 126 MB L2
+            return (None, 0)
+        return (ptr, nbytes)
 
     def _attention(self, node, v):
         x = self._materialize(node.id, v)

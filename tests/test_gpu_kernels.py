@@ -134,7 +134,8 @@ def test_fused_qkv_attention_vs_oracle(g, h):
     bt = cuda(b)
     y = torch.empty(g, 128, d, dtype=torch.bfloat16, device="cuda")
     _lib.call("nf_qkv_attention", xt.data_ptr(), d, 128 * d, wt.data_ptr(), bt.data_ptr(),
-              y.data_ptr(), g, 128, d, h, 1.0 / 8.0, torch.cuda.current_stream().cuda_stream)
+              y.data_ptr(), g, 128, d, h, 1.0 / 8.0, None, 0,
+              torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert normwise(host(y), want) < 2e-2
 
