@@ -351,6 +351,8 @@ def unmerged_legs(args, graph, stores, inputs, heads, flush, stream, merged_valu
     PAPER.md:394-399 "sequential" baseline):
       * ours_sequential: this framework's kernels at M=1, N per-instance plans
         (backbone + head) recorded into one CUDA graph;
+      * ours_concurrent: the same N plans on N streams of one graph (the
+        paper's concurrent baseline);
       * torch_eager_sequential: stock PyTorch ops (cuBLAS / cuDNN / SDPA),
         eager, one instance after another;
       * torch_graph_sequential: the same PyTorch ops captured in a CUDA graph
@@ -390,6 +392,34 @@ def unmerged_legs(args, graph, stores, inputs, heads, flush, stream, merged_valu
                               "kernel_launches": sum(p.kernel_launches +
                                                      (hp.kernel_launches if hp else 0)
                                                      for p, hp in plans)}
+    del g
+
+    # the paper's "concurrent" baseline: the N separate
+    # forwards on N streams of one CUDA graph, free to overlap on the GPU
+    streams = [torch.cuda.Stream() for _ in plans]
+
+    def ours_concurrent():
+        cur = torch.cuda.current_stream()
+        for s_ in streams:
+            s_.wait_stream(cur)
+        for (p, hp), s_ in zip(plans, streams):
+            with torch.cuda.stream(s_):
+                p.launch()
+                if hp is not None:
+                    hp.input_views["feat"].copy_(p.outputs()[0])
+                    hp.launch()
+        for s_ in streams:
+            cur.wait_stream(s_)
+
+    ours_concurrent()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ours_concurrent()
+    _time_steps(g.replay, 3, flush, stream)
+    ms = _time_steps(g.replay, steps, flush, stream)
+    out["ours_concurrent"] = {"value": round(items / (ms / 1e3), 2), "ms_per_step": round(ms, 4),
+                              "streams": len(streams)}
     del g, plans
 
     models = []
@@ -430,7 +460,7 @@ def unmerged_legs(args, graph, stores, inputs, heads, flush, stream, merged_valu
                                      "ms_per_step": round(ms, 4)}
     del g, models
     out["speedup"] = {k: round(merged_value / out[k]["value"], 3)
-                      for k in ("ours_sequential", "torch_eager_sequential",
+                      for k in ("ours_sequential", "ours_concurrent", "torch_eager_sequential",
                                 "torch_graph_sequential")}
     torch.cuda.empty_cache()
     return out
