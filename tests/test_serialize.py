@@ -11,12 +11,14 @@ import numpy as np
 import pytest
 import torch
 
+import importlib
+
 from paper_2009_13062_b200 import build_zoo, merge, model_inputs
-from paper_2009_13062_b200 import serialize as S
 from paper_2009_13062_b200.errors import GraphFormatError, UnsupportedOpError
 from paper_2009_13062_b200.ir import TensorSpec
 from paper_2009_13062_b200.tensors import TensorValue
 
+S = importlib.import_module("paper_2009_13062_b200.serialize")  # the module, not the function
 ART = Path(__file__).parent / "golden" / "artifacts"
 CASES = json.loads((ART / "tensors.json").read_text())
 
