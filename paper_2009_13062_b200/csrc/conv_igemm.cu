@@ -62,10 +62,21 @@ int conv_pick(int64_t pix, int64_t coutg, bool* swap) {
   return 256;
 }
 
+// Max split-K factor for convs (knob NF_CONV_MAXSPLIT, read once): the last
+// arriving split reduces every partial of its tile alone, so deep splits
+// trade HBM streaming parallelism for a serial fix-up.
+int conv_max_splits() {
+  static const int v = [] {
+    const char* e = getenv("NF_CONV_MAXSPLIT");
+    return e ? atoi(e) : 4;
+  }();
+  return v < 1 ? 1 : (v > kMaxSplits ? kMaxSplits : v);
+}
+
 int conv_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) {
   if (ws_bytes <= kCounterBytes || tiles >= 96 || tiles > kCounterBytes / 4) return 1;
   int s = int(kNumSMs / tiles);
-  s = s < kMaxSplits ? s : kMaxSplits;
+  s = s < conv_max_splits() ? s : conv_max_splits();
   s = s < kb_total / 4 ? s : kb_total / 4;  // >= 4 K blocks per split
   while (s > 1 && tiles * s * int64_t(kGemmBM) * bn * 4 > ws_bytes - kCounterBytes) --s;
   return s < 1 ? 1 : s;
@@ -121,7 +132,7 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   const int64_t halo_bytes = (halo_raw + 1023) / 1024 * 1024;
   // (4-channel groups work too — the padded stem — but measured slower than
   // the 8-byte cp.async gather: a 7x7/s2 halo is barely smaller than 49 taps.)
-  const bool halo = halo_enabled() && !swap && N == 1 &&
+  bool halo = halo_enabled() && !swap && N == 1 &&
                     (cg == 16 || cg == 32 || cg == 64 || (cg == 4 && halo_stem())) &&
                     bn <= 64 && halo_h <= 256 && halo_w <= 256 && halo_bytes <= 48 * 1024;
 
@@ -138,8 +149,9 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   p.cH = H; p.cW = W; p.cC = C; p.cCg = cg; p.cK = k; p.cS = stride; p.cP = pad;
   p.cHo = Ho; p.cWo = Wo;
   CUtensorMap mw, my, mr, mh;
+  if (halo && !make_halo_map(&mh, x, N, H, W, C, halo_cpp, halo_w, halo_h))
+    halo = false;  // e.g. pixel rows not 16-byte multiples: per-tap gather instead
   if (halo) {
-    if (!make_halo_map(&mh, x, N, H, W, C, halo_cpp, halo_w, halo_h)) return NF_ERR_UNSUPPORTED;
     p.halo_w = halo_w;
     p.halo_cpp = halo_cpp;
     p.halo_bytes = int(halo_bytes);

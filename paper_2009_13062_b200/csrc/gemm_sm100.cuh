@@ -875,33 +875,42 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
         const int stage = it % kStages;
         mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
-        // chunk j = K elements [k0, k0+8): one tap when cg >= 8, two 4-channel
-        // taps (8-byte halves) when cg == 4 (the padded stem)
         const int k0 = kb * kGemmBK + j * 8;
-        int off[2];
-        bool okh[2];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int kx = k0 + hh * 4;
-          const int tap = kx / p.cCg;
-          const int ch = kx - tap * p.cCg;
-          const int kh = tap / p.cK;
-          off[hh] = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp + ch;
-          okh[hh] = tap < taps;
-        }
         const uint32_t sbase = smem_u32(sA + stage * C::kABytes);
+        if (p.cCg >= 8) {
+          // chunk j = K elements [k0, k0+8) of one tap: one 16-byte copy per row
+          const int tap = k0 / p.cCg;
+          const int ch = k0 - tap * p.cCg;
+          const int kh = tap / p.cK;
+          const int tap_off = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp + ch;
+          const bool tap_ok = tap < taps;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = rb + 16 * i;
-          uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-          if (hoff[i] >= 0) {
-            const uint32_t pix = hsrc + uint32_t(hoff[i] * p.halo_cpp * 2);
-            if (p.cCg >= 8) {
-              if (okh[0])
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                             : "r"(pix + uint32_t(off[0] * 2)));
-            } else {
+          for (int i = 0; i < 8; ++i) {
+            const int r = rb + 16 * i;
+            uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+            if (tap_ok && hoff[i] >= 0)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                           : "r"(hsrc + uint32_t((hoff[i] * p.halo_cpp + tap_off) * 2)));
+            st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v0, v1, v2, v3);
+          }
+        } else {
+          // 4-channel groups (padded stem): two taps per 16-byte chunk
+          int off[2];
+          bool okh[2];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int tap = (k0 + hh * 4) / p.cCg;
+            const int kh = tap / p.cK;
+            off[hh] = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp;
+            okh[hh] = tap < taps;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = rb + 16 * i;
+            uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+            if (hoff[i] >= 0) {
+              const uint32_t pix = hsrc + uint32_t(hoff[i] * p.halo_cpp * 2);
               if (okh[0])
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
                              : "=r"(v0), "=r"(v1)
@@ -911,8 +920,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                              : "=r"(v2), "=r"(v3)
                              : "r"(pix + uint32_t(off[1] * 2)));
             }
+            st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v0, v1, v2, v3);
           }
-          st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v0, v1, v2, v3);
         }
         fence_proxy_async_smem();
         mbar_arrive(&full[stage]);
