@@ -562,6 +562,13 @@ __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restr
 // ---------------------------------------------------------------------------
 constexpr int kRelPitch = 68;                           // words per staged row
 constexpr int kRelStageBytes = 4 * 32 * kRelPitch * 4;  // 34816 B (4 warps)
+inline bool rel_eight_warps() {
+  static const bool on = [] {
+    const char* e = getenv("NF_REL_8WARPS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 inline bool rel_persistent() {
   static const bool on = [] {
     const char* e = getenv("NF_REL_PERSISTENT");
@@ -847,6 +854,238 @@ __global__ void __launch_bounds__(128, NBUF == 1 ? 2 : 1)
   }
 }
 
+// 8-warp variant (one CTA per (sequence, head), two CTAs per SM): warps w
+// and w + 4 share TMEM lane quarter w & 3 and split the 128 key columns in
+// halves, so each thread holds 64 scores (no spills), the rel-shift windows
+// of the two halves run in parallel, and the row max / sum combine through
+// shared memory. Shift windows: warps 0-3 in the Q|K|pad region, warps 4-7
+// in KR + its 4 KB tail (both free once the raw MMA retired).
+constexpr size_t kRel8Smem = 1024 + 2 * kTileBytes + 4096 + kTileBytes + 2 * kTileBytes + 4096 +
+                             (128 + 256 + 128 + 4 * 128) * 4 + 64;
+
+__global__ void __launch_bounds__(256, 2)
+    k_rel_attention_tc8(const __grid_constant__ CUtensorMap map_qkv,
+                        const __grid_constant__ CUtensorMap map_r, const float* __restrict__ rwb,
+                        const float* __restrict__ rrb, __nv_bfloat16* __restrict__ out, int H,
+                        int seqs_per_bias, int seqs_per_r, float scale_log2) {
+  constexpr int S = kAttnS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTileBytes;
+  uint8_t* sV = sK + kTileBytes + 4096;
+  uint8_t* sKR = sV + kTileBytes;  // 256 rows; later P (128 x 128) + shift windows
+  float* sBw = reinterpret_cast<float*>(sKR + 2 * kTileBytes + 4096);
+  float* sCr = sBw + 128;
+  float* sRb = sCr + 256;   // r_w_bias | r_r_bias
+  float* sMax = sRb + 128;  // [2][128]
+  float* sSum = sMax + 256; // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSum + 256);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_s = bars + 1;
+  uint64_t* bar_bd = bars + 2;
+  uint64_t* bar_o = bars + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int quarter = warp & 3;
+  const int half = warp >> 2;  // key columns [64*half, 64*half + 64)
+  const int i_row = quarter * 32 + lane;
+  const int bt = blockIdx.x / H;
+  const int h = blockIdx.x % H;
+  const int inst = bt / seqs_per_bias;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&map_qkv);
+    tma_prefetch_desc(&map_r);
+    mbar_init(bar_load, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_bd, 1);
+    mbar_init(bar_o, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+
+  if (tid == 0) {
+    grid_dependency_wait();
+    mbar_arrive_expect_tx(bar_load, 5 * kTileBytes);
+    tma_load_4d(sQ, &map_qkv, bar_load, 0, h, 0, bt, kEvictFirst);
+    tma_load_4d(sK, &map_qkv, bar_load, 0, H + h, 0, bt, kEvictFirst);
+    tma_load_4d(sV, &map_qkv, bar_load, 0, 2 * H + h, 0, bt, kEvictFirst);
+    tma_load_4d(sKR, &map_r, bar_load, 0, h, 0, bt / seqs_per_r, kEvictLast);
+    tma_load_4d(sKR + kTileBytes, &map_r, bar_load, 0, h, S, bt / seqs_per_r, kEvictLast);
+  }
+  grid_dependents_launch();
+  if (tid < 64) {
+    const float* src = tid < 32 ? rwb : rrb;
+    const int d = (tid & 31) * 2;
+    const float2 v = *reinterpret_cast<const float2*>(src + (int64_t(inst) * H + h) * kAttnD + d);
+    sRb[(tid < 32 ? 0 : 64) + d] = v.x;
+    sRb[(tid < 32 ? 0 : 64) + d + 1] = v.y;
+  }
+  mbar_wait(bar_load, 0);
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 128);
+    const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK);
+#pragma unroll
+    for (int kk = 0; kk < kAttnD / 16; ++kk)
+      umma_f16_ss(tmem, make_sw128_kmajor_desc(qa + kk * 32),
+                  make_sw128_kmajor_desc(ka + kk * 32), idesc, kk != 0);
+    umma_commit(bar_s);
+  }
+  __syncthreads();  // bias vectors in smem
+  // bias . key rows (fp32): bw for the 128 keys, cr for the 256 positions
+  if (tid < 128) {
+    sBw[tid] = bias_dot_row(sK, tid, sRb);
+    sCr[tid] = bias_dot_row(sKR, tid, sRb + 64);
+  } else {
+    sCr[tid] = bias_dot_row(sKR, tid, sRb + 64);
+  }
+
+  mbar_wait(bar_s, 0);
+  tc_fence_after();
+  uint32_t r[2][32];  // AC of this row, key columns 64*half ..
+#pragma unroll
+  for (int c = 0; c < 2; ++c) tmem_ld_32x32b_x32(lane_base + uint32_t(64 * half + c * 32), r[c]);
+  tmem_ld_wait();
+  tc_fence_before();
+  __syncthreads();  // AC consumed; bias vectors visible
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 256);
+    const uint32_t qa = smem_u32(sQ), ra = smem_u32(sKR);
+#pragma unroll
+    for (int kk = 0; kk < kAttnD / 16; ++kk)
+      umma_f16_ss(tmem, make_sw128_kmajor_desc(qa + kk * 32),
+                  make_sw128_kmajor_desc(ra + kk * 32), idesc, kk != 0);
+    umma_commit(bar_bd);
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      r[c][j] = __float_as_uint(__uint_as_float(r[c][j]) + sBw[64 * half + c * 32 + j]);
+
+  mbar_wait(bar_bd, 0);
+  tc_fence_after();
+  uint8_t* wbuf = (half == 0 ? sQ : sKR) + quarter * 32 * kRelPitch * 4;
+  const uint32_t stage_w = smem_u32(wbuf);
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int c = 2 * half + cc;             // global 32-key chunk
+    const int p0 = 97 - 32 * quarter + 32 * c;  // window start for lane 31, jj 0
+    const int base = p0 < 192 ? p0 : 192;
+    const int shift = 31 - lane + (p0 - base);
+    __syncwarp();
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      uint32_t wv[32];
+      tmem_ld_32x32b_x32(lane_base + uint32_t(base + 32 * hh), wv);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        st_shared_v4(stage_w + uint32_t((lane * kRelPitch + 32 * hh + 4 * q) * 4), wv[4 * q],
+                     wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
+    }
+    __syncwarp();
+    const float* row = reinterpret_cast<const float*>(wbuf) + lane * kRelPitch + shift;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const int p = S - i_row + c * 32 + jj;
+      r[cc][jj] = __float_as_uint(__uint_as_float(r[cc][jj]) + row[jj] + sCr[p]);
+    }
+  }
+  float mx = -INFINITY;
+  {
+    float m8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) m8[q] = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) m8[j & 7] = fmaxf(m8[j & 7], __uint_as_float(r[c][j]));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mx = fmaxf(mx, m8[q]);
+  }
+  sMax[half * 128 + i_row] = mx;
+  tc_fence_before();
+  __syncthreads();  // both halves' maxima; every raw TMEM / window read done
+  mx = fmaxf(sMax[i_row], sMax[128 + i_row]);
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  const uint32_t prow = smem_u32(sKR);  // P overwrites KR (and the half-1 windows)
+  const float mxs = mx * scale_log2;
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int c = 2 * half + cc;
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const float x0 = fmaf(__uint_as_float(r[cc][j]), scale_log2, -mxs);
+      const float x1 = fmaf(__uint_as_float(r[cc][j + 1]), scale_log2, -mxs);
+      const uint32_t packed = pack_bf16x2(ex2_approx(x0), ex2_approx(x1));
+      s4[(j >> 1) & 3] += __uint_as_float(packed << 16) + __uint_as_float(packed & 0xffff0000u);
+      pk[j >> 1] = packed;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      st_shared_v4(prow + kmajor_off(i_row, c * 32 + q * 8, 128), pk[4 * q], pk[4 * q + 1],
+                   pk[4 * q + 2], pk[4 * q + 3]);
+  }
+  sSum[half * 128 + i_row] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();  // P complete
+
+  if (tid == 0) {
+    tc_fence_after();
+    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64, 0, 1);
+    const uint32_t pa = smem_u32(sKR), va = smem_u32(sV);
+#pragma unroll
+    for (int kk = 0; kk < kAttnS / 16; ++kk) {
+      const int blk = kk >> 2, sub = kk & 3;
+      umma_f16_ss(tmem, make_sw128_kmajor_desc(pa + blk * 128 * 128 + sub * 32),
+                  make_sw128_mnmajor_desc(va + kk * 16 * 128, 8192, 1024), idesc, kk != 0);
+    }
+    umma_commit(bar_o);
+  }
+  mbar_wait(bar_o, 0);
+  tc_fence_after();
+  {
+    uint32_t o[32];
+    tmem_ld_32x32b_x32(lane_base + uint32_t(32 * half), o);
+    tmem_ld_wait();
+    const float inv = 1.0f / (sSum[i_row] + sSum[128 + i_row]);
+    const int64_t D = int64_t(H) * kAttnD;
+    __nv_bfloat16* dst = out + (int64_t(bt) * S + i_row) * D + int64_t(h) * kAttnD + 32 * half;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+      u.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+      u.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+      u.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+      *reinterpret_cast<uint4*>(dst + q * 8) = u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
 }  // namespace
 
 int rel_attention(const void* qkv, const void* r, const float* rwb, const float* rrb, void* out,
@@ -875,10 +1114,21 @@ int rel_attention(const void* qkv, const void* r, const float* rwb, const float*
     const int units = int(Bt * H);
     const float scale_log2 = scale * 1.4426950408889634f;
     cudaError_t e;
-    // The persistent double-buffered variant (NBUF = 2, one CTA per SM)
-    // measured slower (92 vs 79 us per XLNet-base layer at 1536 units) than
-    // two single-buffered CTAs per SM, whose chains overlap each other.
-    if (units > 2 * kNumSMs && rel_persistent())
+    // Default: the 8-warp kernel (two warps per TMEM lane quarter). The
+    // persistent double-buffered variant (NBUF = 2, one CTA per SM) measured
+    // slower (92 vs 79 us per XLNet-base layer at 1536 units) than two
+    // single-buffered CTAs per SM, whose chains overlap each other.
+    if (rel_eight_warps()) {
+      static bool attr8 = false;
+      if (!attr8) {
+        cudaFuncSetAttribute(k_rel_attention_tc8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kRel8Smem));
+        attr8 = true;
+      }
+      e = launch_pdl(k_rel_attention_tc8, dim3(units), dim3(256), kRel8Smem, stream, mq, mr, rwb,
+                     rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
+                     int(seqs_per_r), scale_log2);
+    } else if (units > 2 * kNumSMs && rel_persistent())
       e = launch_pdl(k_rel_attention_tc<2>, dim3(kNumSMs), dim3(128), rel_smem<2>(), stream, mq,
                      mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
                      int(seqs_per_r), units, scale_log2);
