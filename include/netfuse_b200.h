@@ -161,6 +161,35 @@ int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
                      float scale, const void* l2_prefetch, int64_t l2_prefetch_bytes,
                      void* stream);
 
+/*
+ * Folded LayerNorm (batch-1 encoders). The merged graph's Add -> GroupNorm
+ * over each instance's D features (reference add engine.py:322-325,
+ * group_norm 263-284) is not launched: the Linear producing the Add's
+ * operand adds the residual in its epilogue and writes per-token partial
+ * sums `out_stats` [g][part][token] (sum, sum of squares; part = 128-feature
+ * tile, ceil(n/128) parts). Consumers rebuild LN(v) from the raw v:
+ *  - as the activations of a Linear (in_*): w holds gamma-scaled weights
+ *    W'[g][n][k] = W[g][n][k] * gamma[g][k], bias b' = b + W beta, in_colsum
+ *    (G, n) = sum_k W'[g][n][k]; y = rstd * (x W'^T - mean * colsum) + b';
+ *  - as the residual (res_*): (r - mean) * rstd * res_gamma + res_beta.
+ * nf_linear_fold_supported(...) is 1 where the kernel implements it (the
+ * swapped 128-token tile path); elsewhere the fold entry points return 2.
+ * Statistics are fp32 and the reduction order fixed (deterministic).
+ */
+int nf_linear_fold_supported(int64_t groups, int64_t rows, int64_t k, int64_t n);
+int nf_grouped_linear_fold(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                           const void* bias, const void* residual, void* y, int64_t y_ld,
+                           int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                           int act, void* workspace, int64_t workspace_bytes,
+                           const float* in_stats, int in_parts, const float* in_colsum,
+                           float in_eps, const float* res_stats, int res_parts,
+                           const float* res_gamma, const float* res_beta, float res_eps,
+                           float* out_stats, void* stream);
+int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                          const float* bias, void* out, int64_t groups, int64_t seq,
+                          int64_t d_model, int64_t heads, float scale, const float* in_stats,
+                          int in_parts, const float* in_colsum, float in_eps, void* stream);
+
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream);

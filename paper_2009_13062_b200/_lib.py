@@ -54,6 +54,11 @@ SIGNATURES: dict[str, list] = {
     "nf_qkv_attention": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f, _p, _i64, _p],
     "nf_grouped_linear_ex": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                              _i64, _i, _i, _i, _i, _p, _i64, _p, _i64, _p],
+    "nf_linear_fold_supported": [_i64, _i64, _i64, _i64],
+    "nf_grouped_linear_fold": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                               _i64, _i, _p, _i64, _p, _i, _p, _f, _p, _i, _p, _p, _f, _p, _p],
+    "nf_qkv_attention_fold": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f,
+                              _p, _i, _p, _f, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],

@@ -191,6 +191,40 @@ int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
                               static_cast<cudaStream_t>(stream), l2_prefetch, l2_prefetch_bytes);
 }
 
+int nf_linear_fold_supported(int64_t groups, int64_t rows, int64_t k, int64_t n) {
+  return nf::linear_fold_supported(groups, rows, k, n) ? 1 : 0;
+}
+
+int nf_grouped_linear_fold(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                           const void* bias, const void* residual, void* y, int64_t y_ld,
+                           int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                           int act, void* workspace, int64_t workspace_bytes,
+                           const float* in_stats, int in_parts, const float* in_colsum,
+                           float in_eps, const float* res_stats, int res_parts,
+                           const float* res_gamma, const float* res_beta, float res_eps,
+                           float* out_stats, void* stream) {
+  if (!x || !w || !y || groups < 1 || rows < 1 || k < 1 || n < 1) return NF_ERR_SHAPE;
+  if (x_ld < k || y_ld < n || (groups > 1 && (x_gs < 1 || y_gs < 1))) return NF_ERR_SHAPE;
+  if (act < NF_ACT_NONE || act > NF_ACT_TANH) return NF_ERR_UNSUPPORTED;
+  const nf::NormFold fold{in_stats, in_colsum, in_parts, in_eps, res_stats,
+                          res_gamma, res_beta, res_parts, res_eps, out_stats};
+  return nf::grouped_linear_tc(x, x_ld, x_gs, w, static_cast<const float*>(bias), residual, y,
+                               y_ld, y_gs, groups, rows, k, n, NF_BF16, act, workspace,
+                               workspace_bytes, static_cast<cudaStream_t>(stream), nullptr, 0,
+                               &fold);
+}
+
+int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                          const float* bias, void* out, int64_t groups, int64_t seq,
+                          int64_t d_model, int64_t heads, float scale, const float* in_stats,
+                          int in_parts, const float* in_colsum, float in_eps, void* stream) {
+  if (!x || !w || !out) return NF_ERR_SHAPE;
+  const nf::NormFold fold{in_stats, in_colsum, in_parts, in_eps, nullptr,
+                          nullptr, nullptr, 0, 0.f, nullptr};
+  return nf::qkv_attention_tc(x, x_ld, x_gs, w, bias, out, groups, seq, d_model, heads, scale,
+                              static_cast<cudaStream_t>(stream), nullptr, 0, &fold);
+}
+
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream) {
   if (!x || !y || N < 1 || H < 1 || W < 1 || C < 1) return NF_ERR_SHAPE;

@@ -493,4 +493,24 @@ NF_DEVICE void pdl_enter() {
   grid_dependents_launch();
 }
 
+// Per-token (mean, rstd) of a folded LayerNorm from its producer's partial sums.
+NF_DEVICE float2 fold_stats(const float2* st, int parts, int rows, int g, int tok, float inv_d,
+                            float eps) {
+  float s = 0.f, ss = 0.f;
+  for (int q0 = 0; q0 < parts; q0 += 8) {
+    float2 v[8];  // up to 8 partials in flight (D <= 1024 in one round trip)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = q0 + i < parts ? __ldcg(st + (int64_t(g) * parts + q0 + i) * rows + tok)
+                            : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s += v[i].x;
+      ss += v[i].y;
+    }
+  }
+  const float mu = s * inv_d;
+  return make_float2(mu, rsqrtf(fmaxf(ss * inv_d - mu * mu, 0.f) + eps));
+}
+
 }  // namespace nf

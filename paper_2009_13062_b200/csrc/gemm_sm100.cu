@@ -91,6 +91,14 @@ static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_
   return L;
 }
 
+// Folded LayerNorms are implemented for swapped, staged 128-token tiles
+// (batch-1 encoders): the plan asks before folding.
+bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
+  if (G < 1 || K % 8 || N % 8 || G > 65535) return false;
+  const LinearPlan L = plan_linear(G, T, K, N, 0);
+  return L.swap && !L.pair && L.bn == 128 && GemmOut<128, true>::kStaged;
+}
+
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
   const LinearPlan L = plan_linear(G, T, K, N, INT64_MAX);
   if (L.splits <= 1) return 0;
@@ -106,7 +114,7 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const void* pf_next, int64_t pf_bytes) {
+                      const void* pf_next, int64_t pf_bytes, const NormFold* fold) {
   // TMA needs 16-byte aligned row strides for x, w and y.
   if (out_dtype != NF_BF16 || K % 8 != 0 || N % 8 != 0) return NF_ERR_UNSUPPORTED;
   if (G > 65535 || T > (int64_t(1) << 30) || N > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
@@ -123,6 +131,25 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.pf_bytes = pf_bytes;
   p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
   const LinearPlan L = plan_linear(G, T, K, N, ws ? ws_bytes : 0);
+  if (fold) {
+    if (!linear_fold_supported(G, T, K, N)) return NF_ERR_UNSUPPORTED;
+    if ((fold->in_stats && (!fold->in_colsum || fold->in_parts < 1)) ||
+        (fold->res_stats && (!residual || !fold->res_gamma || !fold->res_beta ||
+                             fold->res_parts < 1)))
+      return NF_ERR_SHAPE;
+    p.nin_stats = reinterpret_cast<const float2*>(fold->in_stats);
+    p.nin_colsum = fold->in_colsum;
+    p.nin_parts = fold->in_parts;
+    p.nin_inv_d = 1.0f / float(K);
+    p.nin_eps = fold->in_eps;
+    p.nres_stats = reinterpret_cast<const float2*>(fold->res_stats);
+    p.nres_gamma = fold->res_gamma;
+    p.nres_beta = fold->res_beta;
+    p.nres_parts = fold->res_parts;
+    p.nres_inv_d = 1.0f / float(N);
+    p.nres_eps = fold->res_eps;
+    p.nout_stats = reinterpret_cast<float2*>(fold->out_stats);
+  }
   const bool swap = L.swap;
   const int bn = L.bn;
   const int bbox = L.pair ? bn / 2 : bn;  // B rows each CTA loads

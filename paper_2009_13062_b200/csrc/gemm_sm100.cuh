@@ -115,7 +115,26 @@ struct GemmParams {
   // producer once this CTA's own loads are issued (null: none)
   const void* pf_next;
   int64_t pf_bytes;
+  // Folded LayerNorms (swapped staged tiles): LN(v) over an instance's D
+  // features per token is never materialised; its producer writes per-token
+  // partial sums (sum, sum of squares) for each of its 128-feature tiles,
+  // [g][part][token], and consumers rebuild the normalised value.
+  //  in : B operand (tokens) = LN(x); the weights carry gamma, the bias beta,
+  //       colsum[g][n] = sum_k W'[g][n][k]:  y = rstd * (x W'^T - mean * colsum) + b'
+  //  res: residual = LN(r) = (r - mean) * rstd * gamma[n] + beta[n]
+  //  out: this launch's output tiles feed a later LN: write their partial sums
+  const float2* nin_stats;
+  const float* nin_colsum;
+  int nin_parts;
+  float nin_inv_d, nin_eps;
+  const float2* nres_stats;
+  const float* nres_gamma;
+  const float* nres_beta;
+  int nres_parts;
+  float nres_inv_d, nres_eps;
+  float2* nout_stats;
 };
+
 
 #ifndef NF_GEMM_LITE_KB
 #define NF_GEMM_LITE_KB 100  // swapped (weight-streaming) tiles: 2 CTAs per SM
@@ -169,8 +188,10 @@ struct GemmCfg {
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
+  // folded-LN per-token (mean, rstd) of the B operand and of the residual
+  static constexpr int kNormBytes = (SWAP && kStaged && !PAIR && !GATHER) ? 4 * BN * 4 : 0;
   static constexpr size_t kBytes =
-      1024 + size_t(kStages) * kStageBytes + kOutBytes + 512;
+      1024 + size_t(kStages) * kStageBytes + kOutBytes + 512 + kNormBytes;
   static_assert(kStages >= 3, "pipeline too shallow");
   static_assert(kStages <= 32, "barrier array");
   static_assert(kTmemCols <= 512, "TMEM overflow");
@@ -263,6 +284,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   uint64_t* lnbar = hbar + 2;  // LNF: cluster partial-sum arrivals
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lnbar + 1);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  float* sNorm = reinterpret_cast<float*>(sOut + C::kOutBytes + 512);  // C::kNormBytes
+  constexpr bool kFold = C::kNormBytes > 0 && !LNF;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -578,6 +601,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     const int row = quarter * 32 + lane;  // accumulator row == TMEM lane
     const int etid = threadIdx.x - 64;    // 0 .. kEpiThreads-1
     const int col0 = ((warp - 2) >> 2) * kColsPerThread;  // this thread's column range
+    // The residual tile and folded-LN statistics are fetched by these
+    // threads ahead of the accumulator: order them after the previous launch
+    // like the producer's operand loads.
+    if (kResTma || (kFold && (p.nin_stats || p.nres_stats))) grid_dependency_wait();
     const uint32_t stage_base = smem_u32(sOut);
     uint32_t res_phase = 0;
     int local = 0;
@@ -592,9 +619,68 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         mbar_arrive(&tempty[acc]);
       }
     };
+    const bool fold_in = kFold && p.nin_stats != nullptr;
+    const bool fold_res = kFold && kResTma && p.nres_stats != nullptr;
     for (int u = ubase; u < p.units; u += ustride, ++local) {
       const UnitCoord c = decode_unit(p, u, SWAP);
       const int acc = local & 1;
+      // Epilogue operands that do not depend on the accumulator are fetched
+      // while the main loop runs: the residual tile (the previous unit's
+      // store has finished reading the staging buffer: bulk_wait_read0 +
+      // barrier at the end of the unit) and the folded-LN statistics.
+      if constexpr (kResTma) {
+        if (etid == 0) {
+          const int m0r = c.ta * kRowsA + int(rank) * kGemmBM, n0r = c.tb * BN;
+          mbar_arrive_expect_tx(rbar, C::kOutBytes);
+          if (!SWAP) {
+#pragma unroll
+            for (int b = 0; b < BN / kOutBlock; ++b)
+              tma_load_3d(sOut + b * kGemmBM * 128, &map_r, rbar, n0r + b * kOutBlock, m0r, c.g,
+                          kEvictFirst);
+          } else {
+#pragma unroll
+            for (int b = 0; b < kGemmBM / kOutBlock; ++b)
+              tma_load_3d(sOut + b * BN * 128, &map_r, rbar, m0r + b * kOutBlock, n0r, c.g,
+                          kEvictFirst);
+          }
+        }
+      }
+      if constexpr (kFold) {
+        if (fold_in || fold_res) {
+          // (mean, rstd) of this tile's BN tokens, once per unit
+          const int n0s = c.tb * BN;
+          for (int t = etid; t < BN; t += kEpiThreads) {
+            const int tok = n0s + t < p.rows_b ? n0s + t : p.rows_b - 1;
+            if (fold_in) {
+              const float2 m = fold_stats(p.nin_stats, p.nin_parts, p.rows_b, c.g, tok,
+                                          p.nin_inv_d, p.nin_eps);
+              sNorm[t] = m.x;
+              sNorm[BN + t] = m.y;
+            }
+            if (fold_res) {
+              const float2 m = fold_stats(p.nres_stats, p.nres_parts, p.rows_b, c.g, tok,
+                                          p.nres_inv_d, p.nres_eps);
+              sNorm[2 * BN + t] = m.x;
+              sNorm[3 * BN + t] = m.y;
+            }
+          }
+          named_bar_sync(1, kEpiThreads);
+        }
+      }
+      // swapped tiles: this thread's feature row constants, loaded ahead too
+      float hb = 0.f, hcs = 0.f, hgm = 0.f, hbt = 0.f;
+      if constexpr (SWAP) {
+        const int feat = c.ta * kRowsA + int(rank) * kGemmBM + row;
+        if (feat < p.rows_a) {
+          const int64_t fi = int64_t(c.g) * p.features + feat;
+          if (p.bias) hb = __ldg(p.bias + fi);
+          if (fold_in) hcs = __ldg(p.nin_colsum + fi);
+          if (fold_res) {
+            hgm = __ldg(p.nres_gamma + fi);
+            hbt = __ldg(p.nres_beta + fi);
+          }
+        }
+      }
       {
         NF_WAIT_BEGIN();
         mbar_wait(&tfull[acc], (local >> 1) & 1);
@@ -626,6 +712,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         named_bar_sync(1, kEpiThreads);
         if (!*last_flag) {
           release_acc(acc);
+          if constexpr (kResTma) {
+            mbar_wait(rbar, res_phase);  // its residual tile landed unused
+            res_phase ^= 1u;
+          }
           continue;
         }
         __threadfence();
@@ -635,23 +725,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                         int64_t(c.g) * p.out_gstride
                   : nullptr;
       if constexpr (kResTma) {
-        // The previous unit's store has finished reading the staging buffer
-        // (bulk_wait_read0 + barrier below), so it can take this residual.
-        if (etid == 0) {
-          mbar_arrive_expect_tx(rbar, C::kOutBytes);
-          if (!SWAP) {
-#pragma unroll
-            for (int b = 0; b < BN / kOutBlock; ++b)
-              tma_load_3d(sOut + b * kGemmBM * 128, &map_r, rbar, n0 + b * kOutBlock, m0, c.g,
-                          kEvictFirst);
-          } else {
-#pragma unroll
-            for (int b = 0; b < kGemmBM / kOutBlock; ++b)
-              tma_load_3d(sOut + b * BN * 128, &map_r, rbar, m0 + b * kOutBlock, n0, c.g,
-                          kEvictFirst);
-          }
-        }
-        mbar_wait(rbar, res_phase);
+        mbar_wait(rbar, res_phase);  // issued before the accumulator wait
         res_phase ^= 1u;
       }
       const float* bias = p.bias ? p.bias + int64_t(c.g) * p.features : nullptr;
@@ -754,7 +828,20 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           // (features f, f^1) swap one value so each lane stores a packed
           // bf16 pair of adjacent features: 16 32-bit smem stores per chunk.
           const int feat = m0 + row;
-          const float b = (bias && feat < p.rows_a) ? __ldg(bias + feat) : 0.0f;
+          const float b = hb, cs = hcs, gm = hgm, bt = hbt;
+          if constexpr (kFold) {
+            if (fold_in) {
+#pragma unroll
+              for (int j = 0; j < EC; j += 4) {
+                const float4 mu = *reinterpret_cast<const float4*>(sNorm + cc + j);
+                const float4 rs = *reinterpret_cast<const float4*>(sNorm + BN + cc + j);
+                v[j] = rs.x * fmaf(-mu.x, cs, v[j]);
+                v[j + 1] = rs.y * fmaf(-mu.y, cs, v[j + 1]);
+                v[j + 2] = rs.z * fmaf(-mu.z, cs, v[j + 2]);
+                v[j + 3] = rs.w * fmaf(-mu.w, cs, v[j + 3]);
+              }
+            }
+          }
 #pragma unroll
           for (int j = 0; j < EC; ++j) {
             v[j] += b;
@@ -769,7 +856,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
               asm volatile("ld.shared.u16 %0, [%1];"
                            : "=h"(h)
                            : "r"(stage_base + stage_offset(cc + j, row, BN)));
-              v[j] += __uint_as_float(uint32_t(h) << 16);
+              float r = __uint_as_float(uint32_t(h) << 16);
+              if constexpr (kFold) {
+                if (fold_res)
+                  r = fmaf((r - sNorm[2 * BN + cc + j]) * sNorm[3 * BN + cc + j], gm, bt);
+              }
+              v[j] += r;
             }
             v[j] = act_t<ACT>(v[j]);
           }
@@ -817,8 +909,49 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           }
           bulk_commit();
           if (p.splits > 1) p.counters[wtile] = 0u;  // re-arm for the next launch
-          bulk_wait_read0();                          // staging reusable
         }
+        if constexpr (kFold) {
+          if (p.nout_stats) {
+            // Partial LN sums of token t over this tile's 128 features, from
+            // the bf16 values just staged (what the consumer will read). Lane
+            // pair (2t, 2t+1) takes token t's two 64-feature blocks; the
+            // swizzle spreads each 16-byte chunk read over all banks.
+            constexpr int kBlocks = kGemmBM / kOutBlock;  // 2
+            constexpr int kPerTok = kEpiThreads / BN;      // threads per token
+            static_assert(kPerTok == 1 || kPerTok == kBlocks, "stats split");
+            const int t = kPerTok == 1 ? etid : etid >> 1;
+            float s = 0.f, ss = 0.f;
+            if (t < BN) {
+#pragma unroll
+              for (int bb = 0; bb < kBlocks / kPerTok; ++bb) {
+                const int b = kPerTok == 1 ? bb : (etid & 1);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  uint32_t w4[4];
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
+                               : "r"(stage_base + uint32_t(b * BN * 128 + t * 128) +
+                                     (uint32_t(q ^ (t & 7)) << 4)));
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float lo = __uint_as_float(w4[e] << 16);
+                    const float hi = __uint_as_float(w4[e] & 0xffff0000u);
+                    s += lo + hi;
+                    ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                  }
+                }
+              }
+            }
+            if constexpr (kPerTok > 1) {
+              s += __shfl_xor_sync(0xffffffffu, s, 1);
+              ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+            }
+            if (t < BN && (kPerTok == 1 || (etid & 1) == 0) && n0 + t < p.rows_b)
+              __stcg(p.nout_stats + (int64_t(c.g) * p.tiles_a + c.ta) * p.rows_b + n0 + t,
+                     make_float2(s, ss));
+          }
+        }
+        if (etid == 0) bulk_wait_read0();  // staging reusable
         named_bar_sync(1, kEpiThreads);
       } else {
         if (p.splits > 1) {

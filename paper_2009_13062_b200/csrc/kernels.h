@@ -7,12 +7,29 @@
 
 namespace nf {
 
+// Folded LayerNorm operands of a batch-1 GEMM (see GemmParams::nin_*):
+// stats are [g][part][token] (sum, sum of squares) float pairs.
+struct NormFold {
+  const float* in_stats;
+  const float* in_colsum;
+  int in_parts;
+  float in_eps;
+  const float* res_stats;
+  const float* res_gamma;
+  const float* res_beta;
+  int res_parts;
+  float res_eps;
+  float* out_stats;
+};
+
 // gemm_sm100.cu — tcgen05 grouped GEMM (bf16 in, fp32 accumulate).
+bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N);
 int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const void* pf_next = nullptr, int64_t pf_bytes = 0);
+                      const void* pf_next = nullptr, int64_t pf_bytes = 0,
+                      const NormFold* fold = nullptr);
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
 int grouped_linear_ln_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                          const float* bias, const void* residual, const float* gamma,
@@ -72,7 +89,8 @@ int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int 
 // qkv_attention.cu — fused QKV projection + attention, batch 1, S = 128.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream, const void* pf_next = nullptr, int64_t pf_bytes = 0);
+                     cudaStream_t stream, const void* pf_next = nullptr, int64_t pf_bytes = 0,
+                     const NormFold* fold = nullptr);
 
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,

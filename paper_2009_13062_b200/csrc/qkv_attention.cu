@@ -26,7 +26,8 @@ constexpr int kQStages = 4;
 constexpr int kQABytes = kQTile;         // x tile (128 tokens x 64 K)
 constexpr int kQBBytes = 3 * kQD * 128;  // 192 weight rows x 64 K = 24 KB
 constexpr int kQStageBytes = kQABytes + kQBBytes;
-constexpr size_t kQSmem = 1024 + size_t(kQStages) * kQStageBytes + 3 * kQTile + 256;
+// + bias and folded-LN column sums of the head's 192 features (fp32)
+constexpr size_t kQSmem = 1024 + size_t(kQStages) * kQStageBytes + 3 * kQTile + 256 + 2 * 192 * 4;
 
 __device__ __forceinline__ uint32_t sw128_off(int r, int chunk16) {
   return uint32_t(r * 128 + ((chunk16 ^ (r & 7)) << 4));
@@ -36,7 +37,8 @@ __global__ void __launch_bounds__(192, 1)
     k_qkv_attention_tc(const __grid_constant__ CUtensorMap map_x,
                        const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
                        __nv_bfloat16* __restrict__ out, int H, int kb_total, float scale_log2,
-                       const void* pf_next, int64_t pf_bytes) {
+                       const void* pf_next, int64_t pf_bytes, const float2* nin_stats,
+                       const float* nin_colsum, int nin_parts, float nin_eps) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -51,6 +53,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bar_s = bar_acc + 1;
   uint64_t* bar_o = bar_s + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_o + 1);
+  float* sBias = reinterpret_cast<float*>(sV + kQTile + 256);  // [192]
+  float* sCs = sBias + 192;                                     // [192]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -131,6 +135,21 @@ __global__ void __launch_bounds__(192, 1)
     const int etid = threadIdx.x - 64;
     const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
     const float* bq = bias ? bias + int64_t(g) * 3 * D : nullptr;
+    // folded LayerNorm of x (GemmParams::nin_*): y = rstd * (x W'^T - mean * colsum) + b'
+    const float* csq = nin_stats ? nin_colsum + int64_t(g) * 3 * D : nullptr;
+    // The head's bias / column sums into smem while the projection runs (cold
+    // L2 misses off the epilogue's critical path).
+    for (int i = etid; i < 3 * kQD; i += 128) {
+      const int64_t f = int64_t(i / kQD) * D + h * kQD + (i % kQD);
+      sBias[i] = bq ? __ldg(bq + f) : 0.f;
+      sCs[i] = csq ? __ldg(csq + f) : 0.f;
+    }
+    float2 ms = make_float2(0.f, 1.f);
+    if (nin_stats) {
+      grid_dependency_wait();  // the stats come from the previous launch
+      ms = fold_stats(nin_stats, nin_parts, kQS, g, t, 1.0f / float(D), nin_eps);
+    }
+    named_bar_sync(1, 128);
     mbar_wait(bar_acc, 0);
     tc_fence_after();
     // features [0,64) q, [64,128) k, [128,192) v of head h -> K-major tiles
@@ -141,10 +160,15 @@ __global__ void __launch_bounds__(192, 1)
       tmem_ld_wait();
       const int part = c >> 1;                  // 0 q, 1 k, 2 v
       const int f0 = (c & 1) * 32;              // column within the head
-      const float* bp = bq ? bq + part * D + h * kQD + f0 : nullptr;
       float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (bp ? __ldg(bp + j) : 0.f);
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (csq) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = ms.y * fmaf(-ms.x, sCs[c * 32 + j], v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += sBias[c * 32 + j];
       uint8_t* tile = part == 0 ? sQ : (part == 1 ? sK : sV);
       const uint32_t base = smem_u32(tile);
 #pragma unroll
@@ -260,8 +284,11 @@ __global__ void __launch_bounds__(192, 1)
 // null; out (G, 128, D) bf16 context. heads * 64 == D.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream, const void* pf_next, int64_t pf_bytes) {
+                     cudaStream_t stream, const void* pf_next, int64_t pf_bytes,
+                     const NormFold* fold) {
   if (G < 1 || heads < 1 || D != heads * kQD) return NF_ERR_SHAPE;
+  const float2* nin = fold ? reinterpret_cast<const float2*>(fold->in_stats) : nullptr;
+  if (nin && (!fold->in_colsum || fold->in_parts < 1)) return NF_ERR_SHAPE;
   if (S != kQS || D % 64 || G * heads > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
   if (!make_bf16_map(&mx, x, G, S, D, 64, kQS, x_ld, x_gs) ||
@@ -276,7 +303,9 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
   const float sl2 = scale * 1.4426950408889634f;
   cudaError_t e = launch_pdl(k_qkv_attention_tc, dim3(unsigned(G * heads)), dim3(192), kQSmem,
                              stream, mx, mw, bias, static_cast<__nv_bfloat16*>(out), int(heads),
-                             int(D / 64), sl2, pf_next, pf_bytes);
+                             int(D / 64), sl2, pf_next, pf_bytes, nin,
+                             nin ? fold->in_colsum : nullptr, nin ? fold->in_parts : 0,
+                             nin ? fold->in_eps : 0.f);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 

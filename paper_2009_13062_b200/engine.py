@@ -58,6 +58,61 @@ _MODES = {"fast": _lib.NF_MODE_FAST, "exact": _lib.NF_MODE_EXACT}
 _SUPER_GROUP = int(__import__("os").environ.get("NF_SUPER_GROUP", "64"))
 _FUSE_LN = __import__("os").environ.get("NF_FUSE_LN", "0") == "1"
 _L2_PF = __import__("os").environ.get("NF_L2_PF", "0") == "1"  # measured slower (opt-in)
+# Batch-1 LayerNorms folded into their producing / consuming GEMMs (no norm
+# launch; see include/netfuse_b200.h "Folded LayerNorm"). NF_FOLD_LN=0 keeps
+# the separate norm kernel.
+_FOLD_LN = __import__("os").environ.get("NF_FOLD_LN", "1") != "0"
+
+
+class _LinearStep:
+    """One merged-Linear launch. A later norm lowering may attach a residual
+    and folded-LayerNorm operands to it (it is emitted before the norm that
+    absorbs its output is seen)."""
+
+    def __init__(self, x, k, w, b, y, n, groups, rows, dcode, layout, act, mcode, ws, wsb, pf,
+                 fold_ok):
+        self.x, self.k, self.w, self.b, self.y, self.n = x, k, w, b, y, n
+        self.groups, self.rows, self.dcode, self.layout = groups, rows, dcode, layout
+        self.act, self.mcode, self.ws, self.wsb, self.pf = act, mcode, ws, wsb, pf
+        self.fold_ok = fold_ok
+        self.residual = None
+        self.fin = None   # (stats, parts, colsum, eps)
+        self.fres = None  # (stats, parts, gamma, beta, eps)
+        self.out_stats = None
+
+    def __call__(self, st):
+        k, n, rows = self.k, self.n, self.rows
+        if self.fin is None and self.fres is None and self.out_stats is None:
+            _lib.call("nf_grouped_linear_ex", self.x, k, rows * k, self.w, self.b, self.residual,
+                      self.y, n, rows * n, self.groups, rows, k, n, self.dcode, self.layout,
+                      self.act, self.mcode, self.ws, self.wsb, *self.pf, st)
+            return
+        fin = self.fin or (None, 0, None, 0.0)
+        fres = self.fres or (None, 0, None, None, 0.0)
+        _lib.call("nf_grouped_linear_fold", self.x, k, rows * k, self.w, self.b, self.residual,
+                  self.y, n, rows * n, self.groups, rows, k, n, self.act, self.ws, self.wsb,
+                  *fin, *fres, self.out_stats, st)
+
+
+@dataclass
+class _FoldedNorm:
+    """A per-instance LayerNorm that is not launched: ``raw`` (G, T, D) holds
+    its input, ``stats`` the producer's per-token partial sums; ``out`` is
+    only written if some consumer cannot fold it (``emit``)."""
+
+    node_id: str
+    raw: torch.Tensor
+    out: torch.Tensor
+    stats: torch.Tensor
+    parts: int
+    gamma: torch.Tensor
+    beta: torch.Tensor
+    gamma_name: str
+    eps: float
+    m: int
+    rows: int
+    d: int
+    emit: Callable[[int], None]
 
 
 @dataclass
@@ -154,6 +209,8 @@ class Plan:
         self._ln_done: set[str] = set()  # norms computed by a Linear epilogue
         self._pf_sources: set[int] = set()  # launches that prefetch the next weights
         self._add_passthrough: dict[str, tuple[str, str]] = {}  # add -> (linear side, residual)
+        self._lin_out: dict[int, _LinearStep] = {}  # output data_ptr -> its launch
+        self._folded: dict[int, _FoldedNorm] = {}   # out data_ptr -> folded norm (not launched)
         self._cuda_graph: torch.cuda.CUDAGraph | None = None
         self.dispatch_count = 0
         self.op_invocations = 0
@@ -243,6 +300,7 @@ class Plan:
             for r in n.inputs:
                 users.setdefault(parse_ref(r)[0], []).append(n)
         outputs = {parse_ref(r)[0] for r in g.graph_outputs}
+        self._users, self._outputs = users, outputs
 
         # Graph inputs: Pack-only inputs alias their slice of the packed buffer.
         packs = [n for n in order if n.kind is OpKind.PACK]
@@ -310,6 +368,7 @@ class Plan:
                 continue
             if node.id in chains:
                 ch = chains[node.id]
+                self._flush_members(ch["nodes"])
                 try:
                     out = self._lower_conv_chain(ch, weights)
                 except (ShapeError, UnsupportedOpError) as exc:
@@ -326,6 +385,7 @@ class Plan:
                 continue
             members = groups.get(node.id)
             if members is not None:
+                self._flush_members(members)
                 try:
                     batched = self._lower_siblings(members, weights, users, outputs, fused_into)
                 except (ShapeError, UnsupportedOpError) as exc:
@@ -395,7 +455,15 @@ class Plan:
             self.op_invocations += 1
             if node.kind not in _BOUNDARY:
                 self.dispatch_count += 1
+        out_ts = [self.vals[parse_ref(r)[0]].t for r in g.graph_outputs]
         for key in list(self._deferred):
+            if key not in self._deferred:
+                continue
+            fo = self._folded.get(key)
+            if fo is not None and not any(self._aliases(fo.out, t) for t in out_ts):
+                del self._deferred[key]  # every consumer folded it: never launched
+                del self._folded[key]
+                continue
             self._emit_deferred(key)
         if self.fuse and self.device.type == "cuda" and self.prefetch:
             self._insert_l2_prefetch()
@@ -449,13 +517,44 @@ class Plan:
         return None, None
 
     def _emit_deferred(self, key: int) -> None:
-        nid, _, _, _, fn = self._deferred.pop(key)
+        nid, a, b, _, fn = self._deferred.pop(key)
+        self._folded.pop(key, None)
+        for t in (a, b):  # a deferred Add reading a folded norm's output
+            if t is not None:
+                self._flush_folded(t)
         self._emit(nid, fn)
+
+    def _flush_folded(self, t: torch.Tensor) -> None:
+        key, _ = self._deferred_for(t)
+        if key is not None and key in self._folded:
+            self._emit_deferred(key)
+
+    def _flush_members(self, members) -> None:
+        for mem in members:
+            for r in mem.inputs:
+                v = self.vals.get(parse_ref(r)[0])
+                if v is not None:
+                    self._flush_deferred(v.t)
+
+    def _folded_exact(self, x: torch.Tensor) -> _FoldedNorm | None:
+        """The folded norm whose whole output ``x`` is (same storage, dense)."""
+        fo = self._folded.get(x.data_ptr())
+        if fo is None or x.numel() != fo.out.numel() or not x.is_contiguous():
+            return None
+        return fo
+
+    def _fold_aware(self, node: OpNode) -> bool:
+        if node.kind in (OpKind.MATMUL, OpKind.BATCH_MATMUL):
+            return True
+        return node.kind is OpKind.ADD and node.id in self._add_into_norm and \
+            self.mcode == _lib.NF_MODE_FAST
 
     def _flush_deferred(self, t: torch.Tensor, keep_for: OpNode | None = None) -> None:
         key, entry = self._deferred_for(t)
         if key is None:
             return
+        if key in self._folded and keep_for is not None and self._fold_aware(keep_for):
+            return  # the consumer's lowering folds it or flushes it itself
         if keep_for is not None and self._add_into_norm.get(entry[0]) == keep_for.id:
             return
         if keep_for is not None and keep_for.kind in (OpKind.RESHAPE, OpKind.TRANSPOSE):
@@ -886,13 +985,27 @@ class Plan:
             raise ShapeError(f"operands incompatible: {tuple(x.shape)} vs {wsrc.spec.dims}")
         rows = x.numel() // (groups * k_in)
         fast_tc = self.mcode == _lib.NF_MODE_FAST and dt == torch.bfloat16
+        fold_ok = fast_tc and self.fuse and _FOLD_LN and bool(
+            _lib.load().nf_linear_fold_supported(groups, rows, k_in, n_out))
+        # an output that may take the residual must have no other reader
+        feeds_add = fold_ok and act_user is None and self._only_feeds_add(node.id)
+        fo = self._folded_exact(x)
+        if fo is not None and not (fold_ok and fo.m == groups and fo.rows == rows
+                                   and fo.d == k_in):
+            fo = None
+        if fo is None:
+            self._flush_deferred(x)  # x must be materialised before this launch
         layout = _lib.NF_W_NK if fast_tc else _lib.NF_W_KN
-        w = self._w(weights, wname, "linear_nk" if fast_tc else "linear_kn", dt)
-        bias = self._w(weights, node.weights[1], "vec_f32", dt) if len(node.weights) > 1 else None
+        bname = node.weights[1] if len(node.weights) > 1 else None
+        if fo is not None:
+            w, bias, colsum = self._folded_weights(weights, wname, bname, fo, dt)
+        else:
+            w = self._w(weights, wname, "linear_nk" if fast_tc else "linear_kn", dt)
+            bias = self._w(weights, bname, "vec_f32", dt) if bname else None
         y = self._alloc(node.output_spec.dims, dt)
         act = _ACT_OF[act_user.kind] if act_user is not None else _lib.NF_ACT_NONE
-        xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, \
-            y.data_ptr()
+        xp = fo.raw.data_ptr() if fo is not None else x.data_ptr()
+        wp, bp, yp = w.data_ptr(), bias.data_ptr() if bias is not None else None, y.data_ptr()
         dcode, mcode = K.dtype_code(x), self.mcode
         ws = self._workspace(groups, rows, k_in, n_out) if fast_tc else None
         idx = len(self.steps)
@@ -900,11 +1013,41 @@ class Plan:
         if fast_tc and rows <= 256:
             self._pf_sources.add(idx)  # weight-streaming (batch-1) launch
         wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
-        self._emit(node.id, lambda st: _lib.call(
-            "nf_grouped_linear_ex", xp, k_in, rows * k_in, wp, bp, None, yp, n_out,
-            rows * n_out, groups, rows, k_in, n_out, dcode, layout, act, mcode, wsp, wsb,
-            *self._pf_hint(idx), st))
+        step = _LinearStep(xp, k_in, wp, bp, yp, n_out, groups, rows, dcode, layout, act, mcode,
+                           wsp, wsb, self._pf_hint(idx), fold_ok)
+        if fo is not None:
+            step.fin = (fo.stats.data_ptr(), fo.parts, colsum.data_ptr(), fo.eps)
+        if feeds_add and y.is_contiguous():
+            self._lin_out[yp] = step
+        self._emit(node.id, step)
         return DVal(y, node.output_spec.dims)
+
+    def _only_feeds_add(self, nid: str) -> bool:
+        """``nid``'s value reaches exactly one consumer, an Add, through glue views."""
+        cur = nid
+        while True:
+            us = self._users.get(cur, [])
+            if len(us) != 1 or cur in self._outputs:
+                return False
+            if us[0].kind in (OpKind.RESHAPE, OpKind.TRANSPOSE):
+                cur = us[0].id
+                continue
+            return us[0].kind is OpKind.ADD
+
+    def _folded_weights(self, weights, wname, bname, fo: _FoldedNorm, dt):
+        """Weights / bias / column sums of a Linear consuming a folded norm:
+        W' = W * gamma (over K), b' = b + W beta, colsum = sum_k W'."""
+        key = ("fold", wname, bname, fo.gamma_name)
+        if key not in self._wcache:
+            w = self._w(weights, wname, "linear_nk", dt)  # (G, N, K)
+            g, n, k = w.shape
+            wf = w.float()
+            w2 = (wf * fo.gamma.reshape(g, 1, k)).to(dt).contiguous()
+            b = torch.einsum("gnk,gk->gn", wf, fo.beta.reshape(g, k))
+            if bname:
+                b = b + self._w(weights, bname, "vec_f32", dt).reshape(g, n)
+            self._wcache[key] = (w2, b.contiguous(), w2.float().sum(-1).contiguous())
+        return self._wcache[key]
 
     def _linear_ln_chain(self, node, ins, weights, users, outputs):
         """Batch-1 merged Linear -> Add(residual) -> [glue views] -> norm over
@@ -961,6 +1104,8 @@ class Plan:
 
     def _lower_linear_ln(self, node, add, norm, v, weights):
         x = self._materialize(node.id, v)
+        self._flush_deferred(x)
+        self._flush_deferred(self.vals[self._add_passthrough[add.id][1]].t)
         wname = node.weights[0]
         groups = weights[wname].spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
         k_in, n_out = weights[wname].spec.dims[-2], weights[wname].spec.dims[-1]
@@ -1029,19 +1174,33 @@ class Plan:
         groups = weights[wname].spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
         d = weights[wname].spec.dims[-2]
         heads = attn.attrs["heads"]
-        w = self._w(weights, wname, "linear_nk", x.dtype)
-        bias = self._w(weights, node.weights[1], "vec_f32", x.dtype) if len(node.weights) > 1 \
-            else None
+        fo = self._folded_exact(x)
+        if fo is not None and not (_FOLD_LN and fo.m == groups and fo.rows == 128 and fo.d == d):
+            fo = None
+        if fo is None:
+            self._flush_deferred(x)
+        bname = node.weights[1] if len(node.weights) > 1 else None
+        if fo is not None:
+            w, bias, colsum = self._folded_weights(weights, wname, bname, fo, x.dtype)
+        else:
+            w = self._w(weights, wname, "linear_nk", x.dtype)
+            bias = self._w(weights, bname, "vec_f32", x.dtype) if bname else None
         y = self._alloc(attn.output_spec.dims, x.dtype)
         scale = 1.0 / math.sqrt(d // heads)
-        xp, wp, bp, yp = x.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, \
-            y.data_ptr()
+        xp = fo.raw.data_ptr() if fo is not None else x.data_ptr()
+        wp, bp, yp = w.data_ptr(), bias.data_ptr() if bias is not None else None, y.data_ptr()
         idx = len(self.steps)
         self._linear_w[idx] = (wp, w.numel() * w.element_size())
         self._pf_sources.add(idx)
-        self._emit(attn.id, lambda st: _lib.call("nf_qkv_attention", xp, d, 128 * d, wp, bp, yp,
-                                                 groups, 128, d, heads, float(scale),
-                                                 *self._pf_hint(idx), st))
+        if fo is not None:
+            sp, parts, cp, eps = fo.stats.data_ptr(), fo.parts, colsum.data_ptr(), fo.eps
+            self._emit(attn.id, lambda st: _lib.call(
+                "nf_qkv_attention_fold", xp, d, 128 * d, wp, bp, yp, groups, 128, d, heads,
+                float(scale), sp, parts, cp, eps, st))
+        else:
+            self._emit(attn.id, lambda st: _lib.call(
+                "nf_qkv_attention", xp, d, 128 * d, wp, bp, yp, groups, 128, d, heads,
+                float(scale), *self._pf_hint(idx), st))
         return DVal(y, attn.output_spec.dims)
 
     def _pf_hint(self, idx: int) -> tuple:
@@ -1136,19 +1295,76 @@ class Plan:
             result = DVal(out, v.dims, split=v.split)
         xp, yp = base_t.data_ptr(), out.data_ptr()
         rp = None
+        gp, bp = gam.data_ptr(), bet.data_ptr()
+        dcode = K.dtype_code(base_t)
         key, entry = self._deferred_for(base_t)
         if key is not None and self._add_into_norm.get(entry[0]) == node.id:
+            if result.split is not None and self._fold_norm(node, entry, geom, out, gam, bet, eps):
+                del self._deferred[key]
+                return result
             off = xp - key
             a_t, b_t = entry[1], entry[2]
+            self._flush_folded(a_t)
+            self._flush_folded(b_t)
             xp, rp = a_t.data_ptr() + off, b_t.data_ptr() + off
             del self._deferred[key]
         elif key is not None:
             self._emit_deferred(key)
-        gp, bp = gam.data_ptr(), bet.data_ptr()
-        dcode = K.dtype_code(base_t)
         self._emit(node.id, lambda st: _lib.call("nf_group_norm", xp, rp, gp, bp, yp, *geom,
                                                  eps, dcode, st))
         return result
+
+    def _fold_norm(self, node, entry, geom, out, gam, bet, eps) -> bool:
+        """Add(Linear output, residual) -> per-instance LayerNorm at batch 1:
+        the Linear adds the residual in its epilogue and writes the norm's
+        per-token partial sums; the norm itself is not launched (its
+        consumers fold it, or it is emitted on first non-folding use)."""
+        if not (self.fuse and _FOLD_LN) or self.mcode != _lib.NF_MODE_FAST:
+            return False
+        m, rows, s_inst, s_row, g_per, cg = geom[:6]
+        if g_per != 1 or out.dtype != torch.bfloat16:
+            return False
+        _, a_t, b_t, _, _ = entry
+        lin, other = self._lin_out.get(a_t.data_ptr()), b_t
+        if lin is None or a_t.numel() != m * rows * cg:
+            lin, other = self._lin_out.get(b_t.data_ptr()), a_t
+        if lin is None or other.numel() != m * rows * cg or not _dense_block(other):
+            return False
+        if (lin.residual is not None or lin.out_stats is not None or not lin.fold_ok
+                or lin.groups != m or lin.rows != rows or lin.n != cg
+                or s_inst != rows * cg or s_row != cg):
+            return False
+        # same physical layout as the Linear's (G, T, N) output (the Add's
+        # operands are the same view of equal storage blocks)
+        fo_res = self._folded.get(other.data_ptr())
+        if fo_res is not None and (other.numel() != fo_res.out.numel()
+                                   or (fo_res.m, fo_res.rows, fo_res.d) != (m, rows, cg)):
+            fo_res = None
+        if fo_res is None:
+            self._flush_deferred(other)  # plain residual: must be in memory
+            lin.residual = other.data_ptr()
+        else:
+            lin.residual = fo_res.raw.data_ptr()
+            lin.fres = (fo_res.stats.data_ptr(), fo_res.parts, fo_res.gamma.data_ptr(),
+                        fo_res.beta.data_ptr(), fo_res.eps)
+        parts = -(-cg // 128)
+        stats = self._own(torch.zeros((m, parts, rows, 2), dtype=torch.float32,
+                                      device=self.device))
+        lin.out_stats = stats.data_ptr()
+        raw = self._lin_raw(lin, a_t if other is b_t else b_t)
+        xp, yp, gp, bp = raw.data_ptr(), out.data_ptr(), gam.data_ptr(), bet.data_ptr()
+        dcode = K.dtype_code(out)
+        fn = lambda st: _lib.call("nf_group_norm", xp, None, gp, bp, yp, *geom, eps, dcode, st)
+        fo = _FoldedNorm(node.id, raw, out, stats, parts, gam, bet, node.weights[0], eps, m,
+                         rows, cg, fn)
+        self._deferred[out.data_ptr()] = (node.id, None, None, out, fn)
+        self._folded[out.data_ptr()] = fo
+        return True
+
+    @staticmethod
+    def _lin_raw(lin: _LinearStep, view: torch.Tensor) -> torch.Tensor:
+        """The Linear's output buffer as a dense (G, T, N) view."""
+        return view.as_strided((lin.groups, lin.rows, lin.n), (lin.rows * lin.n, lin.n, 1))
 
     def _pointwise(self, node, ins):
         op = _EW_OF[node.kind]
@@ -1175,6 +1391,8 @@ class Plan:
                 srcs[1] is ins[1].t and self.mcode == _lib.NF_MODE_FAST:
             self._deferred[yp] = (node.id, srcs[0], srcs[1], out, fn)
         else:
+            for t in srcs:
+                self._flush_deferred(t)
             self._emit(node.id, fn)
         return result
 

@@ -10,7 +10,8 @@ from paper_2009_13062_b200 import workloads as W
 
 def _copies(plan):
     return sum(1 for nid, fn, _ in plan.steps
-               if fn.__code__.co_consts and "nf_copy_strided" in fn.__code__.co_consts)
+               if hasattr(fn, "__code__") and fn.__code__.co_consts
+               and "nf_copy_strided" in fn.__code__.co_consts)
 
 
 def test_bert_glue_is_zero_copy():
@@ -22,14 +23,47 @@ def test_bert_glue_is_zero_copy():
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
     # outputs are views of plan-owned buffers: no copy launch at all
     assert _copies(plan) == 0
-    # per layer at batch 1: qkv+attn (fused), proj, ln(+residual add),
-    # ff1(+gelu), ff2, ln(+add)
-    assert len(plan.steps) == 2 * 6
+    # per layer at batch 1: qkv+attn (fused), proj(+residual), ff1(+gelu),
+    # ff2(+residual); the LayerNorms are folded into those launches, only the
+    # last one (a graph output) runs as a norm kernel
+    assert len(plan.steps) == 2 * 4 + 1
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.attn" in ids and "merged::l00.qkv" not in ids
     assert not any("res" in nid for nid, _, _ in plan.steps)
     with pytest.raises(UnsupportedOpError):
         plan.launch()
+
+
+def _consts(fn):
+    return [c for c in getattr(fn, "__code__", None).co_consts if isinstance(c, str)] \
+        if hasattr(fn, "__code__") else []
+
+
+def test_layernorms_fold_into_neighbouring_linears():
+    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    st = dict((nid, fn) for nid, fn, _ in plan.steps)
+    # producers add the residual and write the norm statistics
+    for nid in ("merged::l00.proj", "merged::l00.ff2", "merged::l01.proj", "merged::l01.ff2"):
+        assert st[nid].residual is not None and st[nid].out_stats is not None
+    # the first layer's residual is the graph input; later ones are folded norms
+    assert st["merged::l00.proj"].fres is None and st["merged::l01.proj"].fres is not None
+    assert st["merged::l00.ff2"].fres is not None
+    # consumers rebuild LN(x) from the raw sum + statistics
+    assert st["merged::l00.ff1"].fin is not None and st["merged::l01.ff1"].fin is not None
+    assert "nf_qkv_attention_fold" in _consts(st["merged::l01.attn"])
+    assert "nf_qkv_attention" in _consts(st["merged::l00.attn"])
+    assert [nid for nid in st if ".ln" in nid] == ["merged::l01.ln2"]
+
+
+def test_layernorm_fold_opt_out(monkeypatch):
+    from paper_2009_13062_b200 import engine
+    monkeypatch.setattr(engine, "_FOLD_LN", False)
+    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    assert len(plan.steps) == 2 * 6
 
 
 def test_qkv_attention_fusion_needs_batch_one():
