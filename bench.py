@@ -235,7 +235,7 @@ def run_ours(args) -> dict | None:
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
 
-    from paper_2009_13062_b200 import compile_plan
+    from paper_2009_13062_b200 import PipelinedRunner, compile_plan
 
     from paper_2009_13062_b200.sharding import shard_range
     shard = shard_range(args.instances * world, world, rank)  # weak scaling: N per GPU
@@ -282,14 +282,14 @@ def run_ours(args) -> dict | None:
     outs_host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in plan.outputs()]
     d2h = sum(t.numel() * t.element_size() for t in outs_host)
 
+    # serving loop of the public API: each step's H2D copy (pinned host ->
+    # device staging) overlaps the previous step's forward
+    runner = PipelinedRunner(plan)
+
     def e2e_steps(n: int) -> float:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        for _ in range(n):
-            plan.load_inputs(pinned, non_blocking=True)
-            graph_exec.replay()
-            for h, o in zip(outs_host, plan.outputs()):
-                h.copy_(o, non_blocking=True)
+        runner.run([pinned] * n, outs_host)
         e.record(stream)
         torch.cuda.synchronize()
         return s.elapsed_time(e)

@@ -136,6 +136,10 @@ struct GemmParams {
 };
 
 
+#ifndef NF_RES_EARLY
+#define NF_RES_EARLY 1
+#endif
+
 #ifndef NF_GEMM_LITE_KB
 #define NF_GEMM_LITE_KB 100  // swapped (weight-streaming) tiles: 2 CTAs per SM
 #endif
@@ -268,6 +272,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   // Residual tiles arrive by TMA into the output staging buffer (same
   // swizzled layout as the result), so the epilogue adds them from smem.
   constexpr bool kResTma = HAS_RES && C::kStaged;
+  // residual tile requested at the top of the unit (ahead of the accumulator)
+  // or once the accumulator is ready (NF_RES_EARLY=0: swapped tiles only)
+  constexpr bool kResEarly = SWAP || NF_RES_EARLY;
   constexpr int EC = BN < 32 ? BN : 32;  // epilogue column chunk
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -628,7 +635,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       // while the main loop runs: the residual tile (the previous unit's
       // store has finished reading the staging buffer: bulk_wait_read0 +
       // barrier at the end of the unit) and the folded-LN statistics.
-      if constexpr (kResTma) {
+      auto issue_residual = [&]() {
         if (etid == 0) {
           const int m0r = c.ta * kRowsA + int(rank) * kGemmBM, n0r = c.tb * BN;
           mbar_arrive_expect_tx(rbar, C::kOutBytes);
@@ -644,7 +651,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                           kEvictFirst);
           }
         }
-      }
+      };
+      if constexpr (kResTma && kResEarly) issue_residual();
       if constexpr (kFold) {
         if (fold_in || fold_res) {
           // (mean, rstd) of this tile's BN tokens, once per unit
@@ -686,6 +694,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         mbar_wait(&tfull[acc], (local >> 1) & 1);
         if (etid == 0) NF_WAIT_END(3);
       }
+      if constexpr (kResTma && !kResEarly) issue_residual();
       tc_fence_after();
       if (etid == 0 && local == 0) NF_TRACE(4);
       const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);

@@ -1565,6 +1565,80 @@ class Plan:
         return self.out_buffers
 
 
+class PipelinedRunner:
+    """Serve a stream of host batches through one plan with the host->device
+    copy of batch i+1 (pinned host -> device staging, on a copy stream)
+    overlapping the forward of batch i. Each forward starts with one
+    device-side copy per plan input buffer from the staging mirror (so the
+    captured CUDA graph keeps its pointers), and ends with the device->host
+    read of its outputs; the next batch's staging copy waits only for the
+    device copy that consumed the buffer two batches earlier."""
+
+    def __init__(self, plan: Plan):
+        if plan.device.type != "cuda":
+            raise UnsupportedOpError("PipelinedRunner needs a CUDA plan")
+        self.plan = plan
+        bases: dict[int, torch.Tensor] = {}
+        for v in plan.input_views.values():
+            b = v._base if v._base is not None else v
+            bases.setdefault(b.data_ptr(), b)
+        self._bases = list(bases.values())
+        self._mirrors = [[torch.empty_like(b) for b in self._bases] for _ in range(2)]
+        self._views = []
+        for mir in self._mirrors:
+            views = {}
+            for name, v in plan.input_views.items():
+                b = v._base if v._base is not None else v
+                j = next(i for i, bb in enumerate(self._bases) if bb.data_ptr() == b.data_ptr())
+                views[name] = mir[j].as_strided(v.shape, v.stride(),
+                                                v.storage_offset() - b.storage_offset())
+            self._views.append(views)
+        self.copy_stream = torch.cuda.Stream(device=plan.device)
+        self._h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+        self._staged_free = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def _stage(self, i: int, inputs: dict) -> None:
+        k = i % 2
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(self._staged_free[k])
+            for name in self.plan.graph.graph_inputs:
+                if name not in inputs:
+                    raise ExecutionError(name, KeyError(f"graph input {name!r} not provided"))
+                val = inputs[name]
+                data = val.data if isinstance(val, TensorValue) else val
+                dst = self._views[k][name]
+                if tuple(data.shape) != tuple(dst.shape) or data.dtype != dst.dtype:
+                    raise ExecutionError(name, ShapeError(
+                        f"input {name!r}: got {tuple(data.shape)} ({data.dtype}), graph wants "
+                        f"{tuple(dst.shape)} ({dst.dtype})"))
+                dst.copy_(data, non_blocking=True)
+            self._h2d_done[k].record(self.copy_stream)
+
+    def run(self, batches, outputs_host) -> None:
+        """``batches``: sequence of input dicts (pinned host tensors for
+        overlap); ``outputs_host``: one list of host tensors per batch (or a
+        single list reused by every batch) receiving the plan outputs."""
+        main = torch.cuda.current_stream()
+        n = len(batches)
+        if n == 0:
+            return
+        per_batch = len(outputs_host) == n and isinstance(outputs_host[0], (list, tuple))
+        self.copy_stream.wait_stream(main)  # staging starts after work already queued
+        self._stage(0, batches[0])
+        for i in range(n):
+            if i + 1 < n:
+                self._stage(i + 1, batches[i + 1])
+            k = i % 2
+            main.wait_event(self._h2d_done[k])
+            for dst, src in zip(self._bases, self._mirrors[k]):
+                dst.copy_(src, non_blocking=True)
+            self._staged_free[k].record(main)
+            self.plan.replay()
+            outs = outputs_host[i] if per_batch else outputs_host
+            for h, o in zip(outs, self.plan.outputs()):
+                h.copy_(o, non_blocking=True)
+
+
 # ----------------------------------------------------------------------------
 # Reference-compatible entry point
 # ----------------------------------------------------------------------------
