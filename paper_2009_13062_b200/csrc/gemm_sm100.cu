@@ -64,6 +64,16 @@ static bool pair_enabled() {
   return on;
 }
 
+// Experiment knob: cap on persistent CTAs for swapped launches with more
+// units than SMs (NF_SWAP_GRID_CAP, read once; 0 = one CTA per SM).
+static int swap_grid_cap() {
+  static const int v = [] {
+    const char* e = getenv("NF_SWAP_GRID_CAP");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 struct LinearPlan {
   bool swap, pair;
   int bn;
@@ -189,7 +199,16 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
     const int grid = 2 * clusters;
     return launch_tc_act<256, false, true>(act, ma, mb, my, mr, p, grid, stream);
   }
-  const int grid = p.units < kNumSMs ? p.units : kNumSMs;
+  int grid = p.units < kNumSMs ? p.units : kNumSMs;
+  if (swap && p.units > kNumSMs) {
+    // Balanced persistent grid: as many waves as one CTA per SM needs, but
+    // every CTA gets the same unit count (192 units: 96 CTAs x 2 instead of
+    // 44 x 2 + 104 x 1) and fewer CTAs start late behind the previous
+    // launch's SMs (BERT-base N=8 B=1: 0.641 -> 0.636 ms).
+    const int waves = (p.units + kNumSMs - 1) / kNumSMs;
+    grid = (p.units + waves - 1) / waves;
+    if (swap_grid_cap() > 0 && grid > swap_grid_cap()) grid = swap_grid_cap();
+  }
 #define NF_TC(BNV, SW) return launch_tc_act<BNV, SW>(act, ma, mb, my, mr, p, grid, stream)
   if (swap) {
     if (bn == 64) NF_TC(64, true);

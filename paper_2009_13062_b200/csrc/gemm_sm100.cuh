@@ -193,7 +193,11 @@ struct GemmCfg {
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
   // folded-LN per-token (mean, rstd) of the B operand and of the residual
-  static constexpr int kNormBytes = (SWAP && kStaged && !PAIR && !GATHER) ? 4 * BN * 4 : 0;
+#ifndef NF_FOLD_SMEM
+#define NF_FOLD_SMEM 1
+#endif
+  static constexpr int kNormBytes =
+      (NF_FOLD_SMEM && SWAP && kStaged && !PAIR && !GATHER) ? 4 * BN * 4 : 0;
   static constexpr size_t kBytes =
       1024 + size_t(kStages) * kStageBytes + kOutBytes + 512 + kNormBytes;
   static_assert(kStages >= 3, "pipeline too shallow");
