@@ -186,7 +186,8 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   p.units = int(tiles * p.splits);
   p.counters = static_cast<unsigned*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
-  const int grid = p.units < kNumSMs ? p.units : kNumSMs;
+  const int grid = balanced_all() ? balanced_grid(p.units, kNumSMs)
+                                 : (p.units < kNumSMs ? p.units : kNumSMs);
   const bool r = relu != 0;
   // The weights map is the only TMA operand; it sits in the slot its
   // orientation reads (A when swapped, B otherwise).

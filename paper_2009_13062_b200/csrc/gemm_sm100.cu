@@ -195,11 +195,13 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.counters = static_cast<unsigned*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
   if (L.pair) {
-    const int clusters = p.units < kNumSMs / 2 ? p.units : kNumSMs / 2;
+    const int clusters = balanced_all() ? balanced_grid(p.units, kNumSMs / 2)
+                                        : (p.units < kNumSMs / 2 ? p.units : kNumSMs / 2);
     const int grid = 2 * clusters;
     return launch_tc_act<256, false, true>(act, ma, mb, my, mr, p, grid, stream);
   }
   int grid = p.units < kNumSMs ? p.units : kNumSMs;
+  if (!swap && balanced_all()) grid = balanced_grid(p.units, kNumSMs);
   if (swap && p.units > kNumSMs) {
     // Balanced persistent grid: as many waves as one CTA per SM needs, but
     // every CTA gets the same unit count (192 units: 96 CTAs x 2 instead of

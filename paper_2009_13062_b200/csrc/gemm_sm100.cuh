@@ -136,6 +136,23 @@ struct GemmParams {
 };
 
 
+// Persistent grid with equal units per CTA: the waves one CTA per slot
+// needs, spread evenly (e.g. 192 units on 148 SMs: 96 CTAs x 2).
+inline int balanced_grid(int64_t units, int slots) {
+  if (units <= slots) return int(units);
+  const int64_t waves = (units + slots - 1) / slots;
+  return int((units + waves - 1) / waves);
+}
+// NF_BALANCED_ALL=1: also for token-tile (tensor-bound) GEMMs and convs
+// (experiment knob, read once).
+inline bool balanced_all() {
+  static const bool on = [] {
+    const char* e = getenv("NF_BALANCED_ALL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 #ifndef NF_RES_EARLY
 #define NF_RES_EARLY 1
 #endif
