@@ -81,10 +81,32 @@ struct LinearPlan {
   int splits;
 };
 
+// Batch-1 launches with more 128-feature tiles than SMs: token rows on M and
+// 256-feature tiles on N (each CTA then streams 2 weight tiles per
+// activation tile instead of 1) — knob NF_SMALLT_NORMAL (read once).
+static bool smallt_normal() {
+  static const bool on = [] {
+    const char* e = getenv("NF_SMALLT_NORMAL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_t ws_bytes) {
   LinearPlan L;
   L.swap = T <= 256;
   L.bn = pick_bn(T, N);
+  if (L.swap && smallt_normal() && T <= 128 && N >= 256 && N % 256 == 0 &&
+      G * ((N + kGemmBM - 1) / kGemmBM) > kNumSMs) {
+    L.swap = false;
+    L.bn = 256;
+    L.pair = false;
+    L.tiles_a = (T + kGemmBM - 1) / kGemmBM;
+    L.tiles_b = N / 256;
+    L.tiles = G * L.tiles_a * L.tiles_b;
+    L.splits = 1;
+    return L;
+  }
   // Measured (tools/gemm_trace.cu): pairs cut the MMA's operand stalls on
   // 128x256 tensor-bound tiles (4-5 stages of 32 KB per CTA instead of 3 of
   // 48 KB); on batch-1 weight-streaming tiles they only add cluster-launch
