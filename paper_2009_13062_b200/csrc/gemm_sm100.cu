@@ -128,7 +128,9 @@ static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_
 bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
   if (G < 1 || K % 8 || N % 8 || G > 65535) return false;
   const LinearPlan L = plan_linear(G, T, K, N, 0);
-  return L.swap && !L.pair && L.bn == 128 && GemmOut<128, true>::kStaged;
+  if (L.swap) return !L.pair && L.bn == 128 && GemmOut<128, true>::kStaged;
+  // token-row tiles: 256-feature tiles, whole 128-feature statistic parts
+  return L.bn == 256 && N % 128 == 0 && GemmOut<256, false>::kStaged;
 }
 
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {

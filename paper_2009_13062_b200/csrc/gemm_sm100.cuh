@@ -314,6 +314,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
   float* sNorm = reinterpret_cast<float*>(sOut + C::kOutBytes + 512);  // C::kNormBytes
   constexpr bool kFold = C::kNormBytes > 0 && !LNF;
+  // token-row tiles (large T): each epilogue thread owns one token and 128
+  // feature columns, so the folded-LN terms live in registers
+  constexpr bool kFoldN = !SWAP && C::kStaged && BN == 256 && !GATHER && !LNF;
+  static_assert(!kFoldN || kColsPerThread == 128, "one 128-feature part per thread");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -647,8 +651,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         mbar_arrive(&tempty[acc]);
       }
     };
-    const bool fold_in = kFold && p.nin_stats != nullptr;
-    const bool fold_res = kFold && kResTma && p.nres_stats != nullptr;
+    const bool fold_in = (kFold || kFoldN) && p.nin_stats != nullptr;
+    const bool fold_res = (kFold || kFoldN) && kResTma && p.nres_stats != nullptr;
+    const bool fold_out = kFoldN && p.nout_stats != nullptr;
     for (int u = ubase; u < p.units; u += ustride, ++local) {
       const UnitCoord c = decode_unit(p, u, SWAP);
       const int acc = local & 1;
@@ -696,6 +701,20 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           named_bar_sync(1, kEpiThreads);
         }
       }
+      // token-row tiles: this thread's token's LN statistics, loaded ahead
+      float2 nin = make_float2(0.f, 1.f), nres = make_float2(0.f, 1.f);
+      if constexpr (kFoldN) {
+        const int tok = c.ta * kRowsA + int(rank) * kGemmBM + row;
+        if (tok < p.rows_a) {
+          if (fold_in)
+            nin = fold_stats(p.nin_stats, p.nin_parts, p.rows_a, c.g, tok, p.nin_inv_d,
+                             p.nin_eps);
+          if (fold_res)
+            nres = fold_stats(p.nres_stats, p.nres_parts, p.rows_a, c.g, tok, p.nres_inv_d,
+                              p.nres_eps);
+        }
+      }
+      float osum = 0.f, osq = 0.f;  // fold_out: this thread's part of its token's sums
       // swapped tiles: this thread's feature row constants, loaded ahead too
       float hb = 0.f, hcs = 0.f, hgm = 0.f, hbt = 0.f;
       if constexpr (SWAP) {
@@ -791,6 +810,21 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           // Thread = token row; EC consecutive features n0+cc ...
           const int tok = m0 + row;
           const int f0 = n0 + cc;
+          const int64_t gf = int64_t(c.g) * p.features + f0;
+          if constexpr (kFoldN) {
+            if (fold_in) {  // rstd * (acc - mean * colsum); folded parts have whole 128 blocks
+#pragma unroll
+              for (int j = 0; j < EC; j += 4) {
+                const float4 c4 = f0 + j < p.rows_b
+                                      ? __ldg(reinterpret_cast<const float4*>(p.nin_colsum + gf + j))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[j] = nin.y * fmaf(-nin.x, c4.x, v[j]);
+                v[j + 1] = nin.y * fmaf(-nin.x, c4.y, v[j + 1]);
+                v[j + 2] = nin.y * fmaf(-nin.x, c4.z, v[j + 2]);
+                v[j + 3] = nin.y * fmaf(-nin.x, c4.w, v[j + 3]);
+              }
+            }
+          }
           if (bias) {
             if (f0 + EC <= p.rows_b) {
 #pragma unroll
@@ -811,11 +845,26 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                            : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
                            : "r"(stage_base + stage_offset(row, cc + 8 * q, kGemmBM)));
+              float r8[8];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
-                v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xffff0000u);
+                r8[2 * e] = __uint_as_float(w4[e] << 16);
+                r8[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
               }
+              if constexpr (kFoldN) {
+                if (fold_res && f0 + 8 * q < p.rows_b) {  // LN(r) = (r - mean) * rstd * g + b
+                  const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.nres_gamma + gf + 8 * q));
+                  const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.nres_gamma + gf + 8 * q + 4));
+                  const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.nres_beta + gf + 8 * q));
+                  const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.nres_beta + gf + 8 * q + 4));
+                  const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                  const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) r8[e] = fmaf((r8[e] - nres.x) * nres.y, gg[e], bb[e]);
+                }
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[8 * q + e] += r8[e];
             }
           } else if (HAS_RES && tok < p.rows_a) {
             const __nv_bfloat16* rp = res + int64_t(tok) * p.out_ld + f0;
@@ -833,12 +882,25 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           for (int j = 0; j < EC; ++j) v[j] = act_t<ACT>(v[j]);
           if constexpr (C::kStaged) {
 #pragma unroll
-            for (int q = 0; q < EC / 8; ++q)
-              st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM),
-                           pack_bf16x2(v[8 * q], v[8 * q + 1]),
-                           pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                           pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
-                           pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+            for (int q = 0; q < EC / 8; ++q) {
+              const uint32_t w0 = pack_bf16x2(v[8 * q], v[8 * q + 1]);
+              const uint32_t w1 = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+              const uint32_t w2 = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+              const uint32_t w3 = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+              st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM), w0, w1, w2, w3);
+              if constexpr (kFoldN) {
+                if (fold_out) {  // LN sums of the stored (bf16) values
+                  const uint32_t ww[4] = {w0, w1, w2, w3};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float lo = __uint_as_float(ww[e] << 16);
+                    const float hi = __uint_as_float(ww[e] & 0xffff0000u);
+                    osum += lo + hi;
+                    osq = fmaf(lo, lo, fmaf(hi, hi, osq));
+                  }
+                }
+              }
+            }
           } else if (tok < p.rows_a) {
             // Narrow tiles (grouped convs with 4..32 channels per group):
             // each thread writes its row's features straight to HBM.
@@ -921,6 +983,13 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
             }
           }
         }
+      }
+      if constexpr (kFoldN) {
+        // this thread's 128 columns are one whole part of its token's sums
+        const int tok = m0 + row, f = n0 + col0;
+        if (fold_out && tok < p.rows_a && f < p.rows_b)
+          __stcg(p.nout_stats + (int64_t(c.g) * (p.features >> 7) + (f >> 7)) * p.rows_a + tok,
+                 make_float2(osum, osq));
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       release_acc(acc);

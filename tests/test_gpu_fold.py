@@ -43,7 +43,10 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-@pytest.mark.parametrize("G,T,K,N", [(3, 128, 256, 384), (2, 100, 768, 768), (1, 128, 3072, 768)])
+@pytest.mark.parametrize("G,T,K,N", [
+    (3, 128, 256, 384), (2, 100, 768, 768), (1, 128, 3072, 768),  # swapped 128-token tiles
+    (2, 1024, 768, 768), (1, 300, 512, 384), (4, 512, 3072, 768),  # token-row 256-feature tiles
+])
 def test_linear_fold_chain(G, T, K, N):
     lib = _lib.load()
     assert lib.nf_linear_fold_supported(G, T, K, N) == 1
@@ -131,14 +134,15 @@ def test_qkv_attention_fold():
     assert normwise(host(y), want) < 2e-2
 
 
-def test_fold_rejected_outside_swapped_tiles():
+def test_fold_rejected_where_not_implemented():
     lib = _lib.load()
-    assert lib.nf_linear_fold_supported(2, 1024, 768, 768) == 0  # token tiles on M
-    stats = torch.zeros(2, 6, 1024, 2, device="cuda")
+    assert lib.nf_linear_fold_supported(2, 1024, 768, 200) == 0  # 128-feature tiles (N < 256)
+    assert lib.nf_linear_fold_supported(2, 200, 768, 768) == 0   # swapped 256-token tiles
+    stats = torch.zeros(2, 2, 1024, 2, device="cuda")
     x = torch.zeros(2, 1024, 768, dtype=torch.bfloat16, device="cuda")
-    w = torch.zeros(2, 768, 768, dtype=torch.bfloat16, device="cuda")
-    y = torch.empty_like(x)
+    w = torch.zeros(2, 200, 768, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(2, 1024, 200, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(Exception):
         _lib.call("nf_grouped_linear_fold", x.data_ptr(), 768, 1024 * 768, w.data_ptr(), None,
-                  None, y.data_ptr(), 768, 1024 * 768, 2, 1024, 768, 768, 0, None, 0, None, 0,
+                  None, y.data_ptr(), 200, 1024 * 200, 2, 1024, 768, 200, 0, None, 0, None, 0,
                   None, 0.0, None, 0, None, None, 0.0, stats.data_ptr(), _stream())
