@@ -1600,6 +1600,38 @@ class PipelinedRunner:
         self.copy_stream = torch.cuda.Stream(device=plan.device)
         self._h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
         self._staged_free = [torch.cuda.Event(), torch.cuda.Event()]
+        # outputs that are views of one plan buffer (e.g. the stacked heads)
+        # come back with one device->host copy per buffer
+        obases: dict[int, torch.Tensor] = {}
+        for o in plan.outputs():
+            b = o._base if o._base is not None else o
+            obases.setdefault(b.data_ptr(), b)
+        self._out_bases = list(obases.values())
+        self._host_sets: dict[int, list[torch.Tensor]] = {}  # id(output list) -> pinned bases
+
+    def alloc_host_outputs(self, count: int = 1) -> list[list[torch.Tensor]]:
+        """``count`` sets of pinned host outputs laid out like the plan's
+        output buffers; ``run`` fills each set with one copy per buffer."""
+        sets = []
+        for _ in range(count):
+            # same physical layout as each buffer (views index it by stride)
+            mir = [torch.empty_strided(b.shape, b.stride(), dtype=b.dtype, pin_memory=True)
+                   for b in self._out_bases]
+            outs = []
+            for o in self.plan.outputs():
+                b = o._base if o._base is not None else o
+                j = next(i for i, bb in enumerate(self._out_bases)
+                         if bb.data_ptr() == b.data_ptr())
+                outs.append(mir[j].as_strided(o.shape, o.stride(),
+                                              o.storage_offset() - b.storage_offset()))
+            self._host_sets[id(outs)] = mir
+            sets.append(outs)
+        return sets
+
+    def d2h_bytes(self, outputs_host) -> int:
+        mir = self._host_sets.get(id(outputs_host))
+        ts = mir if mir is not None else outputs_host
+        return sum(t.numel() * t.element_size() for t in ts)
 
     def _stage(self, i: int, inputs: dict) -> None:
         k = i % 2
@@ -1639,8 +1671,13 @@ class PipelinedRunner:
             self._staged_free[k].record(main)
             self.plan.replay()
             outs = outputs_host[i] if per_batch else outputs_host
-            for h, o in zip(outs, self.plan.outputs()):
-                h.copy_(o, non_blocking=True)
+            mir = self._host_sets.get(id(outs))
+            if mir is not None:
+                for h, b in zip(mir, self._out_bases):
+                    h.copy_(b, non_blocking=True)
+            else:
+                for h, o in zip(outs, self.plan.outputs()):
+                    h.copy_(o, non_blocking=True)
 
 
 # ----------------------------------------------------------------------------

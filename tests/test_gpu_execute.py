@@ -152,6 +152,13 @@ def test_pipelined_runner_matches_per_batch_forwards():
             for g, r in zip(got, ref):
                 assert torch.equal(g, r)
     assert not torch.equal(want[0][0], want[1][0])
+    # pinned output sets laid out like the plan's buffers: one copy per buffer
+    sets = runner.alloc_host_outputs(len(batches))
+    runner.run(batches, sets)
+    torch.cuda.synchronize()
+    for got, ref in zip(sets, want):
+        for g, r in zip(got, ref):
+            assert torch.equal(g, r)
 
 
 def test_bert_2layer_large_batch_vs_oracle():
