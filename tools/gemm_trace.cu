@@ -1,6 +1,6 @@
 // Per-CTA pipeline timeline of the tcgen05 grouped GEMM (globaltimer ns,
 // relative to the end of a stamp kernel launched just before it, PDL off).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DNF_GEMM_TRACE \
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -DNF_GEMM_TRACE \
 //        -I include -I paper_2009_13062_b200/csrc tools/gemm_trace.cu -o build/gemm_trace -lcuda
 //   NF_PDL=0 build/gemm_trace G T K N
 #include "../paper_2009_13062_b200/csrc/gemm_sm100.cu"
