@@ -24,6 +24,39 @@ bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, 
   return r == CUDA_SUCCESS;
 }
 
+// 4-D view (64, rows, K/64, G) of a K-major bf16 operand with a
+// (64, box_rows, 2, 1) SWIZZLE_128B box: one TMA transaction delivers two
+// consecutive 64-wide k-blocks ([kb][row][128 B] in shared memory).
+static bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t rows,
+                               int64_t K, int box_rows, int64_t row_stride, int64_t g_stride) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || K % 64) return false;
+  if (row_stride <= 0) row_stride = K;
+  if (g_stride <= 0) g_stride = rows * row_stride;
+  if ((row_stride * 2) % 16 || (g_stride * 2) % 16 || (reinterpret_cast<uintptr_t>(base) & 15))
+    return false;
+  cuuint64_t dims[4] = {64, cuuint64_t(rows), cuuint64_t(K / 64), cuuint64_t(G)};
+  cuuint64_t strides[3] = {cuuint64_t(row_stride * 2), 128, cuuint64_t(g_stride * 2)};
+  cuuint32_t box[4] = {64, cuuint32_t(box_rows), 2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Two k-blocks per TMA transaction for swapped 128-token tiles: the batch-1
+// main loop is bound by a per-stage cost, not bytes (tools/gemm_trace.cu:
+// 768->768 main loop 3.7 -> 2.9 us, 3072->768 split 5.1 -> 3.9 us; BERT-8
+// 0.635 -> 0.625 ms). NF_GEMM_KPT=1 keeps one k-block per stage (read once).
+static bool kpt2_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NF_GEMM_KPT");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 static int pick_bn(int64_t T, int64_t N) {
   if (T <= 256) return T <= 64 ? 64 : (T <= 128 ? 128 : 256);
   return N >= 256 ? 256 : (N > 64 ? 128 : 64);
@@ -236,6 +269,13 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
     if (swap_grid_cap() > 0 && grid > swap_grid_cap()) grid = swap_grid_cap();
   }
 #define NF_TC(BNV, SW) return launch_tc_act<BNV, SW>(act, ma, mb, my, mr, p, grid, stream)
+  if (swap && bn == 128 && kpt2_enabled() && K % 64 == 0 &&
+      !(fold && fold->in_stats && fold->res_stats)) {
+    CUtensorMap ma2, mb2;
+    if (make_bf16_map_kpt2(&ma2, w, G, N, K, kGemmBM, 0, 0) &&
+        make_bf16_map_kpt2(&mb2, x, G, T, K, bn, x_ld, x_gs))
+      return launch_tc_kpt2(act, ma2, mb2, my, mr, p, grid, stream);
+  }
   if (swap) {
     if (bn == 64) NF_TC(64, true);
     if (bn == 128) NF_TC(128, true);

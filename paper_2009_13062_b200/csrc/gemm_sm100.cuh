@@ -186,11 +186,13 @@ struct GemmOut {
 #define NF_GEMM_HALO_KB 120  // operand ring of halo-gather convs (2 halo buffers follow)
 #endif
 
-template <int BN, bool SWAP, bool PAIR = false, int GATHER = 0>
+// KPT: k-blocks per TMA transaction / ring stage (2: one 4-D box per operand
+// covers two 64-wide k-blocks).
+template <int BN, bool SWAP, bool PAIR = false, int GATHER = 0, int KPT = 1>
 struct GemmCfg {
   static constexpr bool kStaged = GemmOut<BN, SWAP>::kStaged;
-  static constexpr int kABytes = kGemmBM * kGemmBK * 2;
-  static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * kGemmBK * 2;  // pair: half of B each
+  static constexpr int kABytes = kGemmBM * kGemmBK * 2 * KPT;
+  static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * kGemmBK * 2 * KPT;  // pair: half of B each
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kOutBytes = kStaged ? kGemmBM * BN * 2 : 0;
   // Swapped tiles stream weights at batch 1: a small footprint lets the next
@@ -205,6 +207,7 @@ struct GemmCfg {
   static constexpr int kBudgetKB =
       GATHER == 1 ? (NF_GEMM_HALO_KB > kMinKB ? NF_GEMM_HALO_KB : kMinKB)
       : GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
+      : KPT > 1 ? 225
       : BN >= 256 ? (PAIR ? 225 : 220)
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
@@ -214,7 +217,9 @@ struct GemmCfg {
 #define NF_FOLD_SMEM 1
 #endif
   static constexpr int kNormBytes =
-      (NF_FOLD_SMEM && SWAP && kStaged && !PAIR && !GATHER) ? 4 * BN * 4 : 0;
+      (NF_FOLD_SMEM && SWAP && kStaged && !PAIR && !GATHER) ? (KPT > 1 ? 2 : 4) * BN * 4 : 0;
+  // KPT > 1 leaves room for one (mean, rstd) pair: input OR residual fold
+  static constexpr int kResNormOff = KPT > 1 ? 0 : 2 * BN;
   static constexpr size_t kBytes =
       1024 + size_t(kStages) * kStageBytes + kOutBytes + 512 + kNormBytes;
   static_assert(kStages >= 3, "pipeline too shallow");
@@ -277,14 +282,16 @@ NF_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "me
 template <int N>
 NF_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER, bool PAIR, bool LNF = false>
+template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER, bool PAIR, bool LNF = false,
+          int KPT = 1>
 __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     k_grouped_gemm_tc(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
                       const __grid_constant__ CUtensorMap map_y,
                       const __grid_constant__ CUtensorMap map_r, GemmParams p) {
-  using C = GemmCfg<BN, SWAP, PAIR, GATHER>;
+  using C = GemmCfg<BN, SWAP, PAIR, GATHER, KPT>;
   constexpr int kStages = C::kStages;
+  static_assert(KPT == 1 || (SWAP && !PAIR && !GATHER && !LNF), "multi-k-block stages");
   static_assert(!(PAIR && GATHER), "CTA pairs take TMA operands only");
   constexpr int kRowsA = PAIR ? 2 * kGemmBM : kGemmBM;  // A rows per unit
   constexpr int kEpiWarps = epi_warps<BN>();
@@ -381,6 +388,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       auto a_row = [&](const UnitCoord& c) { return c.ta * kRowsA + int(rank) * kGemmBM; };
       auto b_row = [&](const UnitCoord& c) { return c.tb * BN + (PAIR ? int(rank) * (BN / 2) : 0); };
       auto load_w = [&](int stage, const UnitCoord& c, int kb) {
+        if constexpr (KPT > 1) {  // 4-D maps (64, rows, K/64, G): KPT k-blocks per box
+          tma_load_4d(sA + stage * C::kABytes, &map_a, &full[stage], 0, a_row(c), kb, c.g,
+                      hint_a);
+          return;
+        }
         if (SWAP)
           tload(sA + stage * C::kABytes, &map_a, stage, kb * kGemmBK, a_row(c), c.g, hint_a);
         else
@@ -388,6 +400,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       };
       auto load_x = [&](int stage, const UnitCoord& c, int kb) {
         if (GATHER) return;  // gathered by warps 6..9
+        if constexpr (KPT > 1) {
+          tma_load_4d(sB + stage * C::kBBytes, &map_b, &full[stage], 0, b_row(c), kb, c.g,
+                      hint_b);
+          return;
+        }
         if (SWAP)
           tload(sB + stage * C::kBBytes, &map_b, stage, kb * kGemmBK, b_row(c), c.g, hint_b);
         else
@@ -401,20 +418,20 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         // the previous kernel but the activations do: request the first
         // ring's worth of weight tiles before the dependency wait.
         const UnitCoord c = decode_unit(p, u, SWAP);
-        pre = min(kStages, c.kb1 - c.kb0);
+        pre = min(kStages, (c.kb1 - c.kb0 + KPT - 1) / KPT);
         for (int i = 0; i < pre; ++i) {
           arm(i);
-          load_w(i, c, c.kb0 + i);
+          load_w(i, c, c.kb0 + i * KPT);
         }
         if (!GATHER) grid_dependency_wait();
-        for (int i = 0; i < pre; ++i) load_x(i, c, c.kb0 + i);
+        for (int i = 0; i < pre; ++i) load_x(i, c, c.kb0 + i * KPT);
         it = pre;
       } else if (!GATHER) {
         grid_dependency_wait();
       }
       for (; u < p.units; u += ustride) {
         const UnitCoord c = decode_unit(p, u, SWAP);
-        for (int kb = c.kb0 + pre; kb < c.kb1; ++kb, ++it) {
+        for (int kb = c.kb0 + pre * KPT; kb < c.kb1; kb += KPT, ++it) {
           const int stage = it % kStages;
           {
             NF_WAIT_BEGIN();
@@ -443,7 +460,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-      for (int kb = c.kb0; kb < c.kb1; ++kb, ++it) {
+      for (int kb = c.kb0; kb < c.kb1; kb += KPT, ++it) {
         const int stage = it % kStages;
         {
           NF_WAIT_BEGIN();
@@ -453,18 +470,22 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         tc_fence_after();
         if (lane == 0 && it == 0) NF_TRACE(2);
         if (lane == 0) {
-          const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
-          const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
-          for (int kk = 0; kk < kGemmBK / 16; ++kk) {
-            if constexpr (PAIR)
-              umma_f16_ss_pair(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
-                               make_sw128_kmajor_desc(b_base + kk * 32), idesc,
-                               (kb != c.kb0 || kk != 0) ? 1u : 0u);
-            else
-              umma_f16_ss(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
-                          make_sw128_kmajor_desc(b_base + kk * 32), idesc,
-                          (kb != c.kb0 || kk != 0) ? 1u : 0u);
+          for (int h = 0; h < KPT; ++h) {
+            if (kb + h >= c.kb1) break;  // a split's range ends mid-stage
+            const uint32_t a_base = smem_u32(sA + stage * C::kABytes) + h * (C::kABytes / KPT);
+            const uint32_t b_base = smem_u32(sB + stage * C::kBBytes) + h * (C::kBBytes / KPT);
+#pragma unroll
+            for (int kk = 0; kk < kGemmBK / 16; ++kk) {
+              if constexpr (PAIR)
+                umma_f16_ss_pair(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
+                                 make_sw128_kmajor_desc(b_base + kk * 32), idesc,
+                                 (kb + h != c.kb0 || kk != 0) ? 1u : 0u);
+              else
+                umma_f16_ss(d_tmem, make_sw128_kmajor_desc(a_base + kk * 32),
+                            make_sw128_kmajor_desc(b_base + kk * 32), idesc,
+                            (kb + h != c.kb0 || kk != 0) ? 1u : 0u);
+            }
           }
           // frees the smem slot (both CTAs' halves) once these MMAs retire
           if constexpr (PAIR) umma_commit_pair(&empty[stage]);
@@ -694,8 +715,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
             if (fold_res) {
               const float2 m = fold_stats(p.nres_stats, p.nres_parts, p.rows_b, c.g, tok,
                                           p.nres_inv_d, p.nres_eps);
-              sNorm[2 * BN + t] = m.x;
-              sNorm[3 * BN + t] = m.y;
+              sNorm[C::kResNormOff + t] = m.x;
+              sNorm[C::kResNormOff + BN + t] = m.y;
             }
           }
           named_bar_sync(1, kEpiThreads);
@@ -951,7 +972,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
               float r = __uint_as_float(uint32_t(h) << 16);
               if constexpr (kFold) {
                 if (fold_res)
-                  r = fmaf((r - sNorm[2 * BN + cc + j]) * sNorm[3 * BN + cc + j], gm, bt);
+                  r = fmaf((r - sNorm[C::kResNormOff + cc + j]) * sNorm[C::kResNormOff + BN + cc + j],
+                           gm, bt);
               }
               v[j] += r;
             }
@@ -1271,11 +1293,11 @@ bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, 
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 
 template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0, bool PAIR = false,
-          bool LNF = false>
+          bool LNF = false, int KPT = 1>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
-  using C = GemmCfg<BN, SWAP, PAIR, GATHER>;
-  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR, LNF>;
+  using C = GemmCfg<BN, SWAP, PAIR, GATHER, KPT>;
+  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR, LNF, KPT>;
   static bool attr_done = false;  // idempotent attribute set; benign race
   if (!attr_done) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1315,6 +1337,26 @@ static int launch_tc_res(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   if (p.residual)
     return launch_tc<BN, SWAP, ACT, true, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
   return launch_tc<BN, SWAP, ACT, false, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
+}
+
+// Swapped 128-token tiles with two k-blocks per TMA box (4-D maps).
+template <int ACT>
+static int launch_tc_kpt2_res(const CUtensorMap& ma, const CUtensorMap& mb,
+                              const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
+                              int grid, cudaStream_t stream) {
+  if (p.residual)
+    return launch_tc<128, true, ACT, true, 0, false, false, 2>(ma, mb, my, mr, p, grid, stream);
+  return launch_tc<128, true, ACT, false, 0, false, false, 2>(ma, mb, my, mr, p, grid, stream);
+}
+inline int launch_tc_kpt2(int act, const CUtensorMap& ma, const CUtensorMap& mb,
+                          const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
+                          int grid, cudaStream_t stream) {
+  switch (act) {
+    case NF_ACT_RELU: return launch_tc_kpt2_res<NF_ACT_RELU>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_GELU: return launch_tc_kpt2_res<NF_ACT_GELU>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_TANH: return launch_tc_kpt2_res<NF_ACT_TANH>(ma, mb, my, mr, p, grid, stream);
+    default: return launch_tc_kpt2_res<NF_ACT_NONE>(ma, mb, my, mr, p, grid, stream);
+  }
 }
 
 template <int BN, bool SWAP, bool PAIR = false>
