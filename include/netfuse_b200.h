@@ -152,9 +152,11 @@ int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* 
  * Fused merged QKV projection + attention for batch-1 encoders (the merged
  * graph's BatchMatMul(qkv) -> Attention pair: reference `batch_matmul`,
  * engine.py:215-235, then the attention restatement). x (G, S=128, D) bf16
- * rows at x + g*x_gs + t*x_ld; w (G, 3D, D) K-major bf16 (q | k | v output
- * features); bias (G, 3D) fp32 or NULL; out (G, S, D) bf16 context of heads
- * of 64. One CTA per (instance, head); QKV never reaches HBM.
+ * rows at x + g*x_gs + t*x_ld; w (G, 3D, D) K-major bf16 with head-major
+ * rows: row h*192 + p*64 + j holds output feature p*D + h*64 + j (p = 0 q,
+ * 1 k, 2 v), so a head's 192 rows are one TMA box; bias (G, 3D) fp32 in
+ * feature order or NULL; out (G, S, D) bf16 context of heads of 64; D a
+ * multiple of 64. One CTA per (instance, head); QKV never reaches HBM.
  */
 int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,

@@ -27,8 +27,8 @@ bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, 
 // 4-D view (64, rows, K/64, G) of a K-major bf16 operand with a
 // (64, box_rows, 2, 1) SWIZZLE_128B box: one TMA transaction delivers two
 // consecutive 64-wide k-blocks ([kb][row][128 B] in shared memory).
-static bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t rows,
-                               int64_t K, int box_rows, int64_t row_stride, int64_t g_stride) {
+bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t K,
+                        int box_rows, int64_t row_stride, int64_t g_stride) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || K % 64) return false;
   if (row_stride <= 0) row_stride = K;

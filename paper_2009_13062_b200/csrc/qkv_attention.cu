@@ -16,15 +16,22 @@ namespace nf {
 
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
+bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t K,
+                        int box_rows, int64_t row_stride, int64_t g_stride);
 
 namespace {
 
 constexpr int kQS = 128;                 // tokens (= queries = keys)
 constexpr int kQD = 64;                  // head dim
 constexpr int kQTile = kQS * kQD * 2;    // 16 KB: one 128 x 64 bf16 tile
-constexpr int kQStages = 4;
-constexpr int kQABytes = kQTile;         // x tile (128 tokens x 64 K)
-constexpr int kQBBytes = 3 * kQD * 128;  // 192 weight rows x 64 K = 24 KB
+// Each ring stage holds two 64-wide k-blocks, delivered by one 4-D TMA box
+// per operand (the projection main loop is bound by a per-transaction cost):
+// x (128 tokens) and the head's 192 weight rows, stored head-major
+// (G, H, [q|k|v], 64, D) so that they are one contiguous box.
+constexpr int kQKPT = 2;
+constexpr int kQStages = 2;
+constexpr int kQABytes = kQTile * kQKPT;         // x: 2 x (128 tokens x 64 K)
+constexpr int kQBBytes = 3 * kQD * 128 * kQKPT;  // w: 2 x (192 rows x 64 K) = 48 KB
 constexpr int kQStageBytes = kQABytes + kQBBytes;
 // + bias and folded-LN column sums of the head's 192 features (fp32)
 constexpr size_t kQSmem = 1024 + size_t(kQStages) * kQStageBytes + 3 * kQTile + 256 + 2 * 192 * 4;
@@ -83,46 +90,51 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      auto load_w = [&](int stage, int kb) {
-        uint8_t* b = ring + stage * kQStageBytes + kQABytes;
-        for (int part = 0; part < 3; ++part)
-          tma_load_3d(b + part * kQD * 128, &map_w, &full[stage], kb * 64, part * D + h * kQD,
-                      g, kEvictFirst);
+      auto load_w = [&](int stage, int st) {
+        tma_load_4d(ring + stage * kQStageBytes + kQABytes, &map_w, &full[stage], 0,
+                    h * 3 * kQD, st * kQKPT, g, kEvictFirst);
       };
-      auto load_x = [&](int stage, int kb) {
-        tma_load_3d(ring + stage * kQStageBytes, &map_x, &full[stage], kb * 64, 0, g,
+      auto load_x = [&](int stage, int st) {
+        tma_load_4d(ring + stage * kQStageBytes, &map_x, &full[stage], 0, 0, st * kQKPT, g,
                     kEvictLast);
       };
+      const int n_st = (kb_total + kQKPT - 1) / kQKPT;
       // weights do not depend on the previous kernel: first ring before the wait
-      const int pre = kb_total < kQStages ? kb_total : kQStages;
+      const int pre = n_st < kQStages ? n_st : kQStages;
       for (int i = 0; i < pre; ++i) {
         mbar_arrive_expect_tx(&full[i], kQStageBytes);
         load_w(i, i);
       }
       grid_dependency_wait();
       for (int i = 0; i < pre; ++i) load_x(i, i);
-      for (int kb = pre; kb < kb_total; ++kb) {
-        const int stage = kb % kQStages;
-        mbar_wait(&empty[stage], ((kb / kQStages) & 1) ^ 1);
+      for (int st = pre; st < n_st; ++st) {
+        const int stage = st % kQStages;
+        mbar_wait(&empty[stage], ((st / kQStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[stage], kQStageBytes);
-        load_w(stage, kb);
-        load_x(stage, kb);
+        load_w(stage, st);
+        load_x(stage, st);
       }
       prefetch_share_l2(pf_next, pf_bytes);  // the next launch's weights into L2
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16_f32(128, 3 * kQD);
-    for (int kb = 0; kb < kb_total; ++kb) {
-      const int stage = kb % kQStages;
-      mbar_wait(&full[stage], (kb / kQStages) & 1);
+    const int n_st = (kb_total + kQKPT - 1) / kQKPT;
+    for (int st = 0; st < n_st; ++st) {
+      const int stage = st % kQStages;
+      mbar_wait(&full[stage], (st / kQStages) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t a = smem_u32(ring + stage * kQStageBytes);
-        const uint32_t b = a + kQABytes;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16_ss(tmem, make_sw128_kmajor_desc(a + kk * 32), make_sw128_kmajor_desc(b + kk * 32),
-                      idesc, (kb | kk) != 0);
+        for (int hk = 0; hk < kQKPT; ++hk) {
+          const int kb = st * kQKPT + hk;
+          if (kb >= kb_total) break;
+          const uint32_t a = smem_u32(ring + stage * kQStageBytes) + hk * kQTile;
+          const uint32_t b = smem_u32(ring + stage * kQStageBytes + kQABytes) + hk * (3 * kQD * 128);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16_ss(tmem, make_sw128_kmajor_desc(a + kk * 32),
+                        make_sw128_kmajor_desc(b + kk * 32), idesc, (kb | kk) != 0);
+        }
         umma_commit(&empty[stage]);
       }
       __syncwarp();
@@ -280,7 +292,8 @@ __global__ void __launch_bounds__(192, 1)
 }  // namespace
 
 // x (G, 128, D) bf16 rows (x_ld / x_gs element strides), w (G, 3D, D) K-major
-// bf16 (rows [0,D) q, [D,2D) k, [2D,3D) v features), bias (G, 3D) fp32 or
+// bf16 with head-major rows: row h*192 + part*64 + j = feature part*D + h*64 + j
+// (part 0 q, 1 k, 2 v), bias (G, 3D) fp32 in feature order or
 // null; out (G, 128, D) bf16 context. heads * 64 == D.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
@@ -291,8 +304,8 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
   if (nin && (!fold->in_colsum || fold->in_parts < 1)) return NF_ERR_SHAPE;
   if (S != kQS || D % 64 || G * heads > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
-  if (!make_bf16_map(&mx, x, G, S, D, 64, kQS, x_ld, x_gs) ||
-      !make_bf16_map(&mw, w, G, 3 * D, D, 64, kQD, 0, 0))
+  if (!make_bf16_map_kpt2(&mx, x, G, S, D, kQS, x_ld, x_gs) ||
+      !make_bf16_map_kpt2(&mw, w, G, 3 * D, D, 3 * kQD, 0, 0))
     return NF_ERR_UNSUPPORTED;
   static bool attr_done = false;
   if (!attr_done) {

@@ -1189,6 +1189,7 @@ class Plan:
         else:
             w = self._w(weights, wname, "linear_nk", x.dtype)
             bias = self._w(weights, bname, "vec_f32", x.dtype) if bname else None
+        w = self._head_major(w, heads, ("qkv_hm", wname, fo.gamma_name if fo else None))
         y = self._alloc(attn.output_spec.dims, x.dtype)
         scale = 1.0 / math.sqrt(d // heads)
         xp = fo.raw.data_ptr() if fo is not None else x.data_ptr()
@@ -1206,6 +1207,16 @@ class Plan:
                 "nf_qkv_attention", xp, d, 128 * d, wp, bp, yp, groups, 128, d, heads,
                 float(scale), *self._pf_hint(idx), st))
         return DVal(y, attn.output_spec.dims)
+
+    def _head_major(self, w: torch.Tensor, heads: int, key) -> torch.Tensor:
+        """(G, 3D, D) q|k|v rows -> head-major rows (G, H, 3, 64, D) for the
+        fused QKV+attention kernel (one TMA box per head)."""
+        if key not in self._wcache:
+            g, n3, k = w.shape
+            dh = n3 // (3 * heads)
+            self._wcache[key] = w.reshape(g, 3, heads, dh, k).permute(0, 2, 1, 3, 4) \
+                .reshape(g, n3, k).contiguous()
+        return self._wcache[key]
 
     def _pf_hint(self, idx: int) -> tuple:
         """(pointer, bytes) of the next weight-streaming launch's weights for

@@ -124,6 +124,7 @@ def test_qkv_attention_fold():
     want = np.stack([OK.attention(qkv[j], heads=heads) for j in range(g)])
     wf, bf, cs = _fold_w(w, gam, bet, b)
     stats = np.stack([x.sum(-1), (x * x).sum(-1)], -1)[:, None]  # one part: (g, 1, 128, 2)
+    wf = wf.reshape(g, 3, heads, 64, d).transpose(0, 2, 1, 3, 4).reshape(g, 3 * d, d)  # head-major
     xt, wt, bt, ct, stt = cuda(x, torch.bfloat16), cuda(wf, torch.bfloat16), cuda(bf), \
         cuda(cs), cuda(stats)
     y = torch.empty(g, 128, d, dtype=torch.bfloat16, device="cuda")

@@ -130,7 +130,9 @@ def test_fused_qkv_attention_vs_oracle(g, h):
     qkv = OK.bf16_round(np.einsum("gtk,gkn->gtn", x, w) + b[:, None, :])
     want = np.stack([OK.attention(qkv[j], heads=h) for j in range(g)])
     xt = cuda(x, torch.bfloat16)
-    wt = cuda(np.ascontiguousarray(np.swapaxes(w, 1, 2)), torch.bfloat16)
+    # head-major weight rows (ABI): row h*192 + part*64 + j = feature part*D + h*64 + j
+    wnk = np.swapaxes(w, 1, 2).reshape(g, 3, h, 64, d).transpose(0, 2, 1, 3, 4).reshape(g, 3 * d, d)
+    wt = cuda(np.ascontiguousarray(wnk), torch.bfloat16)
     bt = cuda(b)
     y = torch.empty(g, 128, d, dtype=torch.bfloat16, device="cuda")
     _lib.call("nf_qkv_attention", xt.data_ptr(), d, 128 * d, wt.data_ptr(), bt.data_ptr(),
