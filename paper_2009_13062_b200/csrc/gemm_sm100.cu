@@ -28,7 +28,7 @@ bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, 
 // (64, box_rows, 2, 1) SWIZZLE_128B box: one TMA transaction delivers two
 // consecutive 64-wide k-blocks ([kb][row][128 B] in shared memory).
 bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t K,
-                        int box_rows, int64_t row_stride, int64_t g_stride) {
+                        int box_rows, int64_t row_stride, int64_t g_stride, int kpt) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || K % 64) return false;
   if (row_stride <= 0) row_stride = K;
@@ -37,7 +37,7 @@ bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t r
     return false;
   cuuint64_t dims[4] = {64, cuuint64_t(rows), cuuint64_t(K / 64), cuuint64_t(G)};
   cuuint64_t strides[3] = {cuuint64_t(row_stride * 2), 128, cuuint64_t(g_stride * 2)};
-  cuuint32_t box[4] = {64, cuuint32_t(box_rows), 2, 1};
+  cuuint32_t box[4] = {64, cuuint32_t(box_rows), cuuint32_t(kpt), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -48,14 +48,17 @@ bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t r
 // Two k-blocks per TMA transaction for swapped 128-token tiles: the batch-1
 // main loop is bound by a per-stage cost, not bytes (tools/gemm_trace.cu:
 // 768->768 main loop 3.7 -> 2.9 us, 3072->768 split 5.1 -> 3.9 us; BERT-8
-// 0.635 -> 0.625 ms). NF_GEMM_KPT=1 keeps one k-block per stage (read once).
-static bool kpt2_enabled() {
-  static const bool on = [] {
+// 0.635 -> 0.625 ms). NF_GEMM_KPT=1 keeps one k-block per stage, =3 moves
+// three (two 96 KB stages: main loops a further 0-10% shorter but the step
+// 0.620 -> 0.639 ms, split ranges of 16 k-blocks waste a third of a stage).
+static int kpt_setting() {
+  static const int v = [] {
     const char* e = getenv("NF_GEMM_KPT");
-    return !(e && e[0] == '1');
+    return e ? atoi(e) : 2;
   }();
-  return on;
+  return v;
 }
+static bool kpt2_enabled() { return kpt_setting() >= 2; }
 
 static int pick_bn(int64_t T, int64_t N) {
   if (T <= 256) return T <= 64 ? 64 : (T <= 128 ? 128 : 256);
@@ -272,9 +275,11 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   if (swap && bn == 128 && kpt2_enabled() && K % 64 == 0 &&
       !(fold && fold->in_stats && fold->res_stats)) {
     CUtensorMap ma2, mb2;
-    if (make_bf16_map_kpt2(&ma2, w, G, N, K, kGemmBM, 0, 0) &&
-        make_bf16_map_kpt2(&mb2, x, G, T, K, bn, x_ld, x_gs))
-      return launch_tc_kpt2(act, ma2, mb2, my, mr, p, grid, stream);
+    const int kpt = kpt_setting() >= 3 ? 3 : 2;
+    if (make_bf16_map_kpt2(&ma2, w, G, N, K, kGemmBM, 0, 0, kpt) &&
+        make_bf16_map_kpt2(&mb2, x, G, T, K, bn, x_ld, x_gs, kpt))
+      return kpt == 3 ? launch_tc_kpt3(act, ma2, mb2, my, mr, p, grid, stream)
+                      : launch_tc_kpt2(act, ma2, mb2, my, mr, p, grid, stream);
   }
   if (swap) {
     if (bn == 64) NF_TC(64, true);

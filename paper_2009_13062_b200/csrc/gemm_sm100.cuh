@@ -207,6 +207,7 @@ struct GemmCfg {
   static constexpr int kBudgetKB =
       GATHER == 1 ? (NF_GEMM_HALO_KB > kMinKB ? NF_GEMM_HALO_KB : kMinKB)
       : GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
+      : KPT > 2 ? 226
       : KPT > 1 ? 225
       : BN >= 256 ? (PAIR ? 225 : 220)
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
@@ -222,7 +223,7 @@ struct GemmCfg {
   static constexpr int kResNormOff = KPT > 1 ? 0 : 2 * BN;
   static constexpr size_t kBytes =
       1024 + size_t(kStages) * kStageBytes + kOutBytes + 512 + kNormBytes;
-  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert(kStages >= (KPT > 2 ? 2 : 3), "pipeline too shallow");
   static_assert(kStages <= 32, "barrier array");
   static_assert(kTmemCols <= 512, "TMEM overflow");
 };
@@ -1339,24 +1340,35 @@ static int launch_tc_res(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
   return launch_tc<BN, SWAP, ACT, false, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
 }
 
-// Swapped 128-token tiles with two k-blocks per TMA box (4-D maps).
-template <int ACT>
-static int launch_tc_kpt2_res(const CUtensorMap& ma, const CUtensorMap& mb,
-                              const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
-                              int grid, cudaStream_t stream) {
+// Swapped 128-token tiles with KPT k-blocks per TMA box (4-D maps).
+template <int ACT, int KPT>
+static int launch_tc_kpt_res(const CUtensorMap& ma, const CUtensorMap& mb,
+                             const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
+                             int grid, cudaStream_t stream) {
   if (p.residual)
-    return launch_tc<128, true, ACT, true, 0, false, false, 2>(ma, mb, my, mr, p, grid, stream);
-  return launch_tc<128, true, ACT, false, 0, false, false, 2>(ma, mb, my, mr, p, grid, stream);
+    return launch_tc<128, true, ACT, true, 0, false, false, KPT>(ma, mb, my, mr, p, grid, stream);
+  return launch_tc<128, true, ACT, false, 0, false, false, KPT>(ma, mb, my, mr, p, grid, stream);
+}
+template <int KPT>
+inline int launch_tc_kpt(int act, const CUtensorMap& ma, const CUtensorMap& mb,
+                         const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
+                         int grid, cudaStream_t stream) {
+  switch (act) {
+    case NF_ACT_RELU: return launch_tc_kpt_res<NF_ACT_RELU, KPT>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_GELU: return launch_tc_kpt_res<NF_ACT_GELU, KPT>(ma, mb, my, mr, p, grid, stream);
+    case NF_ACT_TANH: return launch_tc_kpt_res<NF_ACT_TANH, KPT>(ma, mb, my, mr, p, grid, stream);
+    default: return launch_tc_kpt_res<NF_ACT_NONE, KPT>(ma, mb, my, mr, p, grid, stream);
+  }
 }
 inline int launch_tc_kpt2(int act, const CUtensorMap& ma, const CUtensorMap& mb,
                           const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
                           int grid, cudaStream_t stream) {
-  switch (act) {
-    case NF_ACT_RELU: return launch_tc_kpt2_res<NF_ACT_RELU>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_GELU: return launch_tc_kpt2_res<NF_ACT_GELU>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_TANH: return launch_tc_kpt2_res<NF_ACT_TANH>(ma, mb, my, mr, p, grid, stream);
-    default: return launch_tc_kpt2_res<NF_ACT_NONE>(ma, mb, my, mr, p, grid, stream);
-  }
+  return launch_tc_kpt<2>(act, ma, mb, my, mr, p, grid, stream);
+}
+inline int launch_tc_kpt3(int act, const CUtensorMap& ma, const CUtensorMap& mb,
+                          const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
+                          int grid, cudaStream_t stream) {
+  return launch_tc_kpt<3>(act, ma, mb, my, mr, p, grid, stream);
 }
 
 template <int BN, bool SWAP, bool PAIR = false>

@@ -17,7 +17,7 @@ namespace nf {
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t K,
-                        int box_rows, int64_t row_stride, int64_t g_stride);
+                        int box_rows, int64_t row_stride, int64_t g_stride, int kpt);
 
 namespace {
 
@@ -304,8 +304,8 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
   if (nin && (!fold->in_colsum || fold->in_parts < 1)) return NF_ERR_SHAPE;
   if (S != kQS || D % 64 || G * heads > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
-  if (!make_bf16_map_kpt2(&mx, x, G, S, D, kQS, x_ld, x_gs) ||
-      !make_bf16_map_kpt2(&mw, w, G, 3 * D, D, 3 * kQD, 0, 0))
+  if (!make_bf16_map_kpt2(&mx, x, G, S, D, kQS, x_ld, x_gs, kQKPT) ||
+      !make_bf16_map_kpt2(&mw, w, G, 3 * D, D, 3 * kQD, 0, 0, kQKPT))
     return NF_ERR_UNSUPPORTED;
   static bool attr_done = false;
   if (!attr_done) {
