@@ -1,8 +1,4 @@
 export PYTHONPATH=.
-NF_GEMM_KPT=3 timeout 600 python -m pytest tests/test_gpu_fold.py tests/test_gpu_linear_smoke.py tests/test_gpu_execute.py -q --timeout 300 -x 2>&1 | tail -2
-for shape in "8 128 768 768" "8 128 3072 768" "8 128 768 3072"; do
-for k in 2 3; do echo "## kpt=$k $shape warm"; NF_GEMM_KPT=$k NF_TRACE_WARM=1 NF_PDL=0 timeout 60 ./tools/bin/gemm_trace $shape | grep -E "first_stage|last_mma"; done
-done
-for i in 1 2; do for k in 2 3; do
-echo "kpt=$k $(NF_GEMM_KPT=$k timeout 120 python bench.py --no-unmerged --no-cpu 2>&1 | tail -1 | cut -c150-210)"
-done; done
+timeout 900 python -m pytest tests -m gpu -q --timeout 300 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 300 python bench.py 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['clocks'], d['cpu_baseline']['value'] if d.get('cpu_baseline') else None)"
