@@ -272,14 +272,20 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
     if (swap_grid_cap() > 0 && grid > swap_grid_cap()) grid = swap_grid_cap();
   }
 #define NF_TC(BNV, SW) return launch_tc_act<BNV, SW>(act, ma, mb, my, mr, p, grid, stream)
-  if (swap && bn == 128 && kpt2_enabled() && K % 64 == 0 &&
+  if (swap && bn == 128 && kpt2_enabled() && K % 64 == 0 && N % 128 == 0 &&
       !(fold && fold->in_stats && fold->res_stats)) {
-    CUtensorMap ma2, mb2;
+    CUtensorMap ma2, mb2, my2, mr2;
     const int kpt = kpt_setting() >= 3 ? 3 : 2;
+    // output / residual tiles (128 tokens x 128 features) as one 4-D box:
+    // (64, T, N/64, G) with a (64, 128, 2, 1) box, the staging buffer's layout
     if (make_bf16_map_kpt2(&ma2, w, G, N, K, kGemmBM, 0, 0, kpt) &&
-        make_bf16_map_kpt2(&mb2, x, G, T, K, bn, x_ld, x_gs, kpt))
-      return kpt == 3 ? launch_tc_kpt3(act, ma2, mb2, my, mr, p, grid, stream)
-                      : launch_tc_kpt2(act, ma2, mb2, my, mr, p, grid, stream);
+        make_bf16_map_kpt2(&mb2, x, G, T, K, bn, x_ld, x_gs, kpt) &&
+        make_bf16_map_kpt2(&my2, y, G, T, N, bn, y_ld, y_gs, 2) &&
+        (!residual || make_bf16_map_kpt2(&mr2, residual, G, T, N, bn, y_ld, y_gs, 2))) {
+      if (!residual) mr2 = my2;
+      return kpt == 3 ? launch_tc_kpt3(act, ma2, mb2, my2, mr2, p, grid, stream)
+                      : launch_tc_kpt2(act, ma2, mb2, my2, mr2, p, grid, stream);
+    }
   }
   if (swap) {
     if (bn == 64) NF_TC(64, true);

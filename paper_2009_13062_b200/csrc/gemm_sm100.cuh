@@ -692,6 +692,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
             for (int b = 0; b < BN / kOutBlock; ++b)
               tma_load_3d(sOut + b * kGemmBM * 128, &map_r, rbar, n0r + b * kOutBlock, m0r, c.g,
                           kEvictFirst);
+          } else if constexpr (KPT > 1) {
+            // 4-D map (64, T, N/64, G): the tile's two 64-feature blocks in one box
+            tma_load_4d(sOut, &map_r, rbar, 0, n0r, m0r / kOutBlock, c.g, kEvictFirst);
           } else {
 #pragma unroll
             for (int b = 0; b < kGemmBM / kOutBlock; ++b)
@@ -1024,6 +1027,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
 #pragma unroll
             for (int b = 0; b < BN / kOutBlock; ++b)
               tma_store_3d(&map_y, sOut + b * kGemmBM * 128, n0 + b * kOutBlock, m0, c.g);
+          } else if constexpr (KPT > 1) {
+            tma_store_4d(&map_y, sOut, 0, n0, m0 / kOutBlock, c.g);
           } else {
 #pragma unroll
             for (int b = 0; b < kGemmBM / kOutBlock; ++b)
