@@ -155,25 +155,9 @@ def dist_env():
 
 def build_workload(model: str, instances: int, batch: int, dtype: str, first_instance: int,
                    heads: bool = True):
-    from paper_2009_13062_b200 import merge, merge_backbone, model_inputs
+    """The merged workload (shared with tests/test_gpu_configs.py)."""
     from paper_2009_13062_b200 import workloads as W
-
-    graph = W.build_graph(model, batch=batch, dtype=dtype)
-    ids = list(range(first_instance, first_instance + instances))
-    stores = [W.build_weights(model, dtype=dtype, seed=0, model=m) for m in ids]
-    inputs = [model_inputs(graph, seed=0, model=m) for m in ids]
-    head_list = None
-    if heads:
-        out = graph.node_map()[graph.graph_outputs[0].rsplit(":", 1)[0]].output_spec
-        if len(out.dims) == 4:  # CNN: per-task FC 2048 -> 1000 on the pooled features
-            head_list = [W.fc_head(out, 1000, seed=100 + m) for m in ids]
-        else:
-            widths = W.head_widths(first_instance + instances)[first_instance:]
-            head_list = [W.classifier_head(out, w, seed=100 + m) for m, w in zip(ids, widths)]
-        merged, mstore = merge_backbone(graph, {n.id for n in graph.nodes}, stores, head_list)
-    else:
-        merged, mstore = merge(graph, stores)
-    return graph, stores, inputs, merged, mstore, head_list
+    return W.merged_workload(model, instances, batch, dtype, first_instance, heads)
 
 
 def linear_launch_bytes(merged, mstore, step_ids=None) -> dict[str, tuple[int, int]]:

@@ -136,19 +136,6 @@ int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups
                                 int stride, int pad, int kpad);
 
 /*
- * Merged Linear + residual + LayerNorm (batch-1 encoders): the merged graph's
- * BatchMatMul -> Add -> GroupNorm(groups = instances) chain (reference
- * batch_matmul engine.py:215-235, add 322-325, group_norm 263-284) as one
- * launch: y = LN(x W^T + bias + residual) over the n output features of each
- * of the rows (<= 128) tokens, gamma/beta (groups, n) fp32, n <= 1024.
- * x / residual / y rows at base + g*gs + t*ld (bf16), w (groups, n, k) bf16.
- */
-int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                         const float* bias, const void* residual, const float* gamma,
-                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
-                         int64_t groups, int64_t rows, int64_t k, int64_t n, void* stream);
-
-/*
  * Fused merged QKV projection + attention for batch-1 encoders (the merged
  * graph's BatchMatMul(qkv) -> Attention pair: reference `batch_matmul`,
  * engine.py:215-235, then the attention restatement). x (G, S=128, D) bf16
@@ -160,22 +147,24 @@ int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* 
  */
 int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
-                     float scale, const void* l2_prefetch, int64_t l2_prefetch_bytes,
-                     void* stream);
+                     float scale, void* stream);
 
 /*
  * Folded LayerNorm (batch-1 encoders). The merged graph's Add -> GroupNorm
  * over each instance's D features (reference add engine.py:322-325,
  * group_norm 263-284) is not launched: the Linear producing the Add's
- * operand adds the residual in its epilogue and writes per-token partial
- * sums `out_stats` [g][part][token] (sum, sum of squares; part = 128-feature
- * tile, ceil(n/128) parts). Consumers rebuild LN(v) from the raw v:
+ * operand adds the residual in its epilogue and writes per-token statistics
+ * `out_stats` [g][part][token] (sum, centred sum of squares M2 about the
+ * part's own mean; part = 128-feature tile, n/128 parts). Consumers merge the
+ * parts (Chan et al.: no E[x^2] - mean^2 cancellation, so the result does not
+ * degrade with |mean| / std) and rebuild LN(v) from the raw v:
  *  - as the activations of a Linear (in_*): w holds gamma-scaled weights
  *    W'[g][n][k] = W[g][n][k] * gamma[g][k], bias b' = b + W beta, in_colsum
  *    (G, n) = sum_k W'[g][n][k]; y = rstd * (x W'^T - mean * colsum) + b';
  *  - as the residual (res_*): (r - mean) * rstd * res_gamma + res_beta.
  * nf_linear_fold_supported(...) is 1 where the kernel implements it (the
- * swapped 128-token tile path); elsewhere the fold entry points return 2.
+ * swapped 128-token tile path, n a multiple of 128); elsewhere the fold
+ * entry points return 2.
  * Statistics are fp32 and the reduction order fixed (deterministic).
  */
 int nf_linear_fold_supported(int64_t groups, int64_t rows, int64_t k, int64_t n);
@@ -208,20 +197,6 @@ int64_t nf_linear_workspace_bytes(int64_t groups, int64_t rows, int64_t k, int64
  * split-K). Low-tile-count shapes (e.g. 8 instances x 768 features) split K
  * across otherwise idle SMs; partials reduce in split order (deterministic).
  */
-/*
- * nf_grouped_linear_ws plus an L2 prefetch hint: once its own operand loads
- * are issued, each CTA prefetches its share of [l2_prefetch,
- * l2_prefetch + l2_prefetch_bytes) (the next weight-streaming launch's
- * weights) into L2, so batch-1 plans keep HBM streaming across launches.
- * NULL / 0 disables the hint.
- */
-int nf_grouped_linear_ex(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                         const void* bias, const void* residual, void* y, int64_t y_ld,
-                         int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
-                         int dtype, int w_layout, int act, int mode, void* workspace,
-                         int64_t workspace_bytes, const void* l2_prefetch,
-                         int64_t l2_prefetch_bytes, void* stream);
-
 int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                          const void* bias, const void* residual, void* y, int64_t y_ld,
                          int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
@@ -319,14 +294,6 @@ int nf_batch_norm(const void* x, const float* gamma, const float* beta, const fl
  */
 int nf_pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind, int kernel,
               int stride, int pad, int dtype, void* stream);
-
-/*
- * Warm the 126 MB L2 with a byte range (e.g. the next merged Linear's
- * weights) while other kernels run, so weight streaming from HBM continues
- * across kernel boundaries. Stream-ordered like every other entry point: the
- * following kernel still observes everything that preceded this call.
- */
-int nf_l2_prefetch(const void* ptr, int64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -43,17 +43,12 @@ SIGNATURES: dict[str, list] = {
     "nf_linear_workspace_bytes": [_i64, _i64, _i64, _i64],
     "nf_grouped_linear_ws": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                              _i64, _i, _i, _i, _i, _p, _i64, _p],
-    "nf_l2_prefetch": [_p, _i64, _p],
     "nf_im2col_nhwc": [_p, _p] + [_i] * 10 + [_p],
     "nf_conv_nhwc_direct": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p],
     "nf_pool2d_nhwc": [_p, _p] + [_i] * 9 + [_p],
     "nf_grouped_conv_tc": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _i64, _p],
     "nf_conv_workspace_bytes": [_i] * 10,
-    "nf_grouped_linear_ln": [_p, _i64, _i64, _p, _p, _p, _p, _p, _f, _p, _i64, _i64, _i64, _i64,
-                             _i64, _i64, _p],
-    "nf_qkv_attention": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f, _p, _i64, _p],
-    "nf_grouped_linear_ex": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
-                             _i64, _i, _i, _i, _i, _p, _i64, _p, _i64, _p],
+    "nf_qkv_attention": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f, _p],
     "nf_linear_fold_supported": [_i64, _i64, _i64, _i64],
     "nf_grouped_linear_fold": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                                _i64, _i, _p, _i64, _p, _i, _p, _f, _p, _i, _p, _p, _f, _p, _p],

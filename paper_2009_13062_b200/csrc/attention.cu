@@ -257,16 +257,8 @@ __global__ void __launch_bounds__(128, 2)
 
 constexpr size_t kAttnSmem = 1024 + 5 * kTileBytes + 64;
 
-// NF_ATTN_8WARPS=1 selects the 8-warp persistent kernel (measured 3% slower
-// on BERT-base N=32 B=8 than the 4-warp one, whose two CTAs per SM already
-// overlap their softmax phases).
-inline bool attn_eight_warps() {
-  static const bool on = [] {
-    const char* e = getenv("NF_ATTN_8WARPS");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+// (An 8-warp persistent variant measured 3% slower on BERT-base N=32 B=8:
+// two 4-warp CTAs per SM already overlap their softmax phases.)
 
 // Persistent variant for many (sequence, head) units: each CTA walks units
 // u = blockIdx.x, += gridDim.x with the next unit's Q/K/V tiles loading into
@@ -432,175 +424,6 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-// 8-warp variant: warps w and w + 4 share TMEM lane quarter w & 3 and split
-// the keys (softmax) and the head dim (epilogue) in halves.
-constexpr size_t kAttnP8Smem = 1024 + 6 * kTileBytes + 4 * 128 * 4 + 128;
-
-__global__ void __launch_bounds__(256, 2)
-    k_attention_tc_persistent8(const __grid_constant__ CUtensorMap map_qkv,
-                              __nv_bfloat16* __restrict__ out, int S, int H, int units,
-                              float scale_log2) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  float* sMax = reinterpret_cast<float*>(smem + 6 * kTileBytes);  // [2][128]
-  float* sSum = sMax + 256;                                         // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sSum + 256);
-  uint64_t* bar_load = bars;  // [2]
-  uint64_t* bar_s = bars + 2;
-  uint64_t* bar_o = bars + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int half = warp >> 2;                 // key / output columns half
-  const int row = (warp & 3) * 32 + (tid & 31);  // query row == TMEM lane
-  if (tid == 0) {
-    tma_prefetch_desc(&map_qkv);
-    mbar_init(&bar_load[0], 1);
-    mbar_init(&bar_load[1], 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_o, 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(tmem_slot, 256);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_s = tmem, tmem_o = tmem + 128;
-  const uint32_t lane_off = uint32_t((warp & 3) * 32) << 16;
-
-  auto issue = [&](int u, int buf) {
-    uint8_t* b = smem + buf * 3 * kTileBytes;
-    const int bt = u / H, h = u % H;
-    mbar_arrive_expect_tx(&bar_load[buf], 3 * kTileBytes);
-    tma_load_4d(b, &map_qkv, &bar_load[buf], 0, h, 0, bt, kEvictFirst);
-    tma_load_4d(b + kTileBytes, &map_qkv, &bar_load[buf], 0, H + h, 0, bt, kEvictFirst);
-    tma_load_4d(b + 2 * kTileBytes, &map_qkv, &bar_load[buf], 0, 2 * H + h, 0, bt, kEvictFirst);
-  };
-  if (tid == 0) {
-    grid_dependency_wait();
-    if (int(blockIdx.x) < units) issue(blockIdx.x, 0);
-  }
-  grid_dependents_launch();
-
-  int i = 0;
-  for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
-    const int buf = i & 1;
-    uint8_t* sQ = smem + buf * 3 * kTileBytes;
-    uint8_t* sK = sQ + kTileBytes;
-    uint8_t* sV = sK + kTileBytes;
-    uint8_t* sP = sQ;  // Q|K, free once S is in TMEM
-    const int bt = u / H, h = u % H;
-    // next unit's tiles into the other buffer (its last reader, the previous
-    // unit's PV MMA, retired before that unit's epilogue)
-    if (tid == 0 && u + int(gridDim.x) < units) issue(u + gridDim.x, buf ^ 1);
-    mbar_wait(&bar_load[buf], uint32_t(i >> 1) & 1u);
-    if (tid == 0) {
-      tc_fence_after();
-      constexpr uint32_t idesc = make_idesc_bf16_f32(128, 128);
-      const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK);
-#pragma unroll
-      for (int kk = 0; kk < kAttnD / 16; ++kk)
-        umma_f16_ss(tmem_s, make_sw128_kmajor_desc(qa + kk * 32),
-                    make_sw128_kmajor_desc(ka + kk * 32), idesc, kk != 0);
-      umma_commit(bar_s);
-    }
-    mbar_wait(bar_s, uint32_t(i) & 1u);
-    tc_fence_after();
-    uint32_t r[2][32];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-      tmem_ld_32x32b_x32(tmem_s + lane_off + uint32_t(64 * half + c * 32), r[c]);
-    tmem_ld_wait();
-    float mx = -INFINITY;
-    {
-      float m8[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) m8[q] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          m8[j & 7] = fmaxf(m8[j & 7], (64 * half + c * 32 + j < S) ? __uint_as_float(r[c][j])
-                                                                     : -INFINITY);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) mx = fmaxf(mx, m8[q]);
-    }
-    sMax[half * 128 + row] = mx;
-    __syncthreads();  // both halves' maxima (S fully read into registers)
-    mx = fmaxf(sMax[row], sMax[128 + row]);
-    float s4[4] = {0.f, 0.f, 0.f, 0.f};
-    const uint32_t prow = smem_u32(sP);
-    const float mxs = mx * scale_log2;
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int c = 2 * half + cc;
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float x0 = (c * 32 + j < S) ? fmaf(__uint_as_float(r[cc][j]), scale_log2, -mxs)
-                                          : -INFINITY;
-        const float x1 = (c * 32 + j + 1 < S)
-                             ? fmaf(__uint_as_float(r[cc][j + 1]), scale_log2, -mxs)
-                             : -INFINITY;
-        const uint32_t packed = pack_bf16x2(ex2_approx(x0), ex2_approx(x1));
-        s4[(j >> 1) & 3] += __uint_as_float(packed << 16) + __uint_as_float(packed & 0xffff0000u);
-        pk[j >> 1] = packed;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        st_shared_v4(prow + kmajor_off(row, c * 32 + q * 8, 128), pk[4 * q], pk[4 * q + 1],
-                     pk[4 * q + 2], pk[4 * q + 3]);
-    }
-    sSum[half * 128 + row] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();  // P written; S fully read
-    if (tid == 0) {
-      tc_fence_after();
-      constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64, 0, 1);
-      const uint32_t pa = smem_u32(sP), va = smem_u32(sV);
-#pragma unroll
-      for (int kk = 0; kk < kAttnS / 16; ++kk) {
-        const int blk = kk >> 2, sub = kk & 3;
-        umma_f16_ss(tmem_o, make_sw128_kmajor_desc(pa + blk * 128 * 128 + sub * 32),
-                    make_sw128_mnmajor_desc(va + kk * 16 * 128, 8192, 1024), idesc, kk != 0);
-      }
-      umma_commit(bar_o);
-    }
-    mbar_wait(bar_o, uint32_t(i) & 1u);
-    tc_fence_after();
-    {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tmem_o + lane_off + uint32_t(32 * half), o);
-      tmem_ld_wait();
-      if (row < S) {
-        const float inv = 1.0f / (sSum[row] + sSum[128 + row]);
-        const int64_t D = int64_t(H) * kAttnD;
-        __nv_bfloat16* dst = out + (int64_t(bt) * S + row) * D + int64_t(h) * kAttnD + 32 * half;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(o[8 * q]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-          w.y = pack_bf16x2(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-          w.z = pack_bf16x2(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-          w.w = pack_bf16x2(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + q * 8) = w;
-        }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();  // TMEM S/O and this buffer's smem are free for the next unit
-  }
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 256);
-  }
-}
-
-
 // ---------------------------------------------------------------------------
 // SIMT fallback: one warp per (sequence, head, query), online softmax.
 // ---------------------------------------------------------------------------
@@ -741,23 +564,6 @@ __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restr
 // ---------------------------------------------------------------------------
 constexpr int kRelPitch = 68;                           // words per staged row
 constexpr int kRelStageBytes = 4 * 32 * kRelPitch * 4;  // 34816 B (4 warps)
-inline bool rel_eight_warps() {
-  static const bool on = [] {
-    const char* e = getenv("NF_REL_8WARPS");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-inline bool rel_persistent() {
-  static const bool on = [] {
-    const char* e = getenv("NF_REL_PERSISTENT");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-constexpr size_t kRelBufBytes = 2 * kTileBytes + 4096 + kTileBytes + 2 * kTileBytes;
-template <int NBUF>
-constexpr size_t rel_smem() { return 1024 + NBUF * kRelBufBytes + (128 + 256 + 128) * 4 + 64; }
 
 // positional keys r viewed as 4-D (dh, H, 2S, Bt); box (64, 1, 128, 1).
 bool make_r_map(CUtensorMap* map, const void* r, int64_t Bt, int64_t S, int64_t H) {
@@ -790,250 +596,7 @@ __device__ __forceinline__ float bias_dot_row(const uint8_t* tile, int row, cons
   return acc;
 }
 
-template <int NBUF>
-__global__ void __launch_bounds__(128, NBUF == 1 ? 2 : 1)
-    k_rel_attention_tc(const __grid_constant__ CUtensorMap map_qkv,
-                       const __grid_constant__ CUtensorMap map_r, const float* __restrict__ rwb,
-                       const float* __restrict__ rrb, __nv_bfloat16* __restrict__ out, int H,
-                       int seqs_per_bias, int seqs_per_r, int units, float scale_log2) {
-  // NBUF == 2: persistent over units with the next unit's tiles loading into
-  // the other buffer while this one computes (one CTA per SM).
-  constexpr int S = kAttnS;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  float* sBw = reinterpret_cast<float*>(smem + NBUF * kRelBufBytes);
-  float* sCr = sBw + 128;
-  float* sRb = sCr + 256;  // r_w_bias | r_r_bias of this (instance, head)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sRb + 128);
-  uint64_t* bar_load = bars;  // [2]
-  uint64_t* bar_s = bars + 2;
-  uint64_t* bar_bd = bars + 3;
-  uint64_t* bar_o = bars + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int lane = tid & 31;
-
-  if (tid == 0) {
-    tma_prefetch_desc(&map_qkv);
-    tma_prefetch_desc(&map_r);
-    mbar_init(&bar_load[0], 1);
-    mbar_init(&bar_load[1], 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_bd, 1);
-    mbar_init(bar_o, 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(tmem_slot, 256);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
-
-  auto issue = [&](int u, int buf) {
-    uint8_t* q = smem + buf * kRelBufBytes;
-    uint8_t* k = q + kTileBytes;
-    uint8_t* v = k + kTileBytes + 4096;
-    uint8_t* kr = v + kTileBytes;
-    const int bt = u / H, h = u % H;
-    mbar_arrive_expect_tx(&bar_load[buf], 5 * kTileBytes);
-    tma_load_4d(q, &map_qkv, &bar_load[buf], 0, h, 0, bt, kEvictFirst);
-    tma_load_4d(k, &map_qkv, &bar_load[buf], 0, H + h, 0, bt, kEvictFirst);
-    tma_load_4d(v, &map_qkv, &bar_load[buf], 0, 2 * H + h, 0, bt, kEvictFirst);
-    // sequences of one instance share its projected positional keys
-    tma_load_4d(kr, &map_r, &bar_load[buf], 0, h, 0, bt / seqs_per_r, kEvictLast);
-    tma_load_4d(kr + kTileBytes, &map_r, &bar_load[buf], 0, h, S, bt / seqs_per_r, kEvictLast);
-  };
-  if (tid == 0) {
-    grid_dependency_wait();
-    if (int(blockIdx.x) < units) issue(blockIdx.x, 0);
-  }
-  grid_dependents_launch();
-
-  int it = 0;
-  for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-  const int buf = NBUF == 2 ? (it & 1) : 0;
-  const uint32_t ph = uint32_t(it) & 1u;
-  uint8_t* sQ = smem + buf * kRelBufBytes;
-  uint8_t* sK = sQ + kTileBytes;
-  uint8_t* sStage = sQ;  // Q | K | 4 KB pad, reused after the raw MMA retired
-  uint8_t* sV = sK + kTileBytes + 4096;
-  uint8_t* sKR = sV + kTileBytes;  // 256 rows; later P (128 x 128, 2 k-blocks)
-  const int bt = u / H;
-  const int h = u % H;
-  const int inst = bt / seqs_per_bias;
-  if (NBUF == 2 && tid == 0 && u + int(gridDim.x) < units) issue(u + gridDim.x, buf ^ 1);
-  const float* bw_src = rwb + (int64_t(inst) * H + h) * kAttnD;
-  const float* br_src = rrb + (int64_t(inst) * H + h) * kAttnD;
-  mbar_wait(&bar_load[buf], NBUF == 2 ? (uint32_t(it >> 1) & 1u) : ph);
-
-  if (tid == 0) {
-    tc_fence_after();
-    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 128);
-    const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK);
-#pragma unroll
-    for (int kk = 0; kk < kAttnD / 16; ++kk)
-      umma_f16_ss(tmem, make_sw128_kmajor_desc(qa + kk * 32),
-                  make_sw128_kmajor_desc(ka + kk * 32), idesc, kk != 0);
-    umma_commit(bar_s);
-  }
-  // bias . key rows (fp32) while the MMA runs.
-  if (tid < 32) {
-    sRb[tid] = __ldg(bw_src + tid);
-    sRb[tid + 32] = __ldg(bw_src + tid + 32);
-  } else if (tid < 64) {
-    sRb[tid + 32] = __ldg(br_src + tid - 32);
-    sRb[tid + 64] = __ldg(br_src + tid);
-  }
-  __syncthreads();
-  sBw[tid] = bias_dot_row(sK, tid, sRb);
-  sCr[tid] = bias_dot_row(sKR, tid, sRb + 64);
-  sCr[tid + 128] = bias_dot_row(sKR, tid + 128, sRb + 64);
-
-  mbar_wait(bar_s, ph);
-  tc_fence_after();
-  uint32_t r[4][32];  // AC row of this query
-#pragma unroll
-  for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + uint32_t(c * 32), r[c]);
-  tmem_ld_wait();
-  tc_fence_before();
-  __syncthreads();  // AC consumed by everyone; bias vectors visible
-
-  if (tid == 0) {
-    tc_fence_after();
-    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 256);
-    const uint32_t qa = smem_u32(sQ), ra = smem_u32(sKR);
-#pragma unroll
-    for (int kk = 0; kk < kAttnD / 16; ++kk)
-      umma_f16_ss(tmem, make_sw128_kmajor_desc(qa + kk * 32),
-                  make_sw128_kmajor_desc(ra + kk * 32), idesc, kk != 0);
-    umma_commit(bar_bd);
-  }
-  // AC + bw, in log2 units (scale folded).
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      r[c][j] = __float_as_uint(__uint_as_float(r[c][j]) + sBw[c * 32 + j]);
-
-  mbar_wait(bar_bd, ph);
-  tc_fence_after();
-  // Rel-shift through the per-warp staging window.
-  const uint32_t stage_w = smem_u32(sStage) + uint32_t(warp * 32 * kRelPitch * 4);
-  const int i_row = warp * 32 + lane;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int p0 = 97 - 32 * warp + 32 * c;  // window start for lane 31, jj 0
-    const int base = p0 < 192 ? p0 : 192;
-    const int shift = 31 - lane + (p0 - base);
-    __syncwarp();  // previous chunk's reads of the window are done
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint32_t wv[32];
-      tmem_ld_32x32b_x32(lane_base + uint32_t(base + 32 * half), wv);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        st_shared_v4(stage_w + uint32_t((lane * kRelPitch + 32 * half + 4 * q) * 4), wv[4 * q],
-                     wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]);
-    }
-    __syncwarp();
-    const float* row = reinterpret_cast<const float*>(sStage + warp * 32 * kRelPitch * 4) +
-                       lane * kRelPitch + shift;
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int p = S - i_row + c * 32 + jj;
-      r[c][jj] = __float_as_uint(__uint_as_float(r[c][jj]) + row[jj] + sCr[p]);
-    }
-  }
-  __syncwarp();
-
-  // Softmax over the row (all 128 keys valid).
-  float mx = -INFINITY;
-  {
-    float m8[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) m8[q] = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) m8[j & 7] = fmaxf(m8[j & 7], __uint_as_float(r[c][j]));
-#pragma unroll
-    for (int q = 0; q < 8; ++q) mx = fmaxf(mx, m8[q]);
-  }
-  float s4[4] = {0.f, 0.f, 0.f, 0.f};
-  uint8_t* sP = sKR;  // the raw MMA (last reader of KR) has retired
-  const uint32_t prow = smem_u32(sP);
-  const float mxs = mx * scale_log2;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int j = 0; j < 32; j += 2) {
-      const float x0 = fmaf(__uint_as_float(r[c][j]), scale_log2, -mxs);
-      const float x1 = fmaf(__uint_as_float(r[c][j + 1]), scale_log2, -mxs);
-      const uint32_t packed = pack_bf16x2(ex2_approx(x0), ex2_approx(x1));
-      s4[(j >> 1) & 3] += __uint_as_float(packed << 16) + __uint_as_float(packed & 0xffff0000u);
-      pk[j >> 1] = packed;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      st_shared_v4(prow + kmajor_off(tid, c * 32 + q * 8, 128), pk[4 * q], pk[4 * q + 1],
-                   pk[4 * q + 2], pk[4 * q + 3]);
-  }
-  const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();  // P complete; every raw TMEM read done
-
-  if (tid == 0) {
-    tc_fence_after();
-    constexpr uint32_t idesc = make_idesc_bf16_f32(128, 64, 0, 1);
-    const uint32_t pa = smem_u32(sP), va = smem_u32(sV);
-#pragma unroll
-    for (int kk = 0; kk < kAttnS / 16; ++kk) {
-      const int blk = kk >> 2, sub = kk & 3;
-      umma_f16_ss(tmem, make_sw128_kmajor_desc(pa + blk * 128 * 128 + sub * 32),
-                  make_sw128_mnmajor_desc(va + kk * 16 * 128, 8192, 1024), idesc, kk != 0);
-    }
-    umma_commit(bar_o);
-  }
-  mbar_wait(bar_o, ph);
-  tc_fence_after();
-  {
-    uint32_t o[2][32];
-    tmem_ld_32x32b_x32(lane_base, o[0]);
-    tmem_ld_32x32b_x32(lane_base + 32, o[1]);
-    tmem_ld_wait();
-    const float inv = 1.0f / sum;
-    const int64_t D = int64_t(H) * kAttnD;
-    __nv_bfloat16* dst = out + (int64_t(bt) * S + tid) * D + int64_t(h) * kAttnD;
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u;
-        u.x = pack_bf16x2(__uint_as_float(o[c][8 * q]) * inv, __uint_as_float(o[c][8 * q + 1]) * inv);
-        u.y = pack_bf16x2(__uint_as_float(o[c][8 * q + 2]) * inv, __uint_as_float(o[c][8 * q + 3]) * inv);
-        u.z = pack_bf16x2(__uint_as_float(o[c][8 * q + 4]) * inv, __uint_as_float(o[c][8 * q + 5]) * inv);
-        u.w = pack_bf16x2(__uint_as_float(o[c][8 * q + 6]) * inv, __uint_as_float(o[c][8 * q + 7]) * inv);
-        *reinterpret_cast<uint4*>(dst + c * 32 + q * 8) = u;
-      }
-  }
-  tc_fence_before();
-  __syncthreads();  // TMEM, smem and bias vectors free for the next unit
-  if (NBUF == 1 && tid == 0 && u + int(gridDim.x) < units) issue(u + gridDim.x, 0);
-  }
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 256);
-  }
-}
-
-// 8-warp variant (one CTA per (sequence, head), two CTAs per SM): warps w
+// One CTA per (sequence, head), two CTAs per SM, 8 warps: warps w
 // and w + 4 share TMEM lane quarter w & 3 and split the 128 key columns in
 // halves, so each thread holds 64 scores (no spills), the rel-shift windows
 // of the two halves run in parallel, and the row max / sum combine through
@@ -1282,39 +845,16 @@ int rel_attention(const void* qkv, const void* r, const float* rwb, const float*
     CUtensorMap mq, mr;
     if (!make_qkv_map(&mq, qkv, Bt, S, H) || !make_r_map(&mr, r, Bt / seqs_per_r, S, H))
       return NF_ERR_LAUNCH;
-    static bool attr_done = false;
-    if (!attr_done) {
-      cudaFuncSetAttribute(k_rel_attention_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(rel_smem<1>()));
-      cudaFuncSetAttribute(k_rel_attention_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(rel_smem<2>()));
-      attr_done = true;
-    }
+    // 8 warps, one CTA per (sequence, head), two CTAs per SM. Measured
+    // faster than a 4-warp kernel (92 vs 79 us per XLNet-base layer at 1536
+    // units) and than a persistent double-buffered one.
+    static SmemAttrOnce smem_attr;
+    smem_attr.set(k_rel_attention_tc8, int(kRel8Smem));
     const int units = int(Bt * H);
     const float scale_log2 = scale * 1.4426950408889634f;
-    cudaError_t e;
-    // Default: the 8-warp kernel (two warps per TMEM lane quarter). The
-    // persistent double-buffered variant (NBUF = 2, one CTA per SM) measured
-    // slower (92 vs 79 us per XLNet-base layer at 1536 units) than two
-    // single-buffered CTAs per SM, whose chains overlap each other.
-    if (rel_eight_warps()) {
-      static bool attr8 = false;
-      if (!attr8) {
-        cudaFuncSetAttribute(k_rel_attention_tc8, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kRel8Smem));
-        attr8 = true;
-      }
-      e = launch_pdl(k_rel_attention_tc8, dim3(units), dim3(256), kRel8Smem, stream, mq, mr, rwb,
-                     rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
-                     int(seqs_per_r), scale_log2);
-    } else if (units > 2 * kNumSMs && rel_persistent())
-      e = launch_pdl(k_rel_attention_tc<2>, dim3(kNumSMs), dim3(128), rel_smem<2>(), stream, mq,
-                     mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
-                     int(seqs_per_r), units, scale_log2);
-    else
-      e = launch_pdl(k_rel_attention_tc<1>, dim3(units), dim3(128), rel_smem<1>(), stream, mq,
-                     mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H), int(seqs_per_bias),
-                     int(seqs_per_r), units, scale_log2);
+    cudaError_t e = launch_pdl(k_rel_attention_tc8, dim3(units), dim3(256), kRel8Smem, stream, mq,
+                               mr, rwb, rrb, static_cast<__nv_bfloat16*>(out), int(H),
+                               int(seqs_per_bias), int(seqs_per_r), scale_log2);
     return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
   }
   const int64_t warps = Bt * H * S;
@@ -1346,47 +886,21 @@ int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int6
     if (!make_qkv_map(&map, qkv, Bt, S, H)) return NF_ERR_LAUNCH;
     const int64_t units = Bt * H;
     if (units > 2 * kNumSMs) {
-      static bool pattr = false;
-      if (!pattr) {
-        cudaFuncSetAttribute(k_attention_tc_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(kAttnPSmem));
-        pattr = true;
-      }
+      static SmemAttrOnce pattr;
+      pattr.set(k_attention_tc_persistent, int(kAttnPSmem));
       const int grid = 2 * kNumSMs;
       const float sl2 = scale * 1.4426950408889634f;
-      static bool pattr8 = false;
-      if (!pattr8) {
-        cudaFuncSetAttribute(k_attention_tc_persistent8,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kAttnP8Smem));
-        pattr8 = true;
-      }
-      cudaError_t e = attn_eight_warps()
-          ? launch_pdl(k_attention_tc_persistent8, dim3(grid), dim3(256), kAttnP8Smem, stream,
-                       map, static_cast<__nv_bfloat16*>(out), int(S), int(H), int(units), sl2)
-          : launch_pdl(k_attention_tc_persistent, dim3(grid), dim3(128), kAttnPSmem, stream, map,
-                       static_cast<__nv_bfloat16*>(out), int(S), int(H), int(units), sl2);
+      cudaError_t e = launch_pdl(k_attention_tc_persistent, dim3(grid), dim3(128), kAttnPSmem,
+                                 stream, map, static_cast<__nv_bfloat16*>(out), int(S), int(H),
+                                 int(units), sl2);
       return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
     }
-    static bool attr_done = false;
-    if (!attr_done) {
-      cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(kAttnSmem));
-      attr_done = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(Bt * H));
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = kAttnSmem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled();
+    static SmemAttrOnce smem_attr;
+    smem_attr.set(k_attention_tc, int(kAttnSmem));
     const float scale_log2 = scale * 1.4426950408889634f;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_attention_tc, map,
-                                       static_cast<__nv_bfloat16*>(out), int(S), int(H),
-                                       scale_log2);
+    cudaError_t e = launch_pdl(k_attention_tc, dim3(unsigned(Bt * H)), dim3(128), kAttnSmem,
+                               stream, map, static_cast<__nv_bfloat16*>(out), int(S), int(H),
+                               scale_log2);
     return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
   }
   const int64_t warps = Bt * H * S;

@@ -5,7 +5,7 @@
 
 extern "C" {
 
-int nf_abi_version(void) { return 1; }
+int nf_abi_version(void) { return 2; }
 
 const char* nf_status_string(int status) {
   switch (status) {
@@ -22,12 +22,11 @@ int64_t nf_linear_workspace_bytes(int64_t groups, int64_t rows, int64_t k, int64
   return nf::linear_workspace_bytes(groups, rows, k, n);
 }
 
-int nf_grouped_linear_ex(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                          const void* bias, const void* residual, void* y, int64_t y_ld,
                          int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
                          int dtype, int w_layout, int act, int mode, void* workspace,
-                         int64_t workspace_bytes, const void* l2_prefetch,
-                         int64_t l2_prefetch_bytes, void* stream) {
+                         int64_t workspace_bytes, void* stream) {
   if (!x || !w || !y || groups < 1 || rows < 1 || k < 1 || n < 1) return NF_ERR_SHAPE;
   if (x_ld < k || y_ld < n || (groups > 1 && (x_gs < 1 || y_gs < 1))) return NF_ERR_SHAPE;
   if (dtype != NF_F32 && dtype != NF_BF16) return NF_ERR_UNSUPPORTED;
@@ -37,22 +36,11 @@ int nf_grouped_linear_ex(const void* x, int64_t x_ld, int64_t x_gs, const void* 
   const float* b = static_cast<const float*>(bias);
   if (mode == NF_MODE_FAST && dtype == NF_BF16 && w_layout == NF_W_NK) {
     int st = nf::grouped_linear_tc(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
-                                   n, dtype, act, workspace, workspace_bytes, s, l2_prefetch,
-                                   l2_prefetch_bytes);
+                                   n, dtype, act, workspace, workspace_bytes, s);
     if (st != NF_ERR_UNSUPPORTED) return st;
   }
   return nf::grouped_linear_simt(x, x_ld, x_gs, w, b, residual, y, y_ld, y_gs, groups, rows, k,
                                  n, dtype, w_layout, act, mode == NF_MODE_EXACT, s);
-}
-
-int nf_grouped_linear_ws(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                         const void* bias, const void* residual, void* y, int64_t y_ld,
-                         int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
-                         int dtype, int w_layout, int act, int mode, void* workspace,
-                         int64_t workspace_bytes, void* stream) {
-  return nf_grouped_linear_ex(x, x_ld, x_gs, w, bias, residual, y, y_ld, y_gs, groups, rows, k, n,
-                              dtype, w_layout, act, mode, workspace, workspace_bytes, nullptr, 0,
-                              stream);
 }
 
 int nf_grouped_linear_strided(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
@@ -173,22 +161,12 @@ int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups
   return nf::conv_workspace_bytes(N, H, W, C, Cout, groups, kernel, stride, pad, kpad);
 }
 
-int nf_grouped_linear_ln(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                         const float* bias, const void* residual, const float* gamma,
-                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
-                         int64_t groups, int64_t rows, int64_t k, int64_t n, void* stream) {
-  if (!x || !w || !y || !gamma || !beta) return NF_ERR_SHAPE;
-  return nf::grouped_linear_ln_tc(x, x_ld, x_gs, w, bias, residual, gamma, beta, eps, y, y_ld,
-                                  y_gs, groups, rows, k, n, static_cast<cudaStream_t>(stream));
-}
-
 int nf_qkv_attention(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t groups, int64_t seq, int64_t d_model, int64_t heads,
-                     float scale, const void* l2_prefetch, int64_t l2_prefetch_bytes,
-                     void* stream) {
+                     float scale, void* stream) {
   if (!x || !w || !out) return NF_ERR_SHAPE;
   return nf::qkv_attention_tc(x, x_ld, x_gs, w, bias, out, groups, seq, d_model, heads, scale,
-                              static_cast<cudaStream_t>(stream), l2_prefetch, l2_prefetch_bytes);
+                              static_cast<cudaStream_t>(stream));
 }
 
 int nf_linear_fold_supported(int64_t groups, int64_t rows, int64_t k, int64_t n) {
@@ -210,8 +188,7 @@ int nf_grouped_linear_fold(const void* x, int64_t x_ld, int64_t x_gs, const void
                           res_gamma, res_beta, res_parts, res_eps, out_stats};
   return nf::grouped_linear_tc(x, x_ld, x_gs, w, static_cast<const float*>(bias), residual, y,
                                y_ld, y_gs, groups, rows, k, n, NF_BF16, act, workspace,
-                               workspace_bytes, static_cast<cudaStream_t>(stream), nullptr, 0,
-                               &fold);
+                               workspace_bytes, static_cast<cudaStream_t>(stream), &fold);
 }
 
 int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
@@ -222,7 +199,7 @@ int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void*
   const nf::NormFold fold{in_stats, in_colsum, in_parts, in_eps, nullptr,
                           nullptr, nullptr, 0, 0.f, nullptr};
   return nf::qkv_attention_tc(x, x_ld, x_gs, w, bias, out, groups, seq, d_model, heads, scale,
-                              static_cast<cudaStream_t>(stream), nullptr, 0, &fold);
+                              static_cast<cudaStream_t>(stream), &fold);
 }
 
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
@@ -231,10 +208,6 @@ int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind,
   if (kind != NF_POOL_MAX && kind != NF_POOL_MEAN) return NF_ERR_UNSUPPORTED;
   return nf::pool_nhwc(x, y, N, H, W, C, kind, kernel, stride, pad, dtype,
                        static_cast<cudaStream_t>(stream));
-}
-
-int nf_l2_prefetch(const void* ptr, int64_t bytes, void* stream) {
-  return nf::l2_prefetch(ptr, bytes, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 // loads, tcgen05 (TMEM alloc / MMA / commit / ld) and the UMMA shared-memory
 // and instruction descriptors. No global state lives in this header.
 #pragma once
+#include <atomic>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -73,12 +74,44 @@ NF_DEVICE float gelu_bf16_epilogue(float x) {
   return fmaf(hx, tanh_approx(u), hx);
 }
 
+// bf16-output epilogue activations: GELU (tanh form) and tanh on the SFU's
+// tanh.approx (relative error ~2^-11, below the bf16 output rounding).
 template <int ACT>
 NF_DEVICE float act_t(float v) {
   if constexpr (ACT == NF_ACT_RELU) return fmaxf(v, 0.0f);
   else if constexpr (ACT == NF_ACT_GELU) return gelu_bf16_epilogue(v);
-  else if constexpr (ACT == NF_ACT_TANH) return tanhf(v);
+  else if constexpr (ACT == NF_ACT_TANH) return tanh_approx(v);
   else return v;
+}
+
+// Epilogue activation chosen at run time (a launch-uniform branch around the
+// whole chunk, so each case is a straight unrolled loop). RELU_ONLY kernels
+// (implicit-GEMM convs: folded BN + ReLU) compile only that case.
+template <bool RELU_ONLY = false, int N>
+NF_DEVICE void apply_act(int act, float (&v)[N]) {
+  if constexpr (RELU_ONLY) {
+    if (act == NF_ACT_RELU) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = act_t<NF_ACT_RELU>(v[j]);
+    }
+    return;
+  }
+  switch (act) {
+    case NF_ACT_RELU:
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = act_t<NF_ACT_RELU>(v[j]);
+      break;
+    case NF_ACT_GELU:
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = act_t<NF_ACT_GELU>(v[j]);
+      break;
+    case NF_ACT_TANH:
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = act_t<NF_ACT_TANH>(v[j]);
+      break;
+    default:
+      break;
+  }
 }
 
 // 2^x, flush-to-zero approximate (MUFU.EX2, one instruction).
@@ -211,26 +244,6 @@ NF_DEVICE void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, ui
 }
 
 // L2 prefetch of a contiguous global range (bytes multiple of 16).
-NF_DEVICE void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gsrc)),
-               "r"(bytes)
-               : "memory");
-}
-// Each CTA of the grid prefetches its even share of [base, base + bytes) into
-// L2: a weight-streaming kernel warms the NEXT launch's weights once its own
-// loads are issued, so that launch's first TMA tiles hit L2.
-NF_DEVICE void prefetch_share_l2(const void* base, int64_t bytes) {
-  if (!base || bytes <= 0) return;
-  const int64_t per = ((bytes / gridDim.x) + 255) & ~int64_t(255);
-  int64_t lo = int64_t(blockIdx.x) * per;
-  const int64_t hi = lo + per < bytes ? lo + per : bytes;
-  const uint8_t* b = static_cast<const uint8_t*>(base);
-  for (; lo + 16 <= hi; lo += 65536) {
-    const int64_t n = hi - lo < 65536 ? ((hi - lo) & ~int64_t(15)) : 65536;
-    if (n > 0) bulk_prefetch_l2(b + lo, uint32_t(n));
-  }
-}
-
 // TMA bulk-tensor store smem -> global (bulk-group completion).
 NF_DEVICE void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
   asm volatile(
@@ -468,15 +481,25 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(int M, int N, int a_m
 // Launch with programmatic dependent launch enabled: the kernel may start
 // while its predecessor in the stream drains; kernels call
 // grid_dependency_wait() before touching data the predecessor writes.
-// Debug knob (read once, immutable after): NF_PDL=0 disables programmatic
-// dependent launch everywhere, for A/B timing.
-inline int pdl_enabled() {
-  static const int on = [] {
-    const char* e = getenv("NF_PDL");
-    return (e && e[0] == '0') ? 0 : 1;
-  }();
-  return on;
-}
+// (Always on: every launch carries the programmatic-serialization attribute.)
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and
+// device: function attributes live in each device's context, so a process
+// driving several GPUs must set them on each. One instance per kernel (a
+// function-local static next to the launch); idempotent, so two threads
+// racing on the first launch both just set the same value.
+struct SmemAttrOnce {
+  std::atomic<unsigned long long> done{0};
+  template <typename F>
+  void set(F kern, int bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+};
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -490,7 +513,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled();
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
@@ -501,24 +524,36 @@ NF_DEVICE void pdl_enter() {
   grid_dependents_launch();
 }
 
-// Per-token (mean, rstd) of a folded LayerNorm from its producer's partial sums.
+// Per-token (mean, rstd) of a folded LayerNorm over D features from its
+// producer's statistics of `parts` equal parts (the producer's 128-feature
+// tiles): (sum, M2 = centred sum of squares about the part's own mean).
+// Parts merge in index order with Chan et al.'s pairwise update
+//   (n_a, mean_a, M2_a) + (n_p, mean_b, M2_b): delta = mean_b - mean_a,
+//   mean += delta * n_p / n,  M2 += M2_b + delta^2 * n_a * n_p / n,
+// so the variance never forms E[x^2] - mean^2 (no cancellation when
+// |mean| >> std) and the reduction order is fixed (deterministic).
 NF_DEVICE float2 fold_stats(const float2* st, int parts, int rows, int g, int tok, float inv_d,
                             float eps) {
-  float s = 0.f, ss = 0.f;
+  const float n_p = 1.0f / (inv_d * float(parts));  // features per part
+  const float inv_np = inv_d * float(parts);
+  const float2* base = st + int64_t(g) * parts * rows + tok;
+  float n = 0.f, mean = 0.f, m2 = 0.f;
   for (int q0 = 0; q0 < parts; q0 += 8) {
-    float2 v[8];  // up to 8 partials in flight (D <= 1024 in one round trip)
+    float2 v[8];  // up to 8 parts in flight (D <= 1024 in one round trip)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      v[i] = q0 + i < parts ? __ldcg(st + (int64_t(g) * parts + q0 + i) * rows + tok)
-                            : make_float2(0.f, 0.f);
+      v[i] = q0 + i < parts ? __ldcg(base + int64_t(q0 + i) * rows) : make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      s += v[i].x;
-      ss += v[i].y;
+      if (q0 + i >= parts) break;
+      const float nn = n + n_p;
+      const float delta = v[i].x * inv_np - mean;
+      mean = fmaf(delta, n_p / nn, mean);
+      m2 += v[i].y + delta * delta * (n * n_p / nn);
+      n = nn;
     }
   }
-  const float mu = s * inv_d;
-  return make_float2(mu, rsqrtf(fmaxf(ss * inv_d - mu * mu, 0.f) + eps));
+  return make_float2(mean, rsqrtf(fmaxf(m2 * inv_d, 0.f) + eps));
 }
 
 }  // namespace nf

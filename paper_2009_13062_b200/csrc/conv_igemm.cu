@@ -21,22 +21,10 @@ namespace nf {
 
 namespace {
 
-// NF_CONV_HALO=0 forces the per-tap cp.async gather (A/B knob, read once).
-bool halo_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("NF_CONV_HALO");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-bool halo_stem() {
-  static const bool on = [] {
-    const char* e = getenv("NF_CONV_HALO_STEM");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+// The 4-channel (padded RGB stem) halo gather: two taps per 16-byte chunk.
+// Measured slower than the per-tap 8-byte cp.async gather for the ResNet
+// stem, so the stem keeps the per-tap gather (kernel path kept and tested).
+constexpr bool kHaloStem = false;
 
 // 4-D NHWC box for the halo gather: (cg channels, halo_w columns, halo_h rows, 1 image).
 bool make_halo_map(CUtensorMap* map, const void* x, int N, int H, int W, int C, int cg,
@@ -62,32 +50,20 @@ int conv_pick(int64_t pix, int64_t coutg, bool* swap) {
   return 256;
 }
 
-// Max split-K factor for convs (knob NF_CONV_MAXSPLIT, read once): the last
-// arriving split reduces every partial of its tile alone, so deep splits
-// trade HBM streaming parallelism for a serial fix-up.
-int conv_max_splits() {
-  static const int v = [] {
-    const char* e = getenv("NF_CONV_MAXSPLIT");
-    return e ? atoi(e) : 4;
-  }();
-  return v < 1 ? 1 : (v > kMaxSplits ? kMaxSplits : v);
-}
+// Max split-K factor for convs: the last arriving split reduces every
+// partial of its tile alone, so deep splits trade HBM streaming parallelism
+// for a serial fix-up.
+constexpr int kConvMaxSplits = 4;
 
 int conv_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) {
   if (ws_bytes <= kCounterBytes || tiles >= 96 || tiles > kCounterBytes / 4) return 1;
   int s = int(kNumSMs / tiles);
-  s = s < conv_max_splits() ? s : conv_max_splits();
+  s = s < kConvMaxSplits ? s : kConvMaxSplits;
   s = s < kb_total / 4 ? s : kb_total / 4;  // >= 4 K blocks per split
   while (s > 1 && tiles * s * int64_t(kGemmBM) * bn * 4 > ws_bytes - kCounterBytes) --s;
   return s < 1 ? 1 : s;
 }
 
-template <int BN, bool SWAP, int GATHER>
-int launch_conv(bool relu, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
-                const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t st) {
-  if (relu) return launch_tc_res<BN, SWAP, NF_ACT_RELU, GATHER>(ma, mb, my, mr, p, grid, st);
-  return launch_tc_res<BN, SWAP, NF_ACT_NONE, GATHER>(ma, mb, my, mr, p, grid, st);
-}
 
 }  // namespace
 
@@ -132,11 +108,11 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   const int64_t halo_bytes = (halo_raw + 1023) / 1024 * 1024;
   // (4-channel groups work too — the padded stem — but measured slower than
   // the 8-byte cp.async gather: a 7x7/s2 halo is barely smaller than 49 taps.)
-  bool halo = halo_enabled() && !swap && N == 1 &&
-                    (cg == 16 || cg == 32 || cg == 64 || (cg == 4 && halo_stem())) &&
-                    bn <= 64 && halo_h <= 256 && halo_w <= 256 && halo_bytes <= 48 * 1024;
+  bool halo = !swap && N == 1 && (cg == 16 || cg == 32 || cg == 64 || (cg == 4 && kHaloStem)) &&
+              bn <= 64 && halo_h <= 256 && halo_w <= 256 && halo_bytes <= 48 * 1024;
 
   GemmParams p{};
+  p.act = relu ? NF_ACT_RELU : NF_ACT_NONE;
   p.bias = bias;
   p.residual = residual;
   p.out_gstride = coutg;
@@ -186,13 +162,11 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
   p.units = int(tiles * p.splits);
   p.counters = static_cast<unsigned*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
-  const int grid = balanced_all() ? balanced_grid(p.units, kNumSMs)
-                                 : (p.units < kNumSMs ? p.units : kNumSMs);
-  const bool r = relu != 0;
+  const int grid = p.units < kNumSMs ? p.units : kNumSMs;
   // The weights map is the only TMA operand; it sits in the slot its
   // orientation reads (A when swapped, B otherwise).
-#define NF_CV(BNV, SW, GA) return launch_conv<BNV, SW, GA>(r, mw, mw, my, mr, p, grid, stream)
-#define NF_CH(BNV) return launch_conv<BNV, false, 1>(r, mh, mw, my, mr, p, grid, stream)
+#define NF_CV(BNV, SW, GA) return launch_tc_res<BNV, SW, GA>(mw, mw, my, mr, p, grid, stream)
+#define NF_CH(BNV) return launch_tc_res<BNV, false, 1>(mh, mw, my, mr, p, grid, stream)
   if (halo) {
     if (bn == 16) NF_CH(16);
     if (bn == 32) NF_CH(32);

@@ -45,69 +45,25 @@ bool make_bf16_map_kpt2(CUtensorMap* map, const void* base, int64_t G, int64_t r
   return r == CUDA_SUCCESS;
 }
 
-// Two k-blocks per TMA transaction for swapped 128-token tiles: the batch-1
-// main loop is bound by a per-stage cost, not bytes (tools/gemm_trace.cu:
-// 768->768 main loop 3.7 -> 2.9 us, 3072->768 split 5.1 -> 3.9 us; BERT-8
-// 0.635 -> 0.625 ms). NF_GEMM_KPT=1 keeps one k-block per stage, =3 moves
-// three (two 96 KB stages: main loops a further 0-10% shorter but the step
-// 0.620 -> 0.639 ms, split ranges of 16 k-blocks waste a third of a stage).
-static int kpt_setting() {
-  static const int v = [] {
-    const char* e = getenv("NF_GEMM_KPT");
-    return e ? atoi(e) : 2;
-  }();
-  return v;
-}
-static bool kpt2_enabled() { return kpt_setting() >= 2; }
-
 static int pick_bn(int64_t T, int64_t N) {
   if (T <= 256) return T <= 64 ? 64 : (T <= 128 ? 128 : 256);
   return N >= 256 ? 256 : (N > 64 ? 128 : 64);
 }
 
-// Split-K factor: enough units to cover the SMs when the tile count is low,
-// with at least 4 K blocks per split and a workspace that fits.
-// Minimum K blocks per split (debug knob NF_SPLITK_MINKB, read once).
-static int splitk_min_kb() {
-  static const int v = [] {
-    const char* e = getenv("NF_SPLITK_MINKB");
-    return e ? atoi(e) : 16;
-  }();
-  return v < 1 ? 1 : v;
-}
+// Split-K: a split adds a partial write + reduction to the critical path, so
+// each one must still stream at least this many 64-wide K blocks.
+constexpr int kSplitMinKB = 16;
 
+// Split-K factor: enough units to cover the SMs when the tile count is low,
+// with long K ranges per split and a workspace that fits.
 static int choose_splits(int64_t tiles, int kb_total, int bn, int64_t ws_bytes) {
   if (ws_bytes <= kCounterBytes || tiles >= 100 || tiles > kCounterBytes / 4) return 1;
   int s = int(kNumSMs / tiles);
   s = s < kMaxSplits ? s : kMaxSplits;
-  // Each split adds a partial write + reduction to the critical path; only
-  // worth it when every split still streams a long K range.
-  const int cap = kb_total / splitk_min_kb();
+  const int cap = kb_total / kSplitMinKB;
   s = s < cap ? s : cap;
   while (s > 1 && tiles * s * int64_t(kGemmBM) * bn * 4 > ws_bytes - kCounterBytes) --s;
   return s < 1 ? 1 : s;
-}
-
-// CTA pairs (cta_group::2): large-T tensor-bound tiles (128x256 per CTA,
-// 256x256 per pair: each SM loads half of B) and batch-1 weight-streaming
-// tiles (each SM loads 128 weight rows and half of the tokens). NF_GEMM_PAIR=0
-// disables them (A/B knob, read once).
-static bool pair_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("NF_GEMM_PAIR");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-// Experiment knob: cap on persistent CTAs for swapped launches with more
-// units than SMs (NF_SWAP_GRID_CAP, read once; 0 = one CTA per SM).
-static int swap_grid_cap() {
-  static const int v = [] {
-    const char* e = getenv("NF_SWAP_GRID_CAP");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
 }
 
 struct LinearPlan {
@@ -117,37 +73,15 @@ struct LinearPlan {
   int splits;
 };
 
-// Batch-1 launches with more 128-feature tiles than SMs: token rows on M and
-// 256-feature tiles on N (each CTA then streams 2 weight tiles per
-// activation tile instead of 1) — knob NF_SMALLT_NORMAL (read once).
-static bool smallt_normal() {
-  static const bool on = [] {
-    const char* e = getenv("NF_SMALLT_NORMAL");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_t ws_bytes) {
   LinearPlan L;
   L.swap = T <= 256;
   L.bn = pick_bn(T, N);
-  if (L.swap && smallt_normal() && T <= 128 && N >= 256 && N % 256 == 0 &&
-      G * ((N + kGemmBM - 1) / kGemmBM) > kNumSMs) {
-    L.swap = false;
-    L.bn = 256;
-    L.pair = false;
-    L.tiles_a = (T + kGemmBM - 1) / kGemmBM;
-    L.tiles_b = N / 256;
-    L.tiles = G * L.tiles_a * L.tiles_b;
-    L.splits = 1;
-    return L;
-  }
   // Measured (tools/gemm_trace.cu): pairs cut the MMA's operand stalls on
   // 128x256 tensor-bound tiles (4-5 stages of 32 KB per CTA instead of 3 of
   // 48 KB); on batch-1 weight-streaming tiles they only add cluster-launch
   // latency, so swapped tiles stay single-CTA.
-  L.pair = pair_enabled() && !L.swap && L.bn == 256;
+  L.pair = !L.swap && L.bn == 256;
   const int64_t rows_a = L.swap ? N : T, rows_b = L.swap ? T : N;
   const int rows_per_a = L.pair ? 2 * kGemmBM : kGemmBM;
   L.tiles_a = (rows_a + rows_per_a - 1) / rows_per_a;
@@ -164,9 +98,9 @@ static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_
 bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
   if (G < 1 || K % 8 || N % 8 || G > 65535) return false;
   const LinearPlan L = plan_linear(G, T, K, N, 0);
-  if (L.swap) return !L.pair && L.bn == 128 && GemmOut<128, true>::kStaged;
-  // token-row tiles: 256-feature tiles, whole 128-feature statistic parts
-  return L.bn == 256 && N % 128 == 0 && GemmOut<256, false>::kStaged;
+  // (token-row tiles at large T use the separate TMA-ring norm: measured
+  // faster there, XLNet N=32 B=4 4.39 vs 4.98 ms, BERT N=32 B=8 7.28 vs 8.09)
+  return L.swap && !L.pair && L.bn == 128 && GemmOut<128, true>::kStaged && N % 128 == 0;
 }
 
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
@@ -184,12 +118,13 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const void* pf_next, int64_t pf_bytes, const NormFold* fold) {
+                      const NormFold* fold) {
   // TMA needs 16-byte aligned row strides for x, w and y.
   if (out_dtype != NF_BF16 || K % 8 != 0 || N % 8 != 0) return NF_ERR_UNSUPPORTED;
   if (G > 65535 || T > (int64_t(1) << 30) || N > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
   if (ws && (reinterpret_cast<uintptr_t>(ws) & 255)) return NF_ERR_SHAPE;
   GemmParams p{};
+  p.act = act;
   p.bias = bias;
   p.residual = residual;
   p.out_gstride = y_gs;
@@ -197,8 +132,6 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.features = int(N);
   p.groups = int(G);
   p.y_direct = y;
-  p.pf_next = pf_next;
-  p.pf_bytes = pf_bytes;
   p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
   const LinearPlan L = plan_linear(G, T, K, N, ws ? ws_bytes : 0);
   if (fold) {
@@ -255,27 +188,24 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.counters = static_cast<unsigned*>(ws);
   p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
   if (L.pair) {
-    const int clusters = balanced_all() ? balanced_grid(p.units, kNumSMs / 2)
-                                        : (p.units < kNumSMs / 2 ? p.units : kNumSMs / 2);
+    const int clusters = p.units < kNumSMs / 2 ? p.units : kNumSMs / 2;
     const int grid = 2 * clusters;
-    return launch_tc_act<256, false, true>(act, ma, mb, my, mr, p, grid, stream);
+    return launch_tc_res<256, false, 0, true>(ma, mb, my, mr, p, grid, stream);
   }
   int grid = p.units < kNumSMs ? p.units : kNumSMs;
-  if (!swap && balanced_all()) grid = balanced_grid(p.units, kNumSMs);
-  if (swap && p.units > kNumSMs) {
-    // Balanced persistent grid: as many waves as one CTA per SM needs, but
-    // every CTA gets the same unit count (192 units: 96 CTAs x 2 instead of
-    // 44 x 2 + 104 x 1) and fewer CTAs start late behind the previous
-    // launch's SMs (BERT-base N=8 B=1: 0.641 -> 0.636 ms).
-    const int waves = (p.units + kNumSMs - 1) / kNumSMs;
-    grid = (p.units + waves - 1) / waves;
-    if (swap_grid_cap() > 0 && grid > swap_grid_cap()) grid = swap_grid_cap();
-  }
-#define NF_TC(BNV, SW) return launch_tc_act<BNV, SW>(act, ma, mb, my, mr, p, grid, stream)
-  if (swap && bn == 128 && kpt2_enabled() && K % 64 == 0 && N % 128 == 0 &&
+  // Swapped launches: a balanced persistent grid, as many waves as one CTA
+  // per SM needs but the same unit count per CTA (192 units: 96 CTAs x 2
+  // instead of 44 x 2 + 104 x 1; BERT-base N=8 B=1 0.641 -> 0.636 ms).
+  if (swap) grid = balanced_grid(p.units, kNumSMs);
+#define NF_TC(BNV, SW) return launch_tc_res<BNV, SW>(ma, mb, my, mr, p, grid, stream)
+  // Swapped 128-token tiles move two 64-wide k-blocks per TMA transaction:
+  // the batch-1 main loop is bound by a per-stage cost, not bytes
+  // (tools/gemm_trace.cu: 768->768 main loop 3.7 -> 2.9 us, 3072->768 split
+  // 5.1 -> 3.9 us). Three per stage measured slower (0.620 -> 0.639 ms).
+  if (swap && bn == 128 && K % 64 == 0 && N % 128 == 0 &&
       !(fold && fold->in_stats && fold->res_stats)) {
     CUtensorMap ma2, mb2, my2, mr2;
-    const int kpt = kpt_setting() >= 3 ? 3 : 2;
+    constexpr int kpt = 2;
     // output / residual tiles (128 tokens x 128 features) as one 4-D box:
     // (64, T, N/64, G) with a (64, 128, 2, 1) box, the staging buffer's layout
     if (make_bf16_map_kpt2(&ma2, w, G, N, K, kGemmBM, 0, 0, kpt) &&
@@ -283,8 +213,7 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
         make_bf16_map_kpt2(&my2, y, G, T, N, bn, y_ld, y_gs, 2) &&
         (!residual || make_bf16_map_kpt2(&mr2, residual, G, T, N, bn, y_ld, y_gs, 2))) {
       if (!residual) mr2 = my2;
-      return kpt == 3 ? launch_tc_kpt3(act, ma2, mb2, my2, mr2, p, grid, stream)
-                      : launch_tc_kpt2(act, ma2, mb2, my2, mr2, p, grid, stream);
+      return launch_tc_res<128, true, 0, false, 2>(ma2, mb2, my2, mr2, p, grid, stream);
     }
   }
   if (swap) {
@@ -296,57 +225,6 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   if (bn == 128) NF_TC(128, false);
   NF_TC(256, false);
 #undef NF_TC
-}
-
-}  // namespace nf
-
-namespace nf {
-
-// Merged Linear + residual + LayerNorm over the N output features (batch-1
-// encoders: T <= 128 tokens per instance, N <= 1024): swapped 128x128 tiles,
-// one cluster of N/128 CTAs per instance exchanging per-token partial sums
-// over DSMEM. y = LN(x W^T + bias + residual) with per-instance gamma/beta
-// (G, N). Replaces the merged graph's BatchMatMul -> Add -> GroupNorm chain
-// (reference batch_matmul engine.py:215-235, add 322-325, group_norm 263-284).
-int grouped_linear_ln_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                         const float* bias, const void* residual, const float* gamma,
-                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
-                         int64_t G, int64_t T, int64_t K, int64_t N, cudaStream_t stream) {
-  if (K % 8 || N % 8 || T < 1 || T > 128 || N > 8 * kGemmBM || !gamma || !beta)
-    return NF_ERR_UNSUPPORTED;
-  if (G > 65535) return NF_ERR_UNSUPPORTED;
-  GemmParams p{};
-  p.bias = bias;
-  p.residual = residual;
-  p.out_gstride = y_gs;
-  p.out_ld = y_ld;
-  p.features = int(N);
-  p.groups = int(G);
-  p.y_direct = y;
-  p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
-  p.ln_gamma = gamma;
-  p.ln_beta = beta;
-  p.ln_eps = eps;
-  p.ln_cluster = int((N + kGemmBM - 1) / kGemmBM);
-  CUtensorMap ma, mb, my, mr;
-  if (!make_bf16_map(&ma, w, G, N, K, kGemmBK, kGemmBM, 0, 0) ||
-      !make_bf16_map(&mb, x, G, T, K, kGemmBK, 128, x_ld, x_gs) ||
-      !make_bf16_map(&my, y, G, T, N, kOutBlock, 128, y_ld, y_gs))
-    return NF_ERR_UNSUPPORTED;
-  mr = my;
-  if (residual && !make_bf16_map(&mr, residual, G, T, N, kOutBlock, 128, y_ld, y_gs))
-    return NF_ERR_UNSUPPORTED;
-  p.rows_a = int(N);
-  p.rows_b = int(T);
-  p.tiles_a = p.ln_cluster;
-  p.tiles_b = 1;
-  p.splits = 1;
-  p.kb_per_split = p.kb_total;
-  p.units = int(G) * p.tiles_a;
-  const int grid = p.units;  // one unit per CTA: clusters are whole instances
-  if (residual)
-    return launch_tc<128, true, NF_ACT_NONE, true, 0, false, true>(ma, mb, my, mr, p, grid, stream);
-  return launch_tc<128, true, NF_ACT_NONE, false, 0, false, true>(ma, mb, my, my, p, grid, stream);
 }
 
 }  // namespace nf

@@ -88,6 +88,7 @@ __device__ unsigned long long g_gemm_wait[148 * 8];
 #endif
 
 struct GemmParams {
+  int act;               // fused epilogue activation (NF_ACT_*)
   const float* bias;     // (G, features) fp32 or nullptr
   const void* residual;  // y-shaped bf16 or nullptr
   int64_t out_gstride;   // elements between instances of y
@@ -105,20 +106,11 @@ struct GemmParams {
   int halo_w, halo_bytes;    // GATHER == 1: halo box width, bytes per buffer (1 KB aligned)
   int halo_cpp;              // channels per halo pixel (cg, or 8 for cg == 4: 16-byte boxes)
   uint32_t halo_tx;          // bytes one halo TMA box delivers
-  // LNF kernels: y = LayerNorm over the N output features of each token
-  // (one cluster of N/128 CTAs per instance), per-instance affine (G, N)
-  const float* ln_gamma;
-  const float* ln_beta;
-  float ln_eps;
-  int ln_cluster;
-  // next weight-streaming launch's weights: prefetched into L2 by the
-  // producer once this CTA's own loads are issued (null: none)
-  const void* pf_next;
-  int64_t pf_bytes;
   // Folded LayerNorms (swapped staged tiles): LN(v) over an instance's D
   // features per token is never materialised; its producer writes per-token
-  // partial sums (sum, sum of squares) for each of its 128-feature tiles,
-  // [g][part][token], and consumers rebuild the normalised value.
+  // statistics (sum, centred sum of squares M2) of each of its 128-feature
+  // tiles, [g][part][token], and consumers merge them (Chan et al.) and
+  // rebuild the normalised value.
   //  in : B operand (tokens) = LN(x); the weights carry gamma, the bias beta,
   //       colsum[g][n] = sum_k W'[g][n][k]:  y = rstd * (x W'^T - mean * colsum) + b'
   //  res: residual = LN(r) = (r - mean) * rstd * gamma[n] + beta[n]
@@ -142,15 +134,6 @@ inline int balanced_grid(int64_t units, int slots) {
   if (units <= slots) return int(units);
   const int64_t waves = (units + slots - 1) / slots;
   return int((units + waves - 1) / waves);
-}
-// NF_BALANCED_ALL=1: also for token-tile (tensor-bound) GEMMs and convs
-// (experiment knob, read once).
-inline bool balanced_all() {
-  static const bool on = [] {
-    const char* e = getenv("NF_BALANCED_ALL");
-    return e && e[0] == '1';
-  }();
-  return on;
 }
 
 #ifndef NF_RES_EARLY
@@ -207,7 +190,6 @@ struct GemmCfg {
   static constexpr int kBudgetKB =
       GATHER == 1 ? (NF_GEMM_HALO_KB > kMinKB ? NF_GEMM_HALO_KB : kMinKB)
       : GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
-      : KPT > 2 ? 226
       : KPT > 1 ? 225
       : BN >= 256 ? (PAIR ? 225 : 220)
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
@@ -223,7 +205,7 @@ struct GemmCfg {
   static constexpr int kResNormOff = KPT > 1 ? 0 : 2 * BN;
   static constexpr size_t kBytes =
       1024 + size_t(kStages) * kStageBytes + kOutBytes + 512 + kNormBytes;
-  static_assert(kStages >= (KPT > 2 ? 2 : 3), "pipeline too shallow");
+  static_assert(kStages >= 3, "pipeline too shallow");
   static_assert(kStages <= 32, "barrier array");
   static_assert(kTmemCols <= 512, "TMEM overflow");
 };
@@ -283,8 +265,7 @@ NF_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "me
 template <int N>
 NF_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER, bool PAIR, bool LNF = false,
-          int KPT = 1>
+template <int BN, bool SWAP, bool HAS_RES, int GATHER, bool PAIR, int KPT = 1>
 __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     k_grouped_gemm_tc(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
@@ -292,7 +273,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                       const __grid_constant__ CUtensorMap map_r, GemmParams p) {
   using C = GemmCfg<BN, SWAP, PAIR, GATHER, KPT>;
   constexpr int kStages = C::kStages;
-  static_assert(KPT == 1 || (SWAP && !PAIR && !GATHER && !LNF), "multi-k-block stages");
+  static_assert(KPT == 1 || (KPT == 2 && SWAP && !PAIR && !GATHER), "multi-k-block stages");
   static_assert(!(PAIR && GATHER), "CTA pairs take TMA operands only");
   constexpr int kRowsA = PAIR ? 2 * kGemmBM : kGemmBM;  // A rows per unit
   constexpr int kEpiWarps = epi_warps<BN>();
@@ -317,15 +298,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
   uint64_t* hbar = rbar + 1;  // [2] halo buffers (GATHER == 1)
-  uint64_t* lnbar = hbar + 2;  // LNF: cluster partial-sum arrivals
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lnbar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hbar + 2);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
   float* sNorm = reinterpret_cast<float*>(sOut + C::kOutBytes + 512);  // C::kNormBytes
-  constexpr bool kFold = C::kNormBytes > 0 && !LNF;
-  // token-row tiles (large T): each epilogue thread owns one token and 128
-  // feature columns, so the folded-LN terms live in registers
-  constexpr bool kFoldN = !SWAP && C::kStaged && BN == 256 && !GATHER && !LNF;
-  static_assert(!kFoldN || kColsPerThread == 128, "one 128-feature part per thread");
+  constexpr bool kFold = C::kNormBytes > 0;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -344,7 +320,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     mbar_init(rbar, 1);
     mbar_init(&hbar[0], 1);
     mbar_init(&hbar[1], 1);
-    mbar_init(lnbar, LNF ? p.ln_cluster : 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], GATHER ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
@@ -361,7 +336,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (PAIR || LNF) cluster_sync();  // peers signal our barriers after this
+  if constexpr (PAIR) cluster_sync();  // the peer signals our barriers after this
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) NF_TRACE(1);
@@ -445,7 +420,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         }
         pre = 0;
       }
-      prefetch_share_l2(p.pf_next, p.pf_bytes);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16_f32(kRowsA, BN);
@@ -501,154 +475,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       __syncwarp();
     }
     if (lane == 0) NF_TRACE(3);
-  } else if (LNF && warp < 2 + kEpiWarps) {
-    // ------------- epilogue + LayerNorm over a cluster's features -------------
-    // Swapped tile (thread = feature row, columns = tokens), one unit per CTA;
-    // the cluster's CL CTAs hold the CL*128 features of one instance. Pass 1:
-    // v = acc + bias + residual, per-token sum / sum of squares over this
-    // CTA's features (warp transpose-reduce + smem); partials go to every
-    // cluster CTA through DSMEM; pass 2 re-reads TMEM and writes
-    // gamma * (v - mean) * rstd + beta.
-    static_assert(!LNF || (SWAP && BN == 128 && !PAIR && GATHER == 0), "LN epilogue config");
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const int etid = threadIdx.x - 64;
-    const int col0 = ((warp - 2) >> 2) * kColsPerThread;  // 64 tokens per thread
-    const uint32_t stage_base = smem_u32(sOut);
-    float* sred = reinterpret_cast<float*>(sOut + C::kOutBytes + 1024);  // [4][128][2]
-    float2* sclu = reinterpret_cast<float2*>(sred + 4 * 128 * 2);      // [8][128]
-    float2* sstat = sclu + 8 * 128;                                      // [128]
-    const uint32_t crank = cluster_ctarank();
-    const int CL = p.ln_cluster;
-    const UnitCoord c = decode_unit(p, blockIdx.x, true);
-    mbar_wait(&tfull[0], 0);
-    tc_fence_after();
-    if (etid == 0) NF_TRACE(4);
-    const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16);
-    const int m0 = c.ta * kGemmBM;
-    const int feat = m0 + row;
-    const bool fok = feat < p.rows_a;
-    const int64_t fidx = int64_t(c.g) * p.features + feat;
-    const float bf = (p.bias && fok) ? __ldg(p.bias + fidx) : 0.f;
-    // The residual tile arrives by TMA in the output staging layout (the same
-    // smem the result is staged in); per-element global loads here would
-    // serialise on L2 latency.
-    if constexpr (HAS_RES) {
-      if (etid == 0) {
-        mbar_arrive_expect_tx(rbar, C::kOutBytes);
-#pragma unroll
-        for (int b = 0; b < kGemmBM / kOutBlock; ++b)
-          tma_load_3d(sOut + b * BN * 128, &map_r, rbar, m0 + b * kOutBlock, 0, c.g, kEvictFirst);
-      }
-      mbar_wait(rbar, 0);
-    }
-    auto load_v = [&](int cc, float (&v)[32]) {
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(t_row + uint32_t(cc), r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float x = __uint_as_float(r[j]) + bf;
-        if constexpr (HAS_RES) {
-          uint16_t h;
-          asm volatile("ld.shared.u16 %0, [%1];"
-                       : "=h"(h)
-                       : "r"(stage_base + stage_offset(cc + j, row, BN)));
-          x += __uint_as_float(uint32_t(h) << 16);
-        }
-        v[j] = fok ? x : 0.f;
-      }
-    };
-#pragma unroll 1
-    for (int cc = col0; cc < col0 + kColsPerThread; cc += 32) {
-      float s1[32], s2[32];
-      load_v(cc, s1);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) s2[j] = s1[j] * s1[j];
-      // transpose-reduce: lane l ends with the warp's sums for token cc + l
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const bool upper = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-          const float a1 = upper ? s1[i] : s1[i + o], k1 = upper ? s1[i + o] : s1[i];
-          const float a2 = upper ? s2[i] : s2[i + o], k2 = upper ? s2[i + o] : s2[i];
-          s1[i] = k1 + __shfl_xor_sync(0xffffffffu, a1, o);
-          s2[i] = k2 + __shfl_xor_sync(0xffffffffu, a2, o);
-        }
-      }
-      sred[(quarter * 128 + cc + lane) * 2] = s1[0];
-      sred[(quarter * 128 + cc + lane) * 2 + 1] = s2[0];
-    }
-    named_bar_sync(1, kEpiThreads);
-    if (etid < 128) {
-      const int t = etid;
-      float cs = 0.f, cq = 0.f;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        cs += sred[(q * 128 + t) * 2];
-        cq += sred[(q * 128 + t) * 2 + 1];
-      }
-      for (int r = 0; r < CL; ++r) st_cluster_f2(&sclu[crank * 128 + t], uint32_t(r), cs, cq);
-    }
-    named_bar_sync(1, kEpiThreads);
-    if (etid == 0) {
-      fence_acq_rel_cluster();
-      for (int r = 0; r < CL; ++r) mbar_arrive_remote(lnbar, uint32_t(r));
-    }
-    if (etid == 0) NF_TRACE(2);
-    mbar_wait_cluster(lnbar, 0);
-    if (etid == 0) NF_TRACE(7);
-    if (etid < 128) {
-      const int t = etid;
-      float ts = 0.f, tq = 0.f;
-      for (int r = 0; r < CL; ++r) {
-        const float2 pr = sclu[r * 128 + t];
-        ts += pr.x;
-        tq += pr.y;
-      }
-      const float inv_n = 1.0f / float(p.rows_a);
-      const float mean = ts * inv_n;
-      const float var = fmaxf(fmaf(-mean, mean, tq * inv_n), 0.f);
-      sstat[t] = make_float2(mean, rsqrtf(var + p.ln_eps));
-    }
-    named_bar_sync(1, kEpiThreads);
-    const float gf = fok ? __ldg(p.ln_gamma + fidx) : 0.f;
-    const float btf = fok ? __ldg(p.ln_beta + fidx) : 0.f;
-#pragma unroll 1
-    for (int cc = col0; cc < col0 + kColsPerThread; cc += 32) {
-      float v[32];
-      load_v(cc, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float2 st = sstat[cc + j];
-        v[j] = fmaf((v[j] - st.x) * st.y, gf, btf);
-      }
-      __syncwarp();  // partner lanes read their residuals before the pair stores
-      const bool odd = lane & 1;
-      const int feven = row & ~1;
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float send = odd ? v[j] : v[j + 1];
-        const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-        const uint32_t packed = odd ? pack_bf16x2(recv, v[j + 1]) : pack_bf16x2(v[j], recv);
-        const int t = cc + j + (odd ? 1 : 0);
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage_base + stage_offset(t, feven, BN)),
-                     "r"(packed)
-                     : "memory");
-      }
-    }
-    tc_fence_before();
-    fence_proxy_async_smem();
-    named_bar_sync(1, kEpiThreads);
-    if (etid == 0) {
-#pragma unroll
-      for (int b = 0; b < kGemmBM / kOutBlock; ++b)
-        tma_store_3d(&map_y, sOut + b * BN * 128, m0 + b * kOutBlock, 0, c.g);
-      bulk_commit();
-      bulk_wait0();
-      NF_TRACE(5);
-    }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------ epilogue ------------------------------
     const int quarter = warp & 3;         // TMEM lane quarter this warp may access
@@ -673,9 +499,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         mbar_arrive(&tempty[acc]);
       }
     };
-    const bool fold_in = (kFold || kFoldN) && p.nin_stats != nullptr;
-    const bool fold_res = (kFold || kFoldN) && kResTma && p.nres_stats != nullptr;
-    const bool fold_out = kFoldN && p.nout_stats != nullptr;
+    const bool fold_in = kFold && p.nin_stats != nullptr;
+    const bool fold_res = kFold && kResTma && p.nres_stats != nullptr;
     for (int u = ubase; u < p.units; u += ustride, ++local) {
       const UnitCoord c = decode_unit(p, u, SWAP);
       const int acc = local & 1;
@@ -726,20 +551,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           named_bar_sync(1, kEpiThreads);
         }
       }
-      // token-row tiles: this thread's token's LN statistics, loaded ahead
-      float2 nin = make_float2(0.f, 1.f), nres = make_float2(0.f, 1.f);
-      if constexpr (kFoldN) {
-        const int tok = c.ta * kRowsA + int(rank) * kGemmBM + row;
-        if (tok < p.rows_a) {
-          if (fold_in)
-            nin = fold_stats(p.nin_stats, p.nin_parts, p.rows_a, c.g, tok, p.nin_inv_d,
-                             p.nin_eps);
-          if (fold_res)
-            nres = fold_stats(p.nres_stats, p.nres_parts, p.rows_a, c.g, tok, p.nres_inv_d,
-                              p.nres_eps);
-        }
-      }
-      float osum = 0.f, osq = 0.f;  // fold_out: this thread's part of its token's sums
       // swapped tiles: this thread's feature row constants, loaded ahead too
       float hb = 0.f, hcs = 0.f, hgm = 0.f, hbt = 0.f;
       if constexpr (SWAP) {
@@ -835,21 +646,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           // Thread = token row; EC consecutive features n0+cc ...
           const int tok = m0 + row;
           const int f0 = n0 + cc;
-          const int64_t gf = int64_t(c.g) * p.features + f0;
-          if constexpr (kFoldN) {
-            if (fold_in) {  // rstd * (acc - mean * colsum); folded parts have whole 128 blocks
-#pragma unroll
-              for (int j = 0; j < EC; j += 4) {
-                const float4 c4 = f0 + j < p.rows_b
-                                      ? __ldg(reinterpret_cast<const float4*>(p.nin_colsum + gf + j))
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-                v[j] = nin.y * fmaf(-nin.x, c4.x, v[j]);
-                v[j + 1] = nin.y * fmaf(-nin.x, c4.y, v[j + 1]);
-                v[j + 2] = nin.y * fmaf(-nin.x, c4.z, v[j + 2]);
-                v[j + 3] = nin.y * fmaf(-nin.x, c4.w, v[j + 3]);
-              }
-            }
-          }
           if (bias) {
             if (f0 + EC <= p.rows_b) {
 #pragma unroll
@@ -876,18 +672,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                 r8[2 * e] = __uint_as_float(w4[e] << 16);
                 r8[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
               }
-              if constexpr (kFoldN) {
-                if (fold_res && f0 + 8 * q < p.rows_b) {  // LN(r) = (r - mean) * rstd * g + b
-                  const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.nres_gamma + gf + 8 * q));
-                  const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.nres_gamma + gf + 8 * q + 4));
-                  const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.nres_beta + gf + 8 * q));
-                  const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.nres_beta + gf + 8 * q + 4));
-                  const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-                  const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) r8[e] = fmaf((r8[e] - nres.x) * nres.y, gg[e], bb[e]);
-                }
-              }
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[8 * q + e] += r8[e];
             }
@@ -903,8 +687,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                 v[4 * q + 3] += __uint_as_float(u2.y & 0xffff0000u);
               }
           }
-#pragma unroll
-          for (int j = 0; j < EC; ++j) v[j] = act_t<ACT>(v[j]);
+          apply_act<GATHER != 0>(p.act, v);
           if constexpr (C::kStaged) {
 #pragma unroll
             for (int q = 0; q < EC / 8; ++q) {
@@ -913,18 +696,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
               const uint32_t w2 = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
               const uint32_t w3 = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
               st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM), w0, w1, w2, w3);
-              if constexpr (kFoldN) {
-                if (fold_out) {  // LN sums of the stored (bf16) values
-                  const uint32_t ww[4] = {w0, w1, w2, w3};
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float lo = __uint_as_float(ww[e] << 16);
-                    const float hi = __uint_as_float(ww[e] & 0xffff0000u);
-                    osum += lo + hi;
-                    osq = fmaf(lo, lo, fmaf(hi, hi, osq));
-                  }
-                }
-              }
             }
           } else if (tok < p.rows_a) {
             // Narrow tiles (grouped convs with 4..32 channels per group):
@@ -981,8 +752,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
               }
               v[j] += r;
             }
-            v[j] = act_t<ACT>(v[j]);
           }
+          apply_act<GATHER != 0>(p.act, v);
           if constexpr (kResTma) __syncwarp();  // partner lanes read before the pair stores
           const bool odd = lane & 1;
           const int feven = row & ~1;
@@ -1010,13 +781,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           }
         }
       }
-      if constexpr (kFoldN) {
-        // this thread's 128 columns are one whole part of its token's sums
-        const int tok = m0 + row, f = n0 + col0;
-        if (fold_out && tok < p.rows_a && f < p.rows_b)
-          __stcg(p.nout_stats + (int64_t(c.g) * (p.features >> 7) + (f >> 7)) * p.rows_a + tok,
-                 make_float2(osum, osq));
-      }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       release_acc(acc);
       if constexpr (C::kStaged) {
@@ -1039,43 +803,46 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         }
         if constexpr (kFold) {
           if (p.nout_stats) {
-            // Partial LN sums of token t over this tile's 128 features, from
-            // the bf16 values just staged (what the consumer will read). Lane
-            // pair (2t, 2t+1) takes token t's two 64-feature blocks; the
-            // swizzle spreads each 16-byte chunk read over all banks.
+            // LN statistics of token t over this tile's 128 features, from the
+            // bf16 values just staged (what the consumer will read): the sum,
+            // then the centred sum of squares about this part's mean (second
+            // pass over smem). Lane pair (2t, 2t+1) takes token t's two
+            // 64-feature blocks; the swizzle spreads each 16-byte chunk read
+            // over all banks.
             constexpr int kBlocks = kGemmBM / kOutBlock;  // 2
             constexpr int kPerTok = kEpiThreads / BN;      // threads per token
             static_assert(kPerTok == 1 || kPerTok == kBlocks, "stats split");
             const int t = kPerTok == 1 ? etid : etid >> 1;
-            float s = 0.f, ss = 0.f;
-            if (t < BN) {
+            auto stat_pass = [&](float mean, bool centred) {
+              float acc = 0.f;
+              if (t < BN) {
 #pragma unroll
-              for (int bb = 0; bb < kBlocks / kPerTok; ++bb) {
-                const int b = kPerTok == 1 ? bb : (etid & 1);
+                for (int bb = 0; bb < kBlocks / kPerTok; ++bb) {
+                  const int b = kPerTok == 1 ? bb : (etid & 1);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  uint32_t w4[4];
-                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                               : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
-                               : "r"(stage_base + uint32_t(b * BN * 128 + t * 128) +
-                                     (uint32_t(q ^ (t & 7)) << 4)));
+                  for (int q = 0; q < 8; ++q) {
+                    uint32_t w4[4];
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
+                                 : "r"(stage_base + uint32_t(b * BN * 128 + t * 128) +
+                                       (uint32_t(q ^ (t & 7)) << 4)));
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float lo = __uint_as_float(w4[e] << 16);
-                    const float hi = __uint_as_float(w4[e] & 0xffff0000u);
-                    s += lo + hi;
-                    ss = fmaf(lo, lo, fmaf(hi, hi, ss));
+                    for (int e = 0; e < 4; ++e) {
+                      const float lo = __uint_as_float(w4[e] << 16) - mean;
+                      const float hi = __uint_as_float(w4[e] & 0xffff0000u) - mean;
+                      acc = centred ? fmaf(lo, lo, fmaf(hi, hi, acc)) : acc + (lo + hi);
+                    }
                   }
                 }
               }
-            }
-            if constexpr (kPerTok > 1) {
-              s += __shfl_xor_sync(0xffffffffu, s, 1);
-              ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-            }
+              if constexpr (kPerTok > 1) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+              return acc;
+            };
+            const float s = stat_pass(0.f, false);
+            const float m2 = stat_pass(s * (1.0f / float(kGemmBM)), true);
             if (t < BN && (kPerTok == 1 || (etid & 1) == 0) && n0 + t < p.rows_b)
               __stcg(p.nout_stats + (int64_t(c.g) * p.tiles_a + c.ta) * p.rows_b + n0 + t,
-                     make_float2(s, ss));
+                     make_float2(s, m2));
           }
         }
         if (etid == 0) bulk_wait_read0();  // staging reusable
@@ -1298,94 +1065,41 @@ inline EncodeTiledFn encode_fn() {
 bool make_bf16_map(CUtensorMap* map, const void* base, int64_t G, int64_t rows, int64_t inner,
                    int box_inner, int box_rows, int64_t row_stride, int64_t g_stride);
 
-template <int BN, bool SWAP, int ACT, bool HAS_RES, int GATHER = 0, bool PAIR = false,
-          bool LNF = false, int KPT = 1>
+template <int BN, bool SWAP, bool HAS_RES, int GATHER = 0, bool PAIR = false, int KPT = 1>
 static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
   using C = GemmCfg<BN, SWAP, PAIR, GATHER, KPT>;
-  auto kern = k_grouped_gemm_tc<BN, SWAP, ACT, HAS_RES, GATHER, PAIR, LNF, KPT>;
-  static bool attr_done = false;  // idempotent attribute set; benign race
-  if (!attr_done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (GATHER == 1 || LNF) ? 232448 : int(C::kBytes));
-    attr_done = true;
-  }
+  auto kern = k_grouped_gemm_tc<BN, SWAP, HAS_RES, GATHER, PAIR, KPT>;
+  static SmemAttrOnce smem_attr;  // one per kernel instantiation, a bit per device
+  smem_attr.set(kern, GATHER == 1 ? 232448 : int(C::kBytes));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(gemm_threads<BN, GATHER>());
-  cfg.dynamicSmemBytes = C::kBytes + (GATHER == 1 ? 1024 + 2 * size_t(p.halo_bytes) : 0) +
-                         (LNF ? 1024 + 16 * 1024 : 0);
+  cfg.dynamicSmemBytes = C::kBytes + (GATHER == 1 ? 1024 + 2 * size_t(p.halo_bytes) : 0);
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  int na = 0;
-  if (pdl_enabled()) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  if (PAIR) {
+    la[1].id = cudaLaunchAttributeClusterDimension;
+    la[1].val.clusterDim.x = 2;
+    la[1].val.clusterDim.y = 1;
+    la[1].val.clusterDim.z = 1;
   }
-  if (PAIR || LNF) {
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = PAIR ? 2 : p.ln_cluster;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = na;
+  cfg.attrs = la;
+  cfg.numAttrs = PAIR ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, mr, p);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 
-template <int BN, bool SWAP, int ACT, int GATHER = 0, bool PAIR = false>
+// Residual / no-residual instantiation (the activation is a kernel argument).
+template <int BN, bool SWAP, int GATHER = 0, bool PAIR = false, int KPT = 1>
 static int launch_tc_res(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& my,
                          const CUtensorMap& mr, const GemmParams& p, int grid,
                          cudaStream_t stream) {
   if (p.residual)
-    return launch_tc<BN, SWAP, ACT, true, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
-  return launch_tc<BN, SWAP, ACT, false, GATHER, PAIR>(ma, mb, my, mr, p, grid, stream);
-}
-
-// Swapped 128-token tiles with KPT k-blocks per TMA box (4-D maps).
-template <int ACT, int KPT>
-static int launch_tc_kpt_res(const CUtensorMap& ma, const CUtensorMap& mb,
-                             const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
-                             int grid, cudaStream_t stream) {
-  if (p.residual)
-    return launch_tc<128, true, ACT, true, 0, false, false, KPT>(ma, mb, my, mr, p, grid, stream);
-  return launch_tc<128, true, ACT, false, 0, false, false, KPT>(ma, mb, my, mr, p, grid, stream);
-}
-template <int KPT>
-inline int launch_tc_kpt(int act, const CUtensorMap& ma, const CUtensorMap& mb,
-                         const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
-                         int grid, cudaStream_t stream) {
-  switch (act) {
-    case NF_ACT_RELU: return launch_tc_kpt_res<NF_ACT_RELU, KPT>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_GELU: return launch_tc_kpt_res<NF_ACT_GELU, KPT>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_TANH: return launch_tc_kpt_res<NF_ACT_TANH, KPT>(ma, mb, my, mr, p, grid, stream);
-    default: return launch_tc_kpt_res<NF_ACT_NONE, KPT>(ma, mb, my, mr, p, grid, stream);
-  }
-}
-inline int launch_tc_kpt2(int act, const CUtensorMap& ma, const CUtensorMap& mb,
-                          const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
-                          int grid, cudaStream_t stream) {
-  return launch_tc_kpt<2>(act, ma, mb, my, mr, p, grid, stream);
-}
-inline int launch_tc_kpt3(int act, const CUtensorMap& ma, const CUtensorMap& mb,
-                          const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
-                          int grid, cudaStream_t stream) {
-  return launch_tc_kpt<3>(act, ma, mb, my, mr, p, grid, stream);
-}
-
-template <int BN, bool SWAP, bool PAIR = false>
-static int launch_tc_act(int act, const CUtensorMap& ma, const CUtensorMap& mb,
-                         const CUtensorMap& my, const CUtensorMap& mr, const GemmParams& p,
-                         int grid, cudaStream_t stream) {
-  switch (act) {
-    case NF_ACT_RELU: return launch_tc_res<BN, SWAP, NF_ACT_RELU, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_GELU: return launch_tc_res<BN, SWAP, NF_ACT_GELU, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
-    case NF_ACT_TANH: return launch_tc_res<BN, SWAP, NF_ACT_TANH, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
-    default: return launch_tc_res<BN, SWAP, NF_ACT_NONE, 0, PAIR>(ma, mb, my, mr, p, grid, stream);
-  }
+    return launch_tc<BN, SWAP, true, GATHER, PAIR, KPT>(ma, mb, my, mr, p, grid, stream);
+  return launch_tc<BN, SWAP, false, GATHER, PAIR, KPT>(ma, mb, my, mr, p, grid, stream);
 }
 
 }  // namespace nf

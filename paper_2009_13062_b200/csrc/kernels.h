@@ -8,7 +8,8 @@
 namespace nf {
 
 // Folded LayerNorm operands of a batch-1 GEMM (see GemmParams::nin_*):
-// stats are [g][part][token] (sum, sum of squares) float pairs.
+// stats are [g][part][token] (sum, centred sum of squares M2) float pairs
+// over the part's 128 features.
 struct NormFold {
   const float* in_stats;
   const float* in_colsum;
@@ -28,13 +29,8 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const void* pf_next = nullptr, int64_t pf_bytes = 0,
                       const NormFold* fold = nullptr);
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
-int grouped_linear_ln_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                         const float* bias, const void* residual, const float* gamma,
-                         const float* beta, float eps, void* y, int64_t y_ld, int64_t y_gs,
-                         int64_t G, int64_t T, int64_t K, int64_t N, cudaStream_t stream);
 
 // linear_simt.cu — CUDA-core grouped linear (exact reference order or FMA).
 int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
@@ -68,8 +64,6 @@ int conv2d_simt(const void* x, const void* w, const float* bias, const float* sc
                 int stride, int pad, int groups, int relu, int dtype, int exact,
                 cudaStream_t s);
 
-int l2_prefetch(const void* ptr, int64_t bytes, cudaStream_t s);
-
 // conv_igemm.cu — implicit-GEMM conv (tcgen05, cp.async im2col gather).
 int grouped_conv_tc(const void* x, const void* w, const float* bias, const void* residual,
                     void* y, int N, int H, int W, int C, int Cout, int G, int k, int stride,
@@ -89,8 +83,7 @@ int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int 
 // qkv_attention.cu — fused QKV projection + attention, batch 1, S = 128.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream, const void* pf_next = nullptr, int64_t pf_bytes = 0,
-                     const NormFold* fold = nullptr);
+                     cudaStream_t stream, const NormFold* fold = nullptr);
 
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,

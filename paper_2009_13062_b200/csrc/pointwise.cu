@@ -405,9 +405,10 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2)
     }
     const int64_t aff = aff_of(u);
     if (aff != aff_cur) load_affine(aff);
-    // one pass: sum and sum of squares (fp32; |x| ~ O(1) activations)
+    // two passes over the registers: mean, then the centred sum of squares
+    // (no E[x^2] - mean^2 cancellation when |mean| >> std)
     float v[Q * V];
-    float sum = 0.f, sq = 0.f;
+    float sum = 0.f;
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       if (lane + 32 * q < nchunks) {
@@ -424,18 +425,20 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2)
           v[q * V + 2 * e] = t.x;
           v[q * V + 2 * e + 1] = t.y;
           sum += t.x + t.y;
-          sq = fmaf(t.x, t.x, fmaf(t.y, t.y, sq));
         }
       }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    }
     const float inv_c = 1.0f / float(Cg);
-    const float mean = sum * inv_c;
-    const float var = fmaxf(fmaf(-mean, mean, sq * inv_c), 0.f);
-    const float rstd = rsqrtf(var + g.eps);
+    const float mean = warp_sum(sum) * inv_c;
+    float sq = 0.f;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (lane + 32 * q < nchunks)
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          const float d = v[q * V + e] - mean;
+          sq = fmaf(d, d, sq);
+        }
+    const float rstd = rsqrtf(warp_sum(sq) * inv_c + g.eps);
     const int64_t b = base_of(u);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -477,13 +480,10 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     const int q = int((g.Cg / 8 + 31) / 32);
     if (vec && q <= 3 && units >= 4 * 148 * 16) {
       // enough rows for each warp of 2 resident blocks per SM to stream several
-      static bool attr_done = false;
-      if (!attr_done) {
-        cudaFuncSetAttribute(k_group_norm_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNormTmaSmem));
-        cudaFuncSetAttribute(k_group_norm_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNormTmaSmem));
-        cudaFuncSetAttribute(k_group_norm_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNormTmaSmem));
-        attr_done = true;
-      }
+      static SmemAttrOnce attr1, attr2, attr3;
+      attr1.set(k_group_norm_tma<1>, int(kNormTmaSmem));
+      attr2.set(k_group_norm_tma<2>, int(kNormTmaSmem));
+      attr3.set(k_group_norm_tma<3>, int(kNormTmaSmem));
       const int warps = 148 * 2 * kNormWarps;
       const int per = int((units + warps - 1) / warps);
       const int nw = int((units + per - 1) / per);
@@ -494,7 +494,6 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     } else if (vec && q == 1) launch_pdl(k_group_norm_vec<__nv_bfloat16, 1>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else if (vec && q == 2) launch_pdl(k_group_norm_vec<__nv_bfloat16, 2>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else if (vec && q == 3) launch_pdl(k_group_norm_vec<__nv_bfloat16, 3>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
-    else if (vec) launch_pdl(k_group_norm_vec<__nv_bfloat16, 4>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else launch_pdl(k_group_norm<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else if (dtype == NF_F32) {
     const bool vec = small && g.sc == 1 && g.Cg % 4 == 0 && g.Cg <= 4 * 32 * (kNormCache / 4) &&
@@ -505,7 +504,6 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     const int q = int((g.Cg / 4 + 31) / 32);
     if (vec && q == 1) launch_pdl(k_group_norm_vec<float, 1>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else if (vec && q <= 4) launch_pdl(k_group_norm_vec<float, 4>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
-    else if (vec) launch_pdl(k_group_norm_vec<float, 8>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
     else launch_pdl(k_group_norm<float>, dim3(grid), dim3(256), 0, s, px, pr, gamma, beta, py, g);
   } else {
     return NF_ERR_UNSUPPORTED;
@@ -663,41 +661,6 @@ int pool2d(const void* x, void* y, int64_t N, int64_t C, int H, int W, int kind,
   else if (dtype == NF_BF16) NF_POOL(__nv_bfloat16);
   else return NF_ERR_UNSUPPORTED;
 #undef NF_POOL
-  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
-}
-
-// ---------------------------------------------------------------------------
-// L2 prefetch of a byte range (the next GEMM's weights): fire-and-forget
-// cp.async.bulk.prefetch.L2 in 16 KB pieces spread over the grid. The kernel
-// lets its successor launch immediately, and only then waits for its own
-// predecessor, so stream dependencies still chain through it.
-// ---------------------------------------------------------------------------
-constexpr int64_t kPrefetchPiece = 16 * 1024;
-
-__global__ void k_l2_prefetch(const uint8_t* __restrict__ base, int64_t bytes) {
-  grid_dependents_launch();
-  const int64_t pieces = (bytes + kPrefetchPiece - 1) / kPrefetchPiece;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < pieces;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t off = i * kPrefetchPiece;
-    int64_t len = bytes - off < kPrefetchPiece ? bytes - off : kPrefetchPiece;
-    len &= ~int64_t(15);
-    if (len > 0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off),
-                   "r"(uint32_t(len))
-                   : "memory");
-  }
-  grid_dependency_wait();
-}
-
-int l2_prefetch(const void* ptr, int64_t bytes, cudaStream_t s) {
-  if (!ptr || bytes <= 0) return NF_OK;
-  if (reinterpret_cast<uintptr_t>(ptr) & 15) return NF_ERR_SHAPE;
-  const int64_t pieces = (bytes + kPrefetchPiece - 1) / kPrefetchPiece;
-  int64_t blocks = (pieces + 63) / 64;
-  if (blocks > kNumSMs) blocks = kNumSMs;
-  launch_pdl(k_l2_prefetch, dim3(unsigned(blocks)), dim3(64), 0, s,
-             static_cast<const uint8_t*>(ptr), bytes);
   return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(192, 1)
     k_qkv_attention_tc(const __grid_constant__ CUtensorMap map_x,
                        const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
                        __nv_bfloat16* __restrict__ out, int H, int kb_total, float scale_log2,
-                       const void* pf_next, int64_t pf_bytes, const float2* nin_stats,
+                       const float2* nin_stats,
                        const float* nin_colsum, int nin_parts, float nin_eps) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -114,7 +114,6 @@ __global__ void __launch_bounds__(192, 1)
         load_w(stage, st);
         load_x(stage, st);
       }
-      prefetch_share_l2(pf_next, pf_bytes);  // the next launch's weights into L2
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = make_idesc_bf16_f32(128, 3 * kQD);
@@ -297,8 +296,7 @@ __global__ void __launch_bounds__(192, 1)
 // null; out (G, 128, D) bf16 context. heads * 64 == D.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream, const void* pf_next, int64_t pf_bytes,
-                     const NormFold* fold) {
+                     cudaStream_t stream, const NormFold* fold) {
   if (G < 1 || heads < 1 || D != heads * kQD) return NF_ERR_SHAPE;
   const float2* nin = fold ? reinterpret_cast<const float2*>(fold->in_stats) : nullptr;
   if (nin && (!fold->in_colsum || fold->in_parts < 1)) return NF_ERR_SHAPE;
@@ -307,16 +305,12 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
   if (!make_bf16_map_kpt2(&mx, x, G, S, D, kQS, x_ld, x_gs, kQKPT) ||
       !make_bf16_map_kpt2(&mw, w, G, 3 * D, D, 3 * kQD, 0, 0, kQKPT))
     return NF_ERR_UNSUPPORTED;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_qkv_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kQSmem));
-    attr_done = true;
-  }
+  static SmemAttrOnce smem_attr;
+  smem_attr.set(k_qkv_attention_tc, int(kQSmem));
   const float sl2 = scale * 1.4426950408889634f;
   cudaError_t e = launch_pdl(k_qkv_attention_tc, dim3(unsigned(G * heads)), dim3(192), kQSmem,
                              stream, mx, mw, bias, static_cast<__nv_bfloat16*>(out), int(heads),
-                             int(D / 64), sl2, pf_next, pf_bytes, nin,
+                             int(D / 64), sl2, nin,
                              nin ? fold->in_colsum : nullptr, nin ? fold->in_parts : 0,
                              nin ? fold->in_eps : 0.f);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;

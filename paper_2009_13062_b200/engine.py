@@ -26,6 +26,7 @@ accumulation order, f32).
 from __future__ import annotations
 
 import math
+import threading
 import time
 from dataclasses import dataclass, field
 from typing import Callable
@@ -53,15 +54,8 @@ _ACT_OF = {OpKind.RELU: _lib.NF_ACT_RELU, OpKind.GELU: _lib.NF_ACT_GELU,
 _EW_OF = {OpKind.ADD: _lib.NF_EW_ADD, OpKind.MUL: _lib.NF_EW_MUL, OpKind.RELU: _lib.NF_EW_RELU,
           OpKind.TANH: _lib.NF_EW_TANH, OpKind.GELU: _lib.NF_EW_GELU}
 _MODES = {"fast": _lib.NF_MODE_FAST, "exact": _lib.NF_MODE_EXACT}
-# Channels per densified super-group for narrow grouped convs (ResNeXt);
-# NF_SUPER_GROUP overrides (A/B knob).
-_SUPER_GROUP = int(__import__("os").environ.get("NF_SUPER_GROUP", "64"))
-_FUSE_LN = __import__("os").environ.get("NF_FUSE_LN", "0") == "1"
-_L2_PF = __import__("os").environ.get("NF_L2_PF", "0") == "1"  # measured slower (opt-in)
-# Batch-1 LayerNorms folded into their producing / consuming GEMMs (no norm
-# launch; see include/netfuse_b200.h "Folded LayerNorm"). NF_FOLD_LN=0 keeps
-# the separate norm kernel.
-_FOLD_LN = __import__("os").environ.get("NF_FOLD_LN", "1") != "0"
+# Channels per densified super-group for narrow grouped convs (ResNeXt).
+_SUPER_GROUP = 64
 
 
 class _LinearStep:
@@ -69,11 +63,11 @@ class _LinearStep:
     and folded-LayerNorm operands to it (it is emitted before the norm that
     absorbs its output is seen)."""
 
-    def __init__(self, x, k, w, b, y, n, groups, rows, dcode, layout, act, mcode, ws, wsb, pf,
+    def __init__(self, x, k, w, b, y, n, groups, rows, dcode, layout, act, mcode, ws, wsb,
                  fold_ok):
         self.x, self.k, self.w, self.b, self.y, self.n = x, k, w, b, y, n
         self.groups, self.rows, self.dcode, self.layout = groups, rows, dcode, layout
-        self.act, self.mcode, self.ws, self.wsb, self.pf = act, mcode, ws, wsb, pf
+        self.act, self.mcode, self.ws, self.wsb = act, mcode, ws, wsb
         self.fold_ok = fold_ok
         self.residual = None
         self.fin = None   # (stats, parts, colsum, eps)
@@ -83,9 +77,9 @@ class _LinearStep:
     def __call__(self, st):
         k, n, rows = self.k, self.n, self.rows
         if self.fin is None and self.fres is None and self.out_stats is None:
-            _lib.call("nf_grouped_linear_ex", self.x, k, rows * k, self.w, self.b, self.residual,
+            _lib.call("nf_grouped_linear_ws", self.x, k, rows * k, self.w, self.b, self.residual,
                       self.y, n, rows * n, self.groups, rows, k, n, self.dcode, self.layout,
-                      self.act, self.mcode, self.ws, self.wsb, *self.pf, st)
+                      self.act, self.mcode, self.ws, self.wsb, st)
             return
         fin = self.fin or (None, 0, None, 0.0)
         fres = self.fres or (None, 0, None, None, 0.0)
@@ -181,7 +175,7 @@ class Plan:
 
     def __init__(self, graph: Graph, weights: WeightStore, *, mode: str = "fast",
                  device: str | torch.device = "cuda", fuse: bool = True,
-                 prefetch: bool = False):
+                 fold_ln: bool = True, weight_cache: dict | None = None):
         if mode not in _MODES:
             raise ValueError(f"mode must be one of {sorted(_MODES)}")
         if torch.device(device).type == "cuda" and not torch.cuda.is_available():
@@ -198,17 +192,16 @@ class Plan:
         self.input_views: dict[str, torch.Tensor] = {}
         self.out_buffers: list[torch.Tensor] = []
         self.out_sources: list[DVal] = []
-        self._wcache: dict[tuple, torch.Tensor] = {}
+        # converted device weights; plans of one (graph, store) may share it
+        self._wcache: dict[tuple, torch.Tensor] = {} if weight_cache is None else weight_cache
         self._buffers: list[torch.Tensor] = []
         # Adds whose launch is deferred so the consuming norm can fuse them:
         # output data_ptr -> (node id, a, b, out, launch closure)
         self._deferred: dict[int, tuple] = {}
-        self._linear_w: dict[int, tuple[int, int]] = {}  # step index -> (weight ptr, bytes)
-        self.prefetch = prefetch
+        # Batch-1 LayerNorms folded into their producing / consuming GEMMs (no
+        # norm launch; include/netfuse_b200.h "Folded LayerNorm")
+        self.fold_ln = fold_ln
         self._add_into_norm: dict[str, str] = {}
-        self._ln_done: set[str] = set()  # norms computed by a Linear epilogue
-        self._pf_sources: set[int] = set()  # launches that prefetch the next weights
-        self._add_passthrough: dict[str, tuple[str, str]] = {}  # add -> (linear side, residual)
         self._lin_out: dict[int, _LinearStep] = {}  # output data_ptr -> its launch
         self._folded: dict[int, _FoldedNorm] = {}   # out data_ptr -> folded norm (not launched)
         self._cuda_graph: torch.cuda.CUDAGraph | None = None
@@ -399,31 +392,6 @@ class Plan:
             ins = [self.vals[parse_ref(r)[0]] for r in node.inputs]
             for v in ins:
                 self._flush_deferred(v.t, keep_for=node)
-            ln_chain = self._linear_ln_chain(node, ins, weights, users, outputs)
-            if ln_chain is not None:
-                add, norm = ln_chain
-                try:
-                    out = self._lower_linear_ln(node, add, norm, ins[0], weights)
-                except (ShapeError, UnsupportedOpError) as exc:
-                    raise ExecutionError(node.id, exc) from exc
-                self.vals[node.id] = out
-                self._ln_done.add(norm.id)
-                self.op_invocations += 1
-                self.dispatch_count += 1
-                continue
-            if node.id in self._add_passthrough:
-                # residual added in the producing Linear's epilogue: the Add is
-                # its (glue-viewed) output
-                self.vals[node.id] = self.vals[self._add_passthrough[node.id][0]]
-                self.op_invocations += 1
-                self.dispatch_count += 1
-                continue
-            if node.id in self._ln_done:
-                # normalised in the producing Linear's epilogue (cluster LN)
-                self.vals[node.id] = ins[0]
-                self.op_invocations += 1
-                self.dispatch_count += 1
-                continue
             attn = self._qkv_attention_pair(node, ins, weights, users, outputs)
             if attn is not None:
                 try:
@@ -465,8 +433,6 @@ class Plan:
                 del self._folded[key]
                 continue
             self._emit_deferred(key)
-        if self.fuse and self.device.type == "cuda" and self.prefetch:
-            self._insert_l2_prefetch()
 
         for ref in g.graph_outputs:
             v = self.vals[parse_ref(ref)[0]]
@@ -703,7 +669,6 @@ class Plan:
                                       bias.view(groups, coutg).contiguous())
             wg, bg = self._wcache[wkey]
             xp, wp, bp, yp = xn.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
-            self._linear_w[len(self.steps)] = (wp, wg.numel() * wg.element_size())
             ws = self._workspace(groups, pix, cg, coutg)
             wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
             self._emit(conv.id, lambda st: _lib.call(
@@ -745,7 +710,6 @@ class Plan:
             ws = self._ws_buffer(need) if need > 0 else None
             wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
             xp, wp, bp, yp = xn.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
-            self._linear_w[len(self.steps)] = (wp, wg.numel() * wg.element_size())
             self._emit(conv.id, lambda st: _lib.call(
                 "nf_grouped_conv_tc", xp, wp, bp, rp, yp, n, h, wd, c_in, cout, groups, k, s,
                 pad, kpad, relu, wsp, wsb, st))
@@ -890,23 +854,6 @@ class Plan:
                 fused_into[act_users[j].id] = m.id
         return True
 
-    def _insert_l2_prefetch(self) -> None:
-        """Before each merged Linear, warm L2 with the *next* Linear's weights
-        so HBM keeps streaming through the attention / norm / epilogue phases
-        in between (B200: 126 MB L2 holds a whole merged layer's GEMM)."""
-        lin = sorted(self._linear_w)
-        if len(lin) < 2:
-            return
-        nxt = {i: self._linear_w[j] for i, j in zip(lin, lin[1:])}
-        steps = []
-        for i, step in enumerate(self.steps):
-            if i in nxt:
-                ptr, nbytes = nxt[i]
-                steps.append(("l2_prefetch", lambda st, p=ptr, b=nbytes:
-                              _lib.call("nf_l2_prefetch", p, b, st), 1))
-            steps.append(step)
-        self.steps = steps
-
     @staticmethod
     def _aliases(buf: torch.Tensor, view: torch.Tensor) -> bool:
         lo = buf.data_ptr()
@@ -989,7 +936,7 @@ class Plan:
         # tiles). Token-row tiles support them too (kernel-tested), but at
         # 512-1024 tokens the separate TMA-ring norm is cheaper: XLNet N=32
         # B=4 4.39 -> 4.98 ms and BERT N=32 B=8 7.28 -> 8.09 ms with folding.
-        fold_ok = fast_tc and self.fuse and _FOLD_LN and rows <= 128 and bool(
+        fold_ok = fast_tc and self.fuse and self.fold_ln and rows <= 128 and bool(
             _lib.load().nf_linear_fold_supported(groups, rows, k_in, n_out))
         # an output that may take the residual must have no other reader
         feeds_add = fold_ok and act_user is None and self._only_feeds_add(node.id)
@@ -1012,13 +959,9 @@ class Plan:
         wp, bp, yp = w.data_ptr(), bias.data_ptr() if bias is not None else None, y.data_ptr()
         dcode, mcode = K.dtype_code(x), self.mcode
         ws = self._workspace(groups, rows, k_in, n_out) if fast_tc else None
-        idx = len(self.steps)
-        self._linear_w[idx] = (w.data_ptr(), w.numel() * w.element_size())
-        if fast_tc and rows <= 256:
-            self._pf_sources.add(idx)  # weight-streaming (batch-1) launch
         wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
         step = _LinearStep(xp, k_in, wp, bp, yp, n_out, groups, rows, dcode, layout, act, mcode,
-                           wsp, wsb, self._pf_hint(idx), fold_ok)
+                           wsp, wsb, fold_ok)
         if fo is not None:
             step.fin = (fo.stats.data_ptr(), fo.parts, colsum.data_ptr(), fo.eps)
         if feeds_add and y.is_contiguous():
@@ -1052,98 +995,6 @@ class Plan:
                 b = b + self._w(weights, bname, "vec_f32", dt).reshape(g, n)
             self._wcache[key] = (w2, b.contiguous(), w2.float().sum(-1).contiguous())
         return self._wcache[key]
-
-    def _linear_ln_chain(self, node, ins, weights, users, outputs):
-        """Batch-1 merged Linear -> Add(residual) -> [glue views] -> norm over
-        each instance's output features: one launch with the residual add and
-        the LayerNorm in the GEMM epilogue (a cluster of N/128 CTAs per
-        instance shares the row statistics over DSMEM)."""
-        # Measured on B200 (BERT-base N=8, B=1): the cluster-LN launch costs
-        # ~5 us of epilogue on the critical path and forgoes split-K for FF2,
-        # more than the separate norm launch it saves (0.757 vs 0.685 ms per
-        # forward), so it is opt-in (NF_FUSE_LN=1).
-        if not (self.fuse and _FUSE_LN) or self.mcode != _lib.NF_MODE_FAST:
-            return None
-        if node.kind not in (OpKind.MATMUL, OpKind.BATCH_MATMUL) or node.id in outputs:
-            return None
-        # Linear -> [glue views] -> Add: the merger may re-lay the Linear's
-        # batch-packed output out channel-packed for the Add (merger.py:237-301)
-        cur, near = node, node.id
-        while True:
-            us = users.get(cur.id, [])
-            if len(us) != 1 or cur.id in outputs:
-                return None
-            if us[0].kind in (OpKind.RESHAPE, OpKind.TRANSPOSE):
-                cur = us[0]
-                near = cur.id
-                continue
-            break
-        if us[0].kind is not OpKind.ADD or us[0].id not in self._add_into_norm:
-            return None
-        add = us[0]
-        refs = [parse_ref(r)[0] for r in add.inputs]
-        if len(refs) != 2 or refs.count(near) != 1:
-            return None
-        norm = self.graph.node_map()[self._add_into_norm[add.id]]
-        v = ins[0]
-        if v.split is not None or v.dtype != torch.bfloat16:
-            return None
-        wsrc = weights[node.weights[0]]
-        if wsrc.data.dtype != torch.bfloat16:
-            return None
-        groups = wsrc.spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
-        k_in, n_out = wsrc.spec.dims[-2], wsrc.spec.dims[-1]
-        rows = v.t.numel() // max(groups * k_in, 1)
-        ngroups = norm.attrs.get("groups", 1)
-        if ngroups != groups or rows > 128 or n_out > 1024 or n_out % 8 or k_in % 8:
-            return None
-        nspec = norm.output_spec
-        if nspec.dims[channel_axis(len(nspec.dims))] != groups * n_out:
-            return None
-        other_id = refs[1] if refs[0] == near else refs[0]
-        if other_id not in self.vals or self.vals[other_id].dtype != torch.bfloat16:
-            return None
-        self._add_passthrough[add.id] = (near, other_id)
-        return add, norm
-
-    def _lower_linear_ln(self, node, add, norm, v, weights):
-        x = self._materialize(node.id, v)
-        self._flush_deferred(x)
-        self._flush_deferred(self.vals[self._add_passthrough[add.id][1]].t)
-        wname = node.weights[0]
-        groups = weights[wname].spec.dims[0] if node.kind is OpKind.BATCH_MATMUL else 1
-        k_in, n_out = weights[wname].spec.dims[-2], weights[wname].spec.dims[-1]
-        rows = x.numel() // (groups * k_in)
-        other = self.vals[self._add_passthrough[add.id][1]]
-        r_t = None
-        if other.split is not None:
-            # channel-packed value kept model-major: (instance, token, channel)
-            # rows are already where the kernel reads them if the storage is
-            # dense with the model axis outermost and channels contiguous
-            t = other.t
-            a = other.split
-            if (_dense_block(t) and t.stride(a + 1) == 1 and t.stride(a) == rows * n_out
-                    and t.numel() == groups * rows * n_out):
-                r_t = t
-        if r_t is None:
-            r_t = self._materialize(node.id, other)
-        if r_t.numel() != groups * rows * n_out:
-            raise ShapeError("residual does not match the linear output")
-        w = self._w(weights, wname, "linear_nk", x.dtype)
-        bias = self._w(weights, node.weights[1], "vec_f32", x.dtype) if len(node.weights) > 1 \
-            else None
-        gam = self._w(weights, norm.weights[0], "vec_f32", x.dtype)
-        bet = self._w(weights, norm.weights[1], "vec_f32", x.dtype)
-        y = self._alloc(node.output_spec.dims, x.dtype)
-        eps = float(norm.attrs["eps"])
-        xp, wp, bp, rp, yp = x.data_ptr(), w.data_ptr(), \
-            bias.data_ptr() if bias is not None else None, r_t.data_ptr(), y.data_ptr()
-        gp, bt = gam.data_ptr(), bet.data_ptr()
-        self._linear_w[len(self.steps)] = (wp, w.numel() * w.element_size())
-        self._emit(node.id, lambda st: _lib.call(
-            "nf_grouped_linear_ln", xp, k_in, rows * k_in, wp, bp, rp, gp, bt, eps, yp, n_out,
-            rows * n_out, groups, rows, k_in, n_out, st))
-        return DVal(y, node.output_spec.dims)
 
     def _qkv_attention_pair(self, node, ins, weights, users, outputs):
         """A batch-1 QKV projection whose only consumer is an Attention over
@@ -1179,7 +1030,8 @@ class Plan:
         d = weights[wname].spec.dims[-2]
         heads = attn.attrs["heads"]
         fo = self._folded_exact(x)
-        if fo is not None and not (_FOLD_LN and fo.m == groups and fo.rows == 128 and fo.d == d):
+        if fo is not None and not (self.fold_ln and fo.m == groups and fo.rows == 128
+                                   and fo.d == d):
             fo = None
         if fo is None:
             self._flush_deferred(x)
@@ -1194,9 +1046,6 @@ class Plan:
         scale = 1.0 / math.sqrt(d // heads)
         xp = fo.raw.data_ptr() if fo is not None else x.data_ptr()
         wp, bp, yp = w.data_ptr(), bias.data_ptr() if bias is not None else None, y.data_ptr()
-        idx = len(self.steps)
-        self._linear_w[idx] = (wp, w.numel() * w.element_size())
-        self._pf_sources.add(idx)
         if fo is not None:
             sp, parts, cp, eps = fo.stats.data_ptr(), fo.parts, colsum.data_ptr(), fo.eps
             self._emit(attn.id, lambda st: _lib.call(
@@ -1205,7 +1054,7 @@ class Plan:
         else:
             self._emit(attn.id, lambda st: _lib.call(
                 "nf_qkv_attention", xp, d, 128 * d, wp, bp, yp, groups, 128, d, heads,
-                float(scale), *self._pf_hint(idx), st))
+                float(scale), st))
         return DVal(y, attn.output_spec.dims)
 
     def _head_major(self, w: torch.Tensor, heads: int, key) -> torch.Tensor:
@@ -1217,21 +1066,6 @@ class Plan:
             self._wcache[key] = w.reshape(g, 3, heads, dh, k).permute(0, 2, 1, 3, 4) \
                 .reshape(g, n3, k).contiguous()
         return self._wcache[key]
-
-    def _pf_hint(self, idx: int) -> tuple:
-        """(pointer, bytes) of the next weight-streaming launch's weights for
-        the launch at step ``idx`` to prefetch into L2 once its own loads are
-        issued (batch-1 plans: HBM keeps streaming across attention / norm
-        launches), or (None, 0)."""
-        if not _L2_PF or idx not in self._pf_sources:
-            return (None, 0)
-        later = [j for j in self._linear_w if j > idx]
-        if not later:
-            return (None, 0)
-        ptr, nbytes = self._linear_w[min(later)]
-        if nbytes > 64 * 1024 * 1024:  # keep the prefetch well inside the 126 MB L2
-            return (None, 0)
-        return (ptr, nbytes)
 
     def _attention(self, node, v):
         x = self._materialize(node.id, v)
@@ -1334,7 +1168,7 @@ class Plan:
         the Linear adds the residual in its epilogue and writes the norm's
         per-token partial sums; the norm itself is not launched (its
         consumers fold it, or it is emitted on first non-folding use)."""
-        if not (self.fuse and _FOLD_LN) or self.mcode != _lib.NF_MODE_FAST:
+        if not (self.fuse and self.fold_ln) or self.mcode != _lib.NF_MODE_FAST:
             return False
         m, rows, s_inst, s_row, g_per, cg = geom[:6]
         if g_per != 1 or out.dtype != torch.bfloat16:
@@ -1695,18 +1529,97 @@ class PipelinedRunner:
 # Reference-compatible entry point
 # ----------------------------------------------------------------------------
 
-_PLAN_CACHE: dict[tuple, Plan] = {}
+class _PlanEntry:
+    """Compiled plans of one (graph, weight store, mode, fuse): the graph and
+    store are held weakly and re-identified with ``is``; the fingerprint pins
+    the exact TensorValue objects (and their in-place version counters) the
+    plans were built from, so a replaced or mutated weight is never served
+    from a stale plan. Plans share the converted device weights but each
+    owns its activations, I/O buffers and split-K workspace; a plan is used
+    by one execute() call at a time."""
+
+    def __init__(self, graph, weights, mode, fuse):
+        import weakref
+        self.graph_ref = weakref.ref(graph)
+        self.store_ref = weakref.ref(weights)
+        self.fingerprint = _weights_fingerprint(graph, weights)
+        self.mode, self.fuse = mode, fuse
+        self.wcache: dict = {}
+        self.free: list[Plan] = []
+        self.lock = threading.Lock()
+
+    def valid_for(self, graph, weights) -> bool:
+        return (self.graph_ref() is graph and self.store_ref() is weights
+                and self.fingerprint == _weights_fingerprint(graph, weights))
+
+
+def _weights_fingerprint(graph: Graph, weights: WeightStore) -> tuple:
+    tvs = tuple((name, id(tv), tv.data._version) for name, tv in weights.tensors.items())
+    return (id(graph.nodes), graph.graph_outputs, tuple(graph.graph_inputs.items()), tvs)
+
+
+class _PlanCache:
+    """Bounded LRU of plan entries behind the stateless ``execute`` entry
+    point (reference contract: pure and reentrant). Entries die
+    with their graph or weight store (weakref finalizers: ids recycle) and
+    past ``capacity``."""
+
+    def __init__(self, capacity: int = 4):
+        from collections import OrderedDict
+        self.capacity = capacity
+        self._lock = threading.Lock()
+        self._entries: "OrderedDict[tuple, _PlanEntry]" = OrderedDict()
+
+    def _drop(self, key, entry) -> None:
+        with self._lock:
+            if self._entries.get(key) is entry:
+                del self._entries[key]
+
+    def checkout(self, graph, weights, mode, fuse) -> tuple[_PlanEntry, Plan]:
+        import weakref
+        key = (id(graph), id(weights), mode, fuse)
+        with self._lock:
+            entry = self._entries.get(key)
+            if entry is not None and not entry.valid_for(graph, weights):
+                del self._entries[key]
+                entry = None
+            if entry is None:
+                entry = _PlanEntry(graph, weights, mode, fuse)
+                self._entries[key] = entry
+                weakref.finalize(graph, self._drop, key, entry)
+                weakref.finalize(weights, self._drop, key, entry)
+                while len(self._entries) > self.capacity:
+                    self._entries.popitem(last=False)
+            else:
+                self._entries.move_to_end(key)
+        with entry.lock:
+            if entry.free:
+                return entry, entry.free.pop()
+        # a new plan (first call, or another thread holds every free one)
+        return entry, Plan(graph, weights, mode=mode, fuse=fuse, weight_cache=entry.wcache)
+
+    @staticmethod
+    def checkin(entry: _PlanEntry, plan: Plan) -> None:
+        with entry.lock:
+            entry.free.append(plan)
+
+    def clear(self) -> None:
+        with self._lock:
+            self._entries.clear()
+
+    def __len__(self) -> int:
+        return len(self._entries)
+
+
+_PLANS = _PlanCache()
 
 
 def compile_plan(graph: Graph, weights: WeightStore, *, mode: str = "fast",
-                 fuse: bool = True, prefetch: bool = False) -> Plan:
-    """Build (or fetch the cached) plan for ``graph`` with ``weights``."""
-    key = (id(graph), id(weights), mode, fuse, prefetch)
-    plan = _PLAN_CACHE.get(key)
-    if plan is None or plan.graph is not graph:
-        plan = Plan(graph, weights, mode=mode, fuse=fuse, prefetch=prefetch)
-        _PLAN_CACHE[key] = plan
-    return plan
+                 fuse: bool = True, fold_ln: bool = True) -> Plan:
+    """Compile ``graph`` with ``weights`` into a caller-owned :class:`Plan`
+    (weights converted to kernel layouts in HBM, buffers preallocated).
+    Every call builds a new plan: the handle is the cache."""
+    return Plan(graph, weights, mode=mode, fuse=fuse, fold_ln=fold_ln)
 
 
 def execute(graph: Graph, weights: WeightStore, inputs: dict[str, TensorValue], *,
@@ -1726,7 +1639,7 @@ def execute(graph: Graph, weights: WeightStore, inputs: dict[str, TensorValue], 
             raise ExecutionError(name, ShapeError(
                 f"input {name!r}: got {tv.spec.dims} ({tv.spec.dtype}), graph wants "
                 f"{spec.dims} ({spec.dtype})"))
-    plan = compile_plan(graph, weights, mode=mode, fuse=fuse)
+    entry, plan = _PLANS.checkout(graph, weights, mode, fuse)
     trace = ExecTrace(op_invocations=plan.op_invocations, dispatch_count=plan.dispatch_count,
                       kernel_launches=plan.kernel_launches)
     t0 = time.perf_counter_ns()
@@ -1734,12 +1647,15 @@ def execute(graph: Graph, weights: WeightStore, inputs: dict[str, TensorValue], 
     events: list | None = [] if trace_nodes else None
     plan.launch(events=events)
     outs = [b.clone() for b in plan.outputs()]
-    torch.cuda.synchronize()
+    torch.cuda.current_stream(plan.device).synchronize()
     trace.total_ns = time.perf_counter_ns() - t0
     if events:
         for i, (nid, _, _) in enumerate(plan.steps):
             ms = events[i].elapsed_time(events[i + 1])
             trace.node_times_ns[nid] = trace.node_times_ns.get(nid, 0) + int(ms * 1e6)
+    # nothing in flight reads the plan's buffers after the stream sync: it
+    # may serve the next call (a call that raised never returns its plan)
+    _PLANS.checkin(entry, plan)
     result = []
     for ref, t in zip(graph.graph_outputs, outs):
         prod = parse_ref(ref)[0]

@@ -125,6 +125,10 @@ def group_norm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, *, grou
     if tuple(gamma.shape) != (c,) or tuple(beta.shape) != (c,):
         raise ShapeError(f"gamma/beta must be ({c},), got {tuple(gamma.shape)} and "
                          f"{tuple(beta.shape)}")
+    if residual is not None and (tuple(residual.shape) != tuple(x.shape)
+                                 or residual.dtype != x.dtype or residual.device != x.device):
+        raise ShapeError(f"residual {tuple(residual.shape)}/{residual.dtype}/{residual.device} "
+                         f"must match x {tuple(x.shape)}/{x.dtype}/{x.device}")
     xc = x.contiguous()
     rc = None if residual is None else residual.contiguous()
     y = torch.empty_like(xc)

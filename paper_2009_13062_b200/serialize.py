@@ -194,8 +194,8 @@ def load_graph(path: str | Path) -> Graph:
 def _blob_name(name: str, taken: set[str]) -> str:
     base = "".join(c if c.isalnum() or c in "._-" else "_" for c in name) + ".tnsr"
     fname = base
-    while fname in taken:  # sanitisation collisions get a numeric prefix
-        fname = f"{len(taken)}_{base}"
+    while fname in taken:  # sanitisation collisions chain a numeric prefix
+        fname = f"{len(taken)}_{fname}"
     taken.add(fname)
     return fname
 

@@ -459,3 +459,47 @@ def classifier_head(in_spec: TensorSpec, width: int, *, seed: int,
 def head_widths(n: int) -> list[int]:
     """Deterministic per-task class counts (GLUE-like: 2, 3, ... )."""
     return [2 + (m % 4) for m in range(n)]
+
+
+# ----------------------------------------------------------------------------
+# BASELINE configurations as merged workloads (bench.py and the config parity
+# tests build the exact same plan through this one function)
+# ----------------------------------------------------------------------------
+
+def merged_workload(model: str, instances: int, batch: int, dtype: str = "bf16",
+                    first_instance: int = 0, heads: bool = True):
+    """Instances ``first_instance .. first_instance+instances-1`` of ``model``
+    merged into one graph: every instance its own seeded weights and inputs,
+    plus (``heads``) its own unmerged per-task head attached with
+    ``merge_backbone``: FC 2048->1000 for the CNNs, a
+    first-token pooler + classifier (``head_widths``) for the encoders.
+
+    Returns (graph, stores, inputs, merged, merged_store, heads)."""
+    from .merger import merge, merge_backbone
+
+    graph = build_graph(model, batch=batch, dtype=dtype)
+    ids = list(range(first_instance, first_instance + instances))
+    stores = [build_weights(model, dtype=dtype, seed=0, model=m) for m in ids]
+    inputs = [model_inputs(graph, seed=0, model=m) for m in ids]
+    head_list = None
+    if heads:
+        out = graph.node_map()[graph.graph_outputs[0].rsplit(":", 1)[0]].output_spec
+        if len(out.dims) == 4:  # CNN: per-task FC 2048 -> 1000 on the pooled features
+            head_list = [fc_head(out, 1000, seed=100 + m) for m in ids]
+        else:
+            widths = head_widths(first_instance + instances)[first_instance:]
+            head_list = [classifier_head(out, w, seed=100 + m) for m, w in zip(ids, widths)]
+        merged, mstore = merge_backbone(graph, {n.id for n in graph.nodes}, stores, head_list)
+    else:
+        merged, mstore = merge(graph, stores)
+    return graph, stores, inputs, merged, mstore, head_list
+
+
+# BASELINE.json configs (name -> model, instances, batch, dtype)
+BASELINE_CONFIGS = {
+    "C1": ("resnet50", 2, 1, "f32"),
+    "C2": ("bert-base", 8, 1, "bf16"),
+    "C3": ("resnext50_32x4d", 32, 1, "bf16"),
+    "C4": ("xlnet-base", 32, 4, "bf16"),
+    "C5": ("bert-base", 32, 8, "bf16"),  # per-GPU shard of N=256 over 8 GPUs
+}

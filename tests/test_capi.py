@@ -31,7 +31,7 @@ def test_ctypes_arity_matches_header():
 
 def test_status_strings_and_abi():
     lib = _lib.load()
-    assert lib.nf_abi_version() == 1
+    assert lib.nf_abi_version() == 2
     for code in range(4):
         assert isinstance(lib.nf_status_string(code), bytes)
 

@@ -28,7 +28,7 @@ CASES = [
     (1, 56, 56, 64, 32, 32, 3, 2, 1, False, True),    # stride 2: 13-row halo
     (1, 9, 11, 4, 16, 16, 3, 1, 1, True, True),       # ragged rows, residual
     (1, 20, 20, 3, 64, 48, 3, 1, 1, False, False),    # 64-channel groups, coutg 48
-    (1, 30, 30, 3, 4, 16, 7, 2, 3, False, True),      # 4-channel halo (NF_CONV_HALO_STEM=1)
+    (1, 30, 30, 3, 4, 16, 7, 2, 3, False, True),      # 4-channel stem-like groups
 ]
 
 

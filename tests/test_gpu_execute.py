@@ -172,3 +172,65 @@ def test_bert_2layer_large_batch_vs_oracle():
     for j in range(2):
         want = OX.execute(graph, stores[j].tensors, inputs[j])[0]
         assert normwise(per[j][0].numpy(), want) < 2e-2
+
+
+# ---------------------------------------------------------------------------
+# execute() is stateless and reentrant (reference
+# tests/test_execute.py:109-118, threaded strategy bench.py:112-121)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,batch", [("cnnblock", 2), ("bert-2l", 1)])
+def test_parallel_runs_different_inputs_bit_identical(name, batch):
+    """8 threads, each with its OWN inputs, race execute() on one merged
+    graph + store: every thread gets exactly its serial result."""
+    from concurrent.futures import ThreadPoolExecutor
+    dtype = "bf16" if name.startswith("bert") else "f32"
+    graph, stores = W.build_zoo(name, num_models=2, batch=batch, dtype=dtype)
+    merged, mstore = merge(graph, stores)
+    bound = [merged.bind_inputs([model_inputs(graph, seed=s, model=j) for j in range(2)])
+             for s in range(8)]
+    serial = [[o.data.cpu() for o in execute(merged.graph, mstore, b)[0]] for b in bound]
+    assert not torch.equal(serial[0][0], serial[1][0])
+
+    def run(i):
+        torch.cuda.set_device(0)
+        with torch.cuda.stream(torch.cuda.Stream()):
+            return i, [o.data.cpu() for o in execute(merged.graph, mstore, bound[i])[0]]
+
+    for _ in range(3):
+        with ThreadPoolExecutor(max_workers=8) as pool:
+            for i, outs in pool.map(run, list(range(8)) * 2):
+                for a, b in zip(outs, serial[i]):
+                    assert torch.equal(a, b), f"thread input {i}"
+
+
+def test_execute_never_serves_stale_weights():
+    """A replaced weight, an in-place edit, and a new store that reuses a
+    freed store's id all take effect on the next execute()."""
+    import gc
+
+    from paper_2009_13062_b200 import TensorSpec, TensorValue, WeightStore
+    graph, stores = build_zoo("ffnn", num_models=1, batch=2)
+    inputs = model_inputs(graph, seed=3)
+    store = WeightStore(dict(stores[0].tensors))
+    base = execute(graph, store, inputs)[0][0].data.cpu()
+    w = store["mm1.w"]
+    store.tensors["mm1.w"] = TensorValue(w.spec, w.data * 2)           # replaced
+    replaced = execute(graph, store, inputs)[0][0].data.cpu()
+    assert not torch.equal(base, replaced)
+    store.tensors["mm1.w"].data.mul_(0.5)                               # edited in place
+    assert torch.equal(execute(graph, store, inputs)[0][0].data.cpu(), base)
+    store.tensors["mm1.w"] = TensorValue(TensorSpec("f32", (3, 3)), torch.zeros(3, 3))  # bad
+    with pytest.raises(ExecutionError):
+        execute(graph, store, inputs)
+    results = {}
+    for seed in range(4):                                               # id reuse after free
+        _, st = build_zoo("ffnn", num_models=1, batch=2, seed=seed)
+        s = WeightStore(dict(st[0].tensors))
+        results[seed] = (id(s), execute(graph, s, inputs)[0][0].data.cpu())
+        del s, st
+        gc.collect()
+    outs = [r[1] for r in results.values()]
+    for i in range(len(outs)):
+        for j in range(i + 1, len(outs)):
+            assert not torch.equal(outs[i], outs[j])

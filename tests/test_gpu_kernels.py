@@ -236,3 +236,35 @@ def test_rel_attention_vs_oracle(dtype, S, B, H, shared):
     want = np.stack([OK.rel_attention(qkv[m], r[m], rw[m], rr[m], heads=H) for m in range(M)])
     got = host(GK.rel_attention(cuda(qkv, dtype), cuda(r, dtype), cuda(rw), cuda(rr), heads=H))
     assert normwise(got, want) < (2e-2 if dtype == torch.bfloat16 else 1e-5)
+
+
+@pytest.mark.parametrize("offset", [0.0, 10.0, 100.0])
+@pytest.mark.parametrize("rows", [64, 12000])  # warp-per-row vec kernel / TMA-ring kernel
+def test_layer_norm_offset_mean_stress(offset, rows):
+    """Rows of x + c with c/std up to ~100 (the TMA-ring norm streams >= 9472
+    rows): two-pass centred statistics keep the variance exact where
+    E[x^2] - mean^2 would cancel. Reference: fp32 LayerNorm of the same bf16
+    inputs (plus residual); normwise error <= 1e-2 of the bf16 output."""
+    from paper_2009_13062_b200 import kernels as KK
+    gen = torch.Generator().manual_seed(rows)
+    d = 768
+    x = ((torch.rand(rows, d, generator=gen) * 2 - 1) + offset).bfloat16().cuda()
+    r = (torch.rand(rows, d, generator=gen) * 0.5).bfloat16().cuda()
+    gam = (torch.rand(d, generator=gen) + 0.5).cuda()
+    bet = (torch.rand(d, generator=gen) - 0.5).cuda()
+    y = KK.layer_norm(x, gam, bet, eps=1e-12, residual=r)
+    ref = torch.nn.functional.layer_norm(x.float() + r.float(), (d,), gam, bet, eps=1e-12)
+    err = ((y.float() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-2, err
+
+
+def test_norm_residual_must_match_x():
+    from paper_2009_13062_b200 import ShapeError
+    from paper_2009_13062_b200 import kernels as KK
+    x = torch.zeros(4, 64, dtype=torch.bfloat16, device="cuda")
+    g = torch.ones(64, device="cuda")
+    with pytest.raises(ShapeError):
+        KK.layer_norm(x, g, g, eps=1e-5, residual=torch.zeros(2, 64, dtype=torch.bfloat16,
+                                                                device="cuda"))
+    with pytest.raises(ShapeError):
+        KK.layer_norm(x, g, g, eps=1e-5, residual=torch.zeros(4, 64, device="cuda"))

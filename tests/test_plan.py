@@ -57,12 +57,10 @@ def test_layernorms_fold_into_neighbouring_linears():
     assert [nid for nid in st if ".ln" in nid] == ["merged::l01.ln2"]
 
 
-def test_layernorm_fold_opt_out(monkeypatch):
-    from paper_2009_13062_b200 import engine
-    monkeypatch.setattr(engine, "_FOLD_LN", False)
+def test_layernorm_fold_opt_out():
     graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
     merged, mstore = merge(graph, stores)
-    plan = Plan(merged.graph, mstore, device="cpu")
+    plan = Plan(merged.graph, mstore, device="cpu", fold_ln=False)
     assert len(plan.steps) == 2 * 6
 
 
@@ -72,17 +70,6 @@ def test_qkv_attention_fusion_needs_batch_one():
     plan = Plan(merged.graph, mstore, device="cpu")
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.qkv" in ids and "merged::l00.attn" in ids
-
-
-def test_cluster_layernorm_fusion_opt_in(monkeypatch):
-    from paper_2009_13062_b200 import engine
-    monkeypatch.setattr(engine, "_FUSE_LN", True)
-    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
-    merged, mstore = merge(graph, stores)
-    plan = Plan(merged.graph, mstore, device="cpu")
-    ids = [nid for nid, _, _ in plan.steps]
-    # qkv+attn, proj+add+ln1, ff1(+gelu), ff2+add+ln2 per layer
-    assert len(ids) == 2 * 4 and not any(".ln" in i for i in ids)
 
 
 def test_gelu_fused_into_linear_epilogue():

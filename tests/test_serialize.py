@@ -97,3 +97,23 @@ def test_malformed_artifacts_raise_with_offsets():
     doc["extra"] = 1
     with pytest.raises(GraphFormatError, match="unknown"):
         S.deserialize(json.dumps(doc))
+
+
+def test_blob_name_double_collision_chains_prefix(tmp_path):
+    """Sanitisation collisions chain the numeric prefix like the reference
+    (serialize.py:227-230): '2_a_b', 'a/b', 'a_b' -> '2_2_a_b.tnsr'."""
+    import json
+
+    import numpy as np
+
+    from paper_2009_13062_b200.serialize import load_weight_store, save_weight_store
+    from paper_2009_13062_b200.tensors import TensorValue, WeightStore
+
+    store = WeightStore({n: TensorValue.from_array(np.full(3, i, np.float32))
+                         for i, n in enumerate(["2_a_b", "a/b", "a_b"])})
+    save_weight_store(store, tmp_path)
+    files = json.loads((tmp_path / "manifest.json").read_text())["tensors"]
+    assert files == {"2_a_b": "2_a_b.tnsr", "a/b": "a_b.tnsr", "a_b": "2_2_a_b.tnsr"}
+    back = load_weight_store(tmp_path)
+    for n in store.tensors:
+        assert back[n].bit_equal(store[n])
