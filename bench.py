@@ -1,23 +1,33 @@
 """Benchmark: merged inferences/s of N same-architecture instances in one
-forward (BASELINE.json metric), on B200.
+forward (BASELINE.json metric: "merged inferences/sec (N instances x batch) at
+N=32; speedup vs N separate runs"), on B200.
 
-Workload (default): BASELINE configs[1] — BERT-base merged N=8 instances,
-batch 1, seq 128, bf16, each instance with its own random-init weights and
-per-task classifier head (unmerged, merge_backbone), synthetic embeddings.
+Workload (default, BASELINE configs[4] per GPU): BERT-base, 32 merged
+instances per GPU, batch 8, seq 128, bf16, each instance with its own
+random-init weights and per-task classifier head (unmerged, merge_backbone),
+synthetic embeddings. `--gpus 8` under torchrun is config C5 itself (N=256
+sharded 32 per GPU). `--config C1..C5` selects another BASELINE config.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+    python bench.py [--config C5] [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N [--scaling weak|strong] ...
 
-Multi-GPU = instance sharding: every rank hosts its own
-`--instances` merged instances (weak scaling), no collective on the hot path;
-the step time is the max over ranks.
+Multi-GPU = instance sharding: weak scaling (default) gives every
+rank `--instances` merged instances; `--scaling strong` splits `--instances`
+(e.g. 256) over the ranks. No collective on the hot path; the step time is the
+max over ranks; one all_gather of the per-instance logits after the timed
+region is timed and reported separately (`gather`).
 
 `value`: device-timed CUDA-graph replays of the merged forward with inputs
 resident in HBM; the L2 is flushed (256 MiB write) between steps, outside the
-timed events. `e2e`: the same through the public plan API with host buffers —
-H2D of every instance's input from pinned memory, forward, D2H of the logits
-— each step. `--impl reference` times the reference CPU algorithm (the
-oracle's numpy restatement of pkg/src/modelmerge/engine.py) on the host cores.
+timed events. `e2e`: the same through the public serving API with host
+buffers (PipelinedRunner: H2D of every instance's input from pinned memory,
+forward, D2H of the logits) each step. `roofline`: the dominant kernel family
+(merged Linear / implicit-GEMM conv launches) — its share of a forward from
+per-launch CUDA events in an instrumented graph replay, times the real
+replay's ms_per_step, against its algorithmic bytes / flops. `--impl reference`
+times the reference CPU algorithm (the oracle's numpy restatement of
+pkg/src/modelmerge/engine.py) on the host cores, on a bounded sample of the
+same workload.
 """
 
 from __future__ import annotations
@@ -208,6 +218,82 @@ def linear_launch_bytes(merged, mstore, step_ids=None) -> dict[str, tuple[int, i
 # Our arm
 # ---------------------------------------------------------------------------
 
+def shard_for(args, world: int, rank: int) -> range:
+    """This rank's instance ids: weak scaling = `--instances` per rank;
+    strong scaling = `--instances` in total, split over the ranks."""
+    from paper_2009_13062_b200.sharding import shard_range
+    total = args.instances * world if args.scaling == "weak" else args.instances
+    return shard_range(total, world, rank)
+
+
+def family_roofline(plan, lin: dict, ms_per_step: float, peaks: dict, reps: int = 5) -> dict:
+    """Dominant-kernel roofline from a live, instrumented CUDA-graph replay:
+    every launch of the plan bracketed by (external) CUDA events recorded
+    into the graph on the launching stream, replayed `reps` times. The
+    family's SHARE of the summed per-launch times is applied to the real
+    (PDL-overlapped) replay's ms_per_step, so the family time can never
+    exceed the step; achieved = algorithmic bytes (flops) / that time."""
+    import torch
+
+    steps = plan.steps
+    dev = plan.device
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(steps) + 1)]
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.launch()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        st = torch.cuda.current_stream()
+        for i, (_, fn, _) in enumerate(steps):
+            evs[i].record(st)
+            fn(st.cuda_stream)
+        evs[-1].record(st)
+    per = [0.0] * len(steps)
+    for _ in range(reps):
+        g.replay()
+        torch.cuda.synchronize(dev)
+        for i in range(len(steps)):
+            per[i] += evs[i].elapsed_time(evs[i + 1]) / reps
+    del g
+    all_ms = sum(per)
+    fam_ms_inst, fam_bytes, fam_flops, fam_n = 0.0, 0, 0, 0
+    for i, (nid, _, _) in enumerate(steps):
+        if nid in lin:
+            fam_ms_inst += per[i]
+            fam_bytes += lin[nid][0]
+            fam_flops += lin[nid][1]
+            fam_n += 1
+    share = fam_ms_inst / all_ms if all_ms else 0.0
+    fam_ms = share * ms_per_step
+    assert fam_ms <= ms_per_step + 1e-9
+    # bound: HBM when the family's arithmetic intensity is under the measured
+    # ridge (bf16 peak / copy bandwidth), tensor otherwise
+    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    tensor_bound = fam_bytes > 0 and fam_flops / fam_bytes > ridge
+    gbs = fam_bytes / (fam_ms / 1e3) / 1e9 if fam_ms else 0.0
+    tflops = fam_flops / (fam_ms / 1e3) / 1e12 if fam_ms else 0.0
+    return {
+        "bound": "tensor" if tensor_bound else "hbm",
+        "achieved": round(tflops if tensor_bound else gbs, 1),
+        "peak": peaks["bf16_tflops"] if tensor_bound else peaks["hbm_gbs"],
+        "unit": "TFLOP/s" if tensor_bound else "GB/s",
+        "frac": round((tflops / peaks["bf16_tflops"]) if tensor_bound
+                      else (gbs / peaks["hbm_gbs"]), 4),
+        "launches_per_step": fam_n,
+        "share_of_step": round(share, 4),
+        "family_ms_per_step": round(fam_ms, 4),
+        "instrumented_ms_per_step": round(all_ms, 4),
+        "algorithmic_bytes_per_step": fam_bytes,
+        "algorithmic_flops_per_step": fam_flops,
+        "algorithmic_bytes_per_launch": fam_bytes // max(fam_n, 1),
+        "hbm_gbs_achieved": round(gbs, 1),
+        "tflops_achieved": round(tflops, 1),
+    }
+
+
 def run_ours(args) -> dict | None:
     import torch
     import torch.distributed as dist
@@ -221,15 +307,19 @@ def run_ours(args) -> dict | None:
 
     from paper_2009_13062_b200 import PipelinedRunner, compile_plan
 
-    from paper_2009_13062_b200.sharding import shard_range
-    shard = shard_range(args.instances * world, world, rank)  # weak scaling: N per GPU
+    shard = shard_for(args, world, rank)
+    total_instances = args.instances * world if args.scaling == "weak" else args.instances
     graph, stores, inputs, merged, mstore, heads = build_workload(
         args.model, len(shard), args.batch, args.dtype, shard.start, heads=not args.no_heads)
+    torch.cuda.reset_peak_memory_stats(dev)
     plan = compile_plan(merged.graph, mstore, mode="fast")
     bound = merged.bind_inputs(inputs)
     plan.load_inputs(bound)
     torch.cuda.synchronize()
     graph_exec = plan.capture()
+    graph_exec.replay()
+    torch.cuda.synchronize()
+    plan_peak = torch.cuda.max_memory_allocated(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -257,8 +347,27 @@ def run_ours(args) -> dict | None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    per_step_items = args.instances * args.batch * world
+    per_step_items = total_instances * args.batch
     value = per_step_items / (ms_per_step / 1e3)
+
+    # ---- end-of-run gather of every instance's logits (not on the hot path)
+    gather = None
+    if world > 1:
+        logits = _per_instance_logits(plan, merged)
+        dist.barrier()
+        ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ge0.record(stream)
+        from paper_2009_13062_b200.sharding import gather_instance_outputs
+        got = gather_instance_outputs(logits, total_instances)
+        ge1.record(stream)
+        torch.cuda.synchronize()
+        gms = ge0.elapsed_time(ge1)
+        t = torch.tensor([gms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather = {"collective": "all_gather (NCCL) of per-instance logits, after timing",
+                  "ms": round(float(t.item()), 4),
+                  "bytes_per_rank": sum(x.numel() * x.element_size() for x in logits),
+                  "instances_gathered": len(got) if got is not None else None}
 
     # ---- e2e through the public API with host buffers --------------------
     pinned = {k: v.data.pin_memory() for k, v in bound.items()}
@@ -289,31 +398,18 @@ def run_ours(args) -> dict | None:
         e2e_ms = float(t.item())
     e2e_value = per_step_items / (e2e_ms / args.steps / 1e3)
 
-    # ---- dominant kernel roofline (merged Linear), CUDA events per launch --
-    lin = linear_launch_bytes(merged, mstore, {nid for nid, _, _ in plan.steps})
-    events: list = []
-    for _ in range(2):
-        events = []
-        plan.launch(events=events)
-    torch.cuda.synchronize()
-    is_cnn = "res" in args.model
-    lin_ms, lin_bytes, lin_flops, lin_n, all_ms = 0.0, 0, 0, 0, 0.0
-    for i, (nid, _, _) in enumerate(plan.steps):
-        ms = events[i].elapsed_time(events[i + 1])
-        all_ms += ms
-        if nid in lin:
-            lin_ms += ms
-            lin_bytes += lin[nid][0]
-            lin_flops += lin[nid][1]
-            lin_n += 1
+    # ---- dominant kernel family roofline (live, instrumented replay) ------
     peaks, peak_src = _peaks()
-    achieved = lin_bytes / (lin_ms / 1e3) / 1e9
-    traffic = None
-    tfile = ROOT / "profiles" / "gemm_traffic.json"
-    if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(f"{args.model}/N{args.instances}/B{args.batch}")
+    lin = linear_launch_bytes(merged, mstore, {nid for nid, _, _ in plan.steps})
+    roofline = family_roofline(plan, lin, ms_per_step, peaks)
+    is_cnn = "res" in args.model
+    roofline["kernel"] = ("k_grouped_gemm_tc (implicit-GEMM merged conv + Linear)" if is_cnn
+                          else "k_grouped_gemm_tc (merged Linear) + k_qkv_attention_tc")
+    roofline["peak_source"] = peak_src
+    roofline["traffic"] = _ncu_traffic(args)
+    roofline["ncu_share"] = _ncu_share(args)
 
-    unmerged = None if args.no_unmerged else unmerged_legs(
+    unmerged = None if (args.no_unmerged or world > 1) else unmerged_legs(
         args, graph, stores, inputs, heads, flush, stream, value)
 
     if world > 1:
@@ -321,31 +417,7 @@ def run_ours(args) -> dict | None:
     if rank != 0:
         dist.destroy_process_group()
         return None
-    cpu = cpu_baseline(args, graph, stores, inputs, heads) if world == 1 and not args.no_cpu \
-        else None
-    # Bound of the dominant kernel family: HBM when its arithmetic intensity is
-    # under the measured ridge (bf16 peak / copy bandwidth), tensor otherwise.
-    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
-    tensor_bound = lin_bytes > 0 and lin_flops / lin_bytes > ridge
-    tflops = lin_flops / (lin_ms / 1e3) / 1e12 if lin_ms else 0.0
-    roofline = {
-        "bound": "tensor" if tensor_bound else "hbm",
-        "kernel": ("k_grouped_gemm_tc (merged Linear) + k_qkv_attention_tc" if not is_cnn else
-                   "k_grouped_gemm_tc (implicit-GEMM merged conv + Linear)"),
-        "achieved": round(tflops if tensor_bound else achieved, 1),
-        "peak": peaks["bf16_tflops"] if tensor_bound else peaks["hbm_gbs"],
-        "unit": "TFLOP/s" if tensor_bound else "GB/s",
-        "frac": round((tflops / peaks["bf16_tflops"]) if tensor_bound
-                      else (achieved / peaks["hbm_gbs"]), 4),
-        "traffic": traffic,
-        "peak_source": peak_src,
-        "launches_per_step": lin_n,
-        "algorithmic_bytes_per_step": lin_bytes,
-        "algorithmic_flops_per_step": lin_flops,
-        "hbm_gbs_achieved": round(achieved, 1),
-        "tflops_achieved": round(tflops, 1),
-        "share_of_step": round(lin_ms / all_ms, 4) if all_ms else None,
-    }
+    cpu = cpu_baseline(args) if world == 1 and not args.no_cpu else None
     if world > 1:
         dist.destroy_process_group()
     return {
@@ -357,17 +429,20 @@ def run_ours(args) -> dict | None:
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": args.dtype,
-        "data": "synthetic (seeded U[-1,1] embeddings; fan-in-scaled random-init weights)",
+        "data": "synthetic (seeded U[-1,1] embeddings / images; fan-in-scaled random-init "
+                "weights)",
         "config": {
-            "workload": f"{args.model} merged N={args.instances} B={args.batch} per GPU"
-                        + ("" if args.no_heads else " + per-task classifier heads"),
+            "workload": f"{args.model} merged N={len(shard)} B={args.batch} per GPU"
+                        + (f" ({total_instances} instances on {world} GPUs)" if world > 1 else "")
+                        + ("" if args.no_heads else " + per-task heads"),
+            "baseline_config": args.config,
             "model": args.model,
-            "instances_per_gpu": args.instances,
-            "global_instances": args.instances * world,
-            "global_batch": args.instances * args.batch * world,
+            "instances_per_gpu": len(shard),
+            "global_instances": total_instances,
+            "global_batch": per_step_items,
             "batch": args.batch,
             "seq_len": 128 if "bert" in args.model or "xlnet" in args.model else None,
             "image": 224 if "res" in args.model else None,
@@ -378,11 +453,45 @@ def run_ours(args) -> dict | None:
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "roofline": roofline,
+        "gather": gather,
+        "memory": {"peak_hbm_allocated_bytes": plan_peak,
+                   "merged_weights_bytes": mstore.total_bytes()},
         "unmerged": unmerged,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": plan.kernel_launches * args.steps,
     }
+
+
+def _per_instance_logits(plan, merged) -> list:
+    """Per-instance head outputs of this rank's plan as same-shape tensors
+    (the heads' widths differ per task: padded to the widest)."""
+    import torch
+    flat = [g[0] for g in merged.slice_outputs(list(plan.outputs()))]
+    width = max(t.shape[-1] for t in flat)
+    return [torch.nn.functional.pad(t, (0, width - t.shape[-1])).contiguous() for t in flat]
+
+
+def _profiles_json(name: str):
+    f = ROOT / "profiles" / name
+    return json.loads(f.read_text()) if f.exists() else {}
+
+
+def _workload_key(args) -> str:
+    return f"{args.model}/N{args.instances}/B{args.batch}/{args.dtype}"
+
+
+def _ncu_traffic(args):
+    """DRAM bytes per dominant-family launch from the committed ncu --set full
+    capture of this workload (profiles/r02_ncu_traffic.json), or None."""
+    return _profiles_json("r02_ncu_traffic.json").get(_workload_key(args))
+
+
+def _ncu_share(args):
+    """The dominant family's share of a forward in the committed ncu launch
+    list of this workload (serialised, cold cache: shares compare, absolute
+    times do not), or None."""
+    return _profiles_json("r02_ncu_share.json").get(_workload_key(args))
 
 
 def _time_steps(fn, n: int, flush, stream) -> float:
@@ -525,116 +634,158 @@ def unmerged_legs(args, graph, stores, inputs, heads, flush, stream, merged_valu
 # Reference CPU path (oracle restatement of the reference numpy kernels)
 # ---------------------------------------------------------------------------
 
-def _layer_graph(model: str, batch: int, dtype: str):
-    from paper_2009_13062_b200 import workloads as W
-    return W.build_graph("bert-2l" if model.startswith("bert") else model, batch=batch,
-                         dtype=dtype)
+class ReferenceSampler:
+    """Bounded samples of the reference CPU algorithm on this config: the
+    oracle's numpy restatement of pkg/src/modelmerge/engine.py (bit-identical
+    to it on every golden vector), one instance per host thread (the
+    reference's `threaded` strategy, bench.py:102-121).
+
+    One job = the work of one instance that is independent of everything
+    else (sequences and layers are independent units of
+    work for the clock): transformers run ONE encoder layer of ONE sequence
+    (1/L of an inference, L = 12); CNNs run one full forward of the instance's
+    batch plus its FC head. Throughput = inference-equivalents completed / the
+    measured wall time of the sample: nothing is extrapolated beyond the
+    sample's own work and the reported time is the time the sample took."""
+
+    def __init__(self, args, instances: list[int]):
+        from paper_2009_13062_b200 import model_inputs
+        from paper_2009_13062_b200 import workloads as W
+
+        self.model = args.model
+        one = W.one_layer_model(args.model)
+        self.layers = W.layer_count(args.model)
+        self.jobs = []
+        if one is not None:
+            g = W.build_graph(one, batch=1, dtype=args.dtype)
+            for m in instances:
+                st = W.build_weights(one, dtype=args.dtype, seed=0, model=m)
+                self.jobs.append((g, st.tensors, model_inputs(g, seed=0, model=m), None))
+            self.items_per_job = 1.0 / self.layers
+            self.unit = f"1 of {self.layers} encoder layers x 1 sequence"
+        else:
+            g = W.build_graph(args.model, batch=args.batch, dtype=args.dtype)
+            out = g.node_map()[g.graph_outputs[0].rsplit(":", 1)[0]].output_spec
+            for m in instances:
+                st = W.build_weights(args.model, dtype=args.dtype, seed=0, model=m)
+                self.jobs.append((g, st.tensors, model_inputs(g, seed=0, model=m),
+                                  W.fc_head(out, 1000, seed=100 + m)))
+            self.items_per_job = float(args.batch)
+            self.unit = f"1 full forward (B={args.batch}) + FC head"
+
+    @staticmethod
+    def _run(job):
+        from oracle import executor as OX
+        g, tensors, x, head = job
+        out = OX.execute(g, tensors, x)[0]
+        if head is not None:
+            OX.execute(head[0], head[1].tensors, {"feat": out})
+        return out
+
+    def step(self, threads: int, jobs: list | None = None) -> tuple[float, float]:
+        """Run `jobs` (default: all) on `threads` host threads; return
+        (inference-equivalents done, wall seconds)."""
+        jobs = self.jobs if jobs is None else jobs
+        t0 = time.perf_counter()
+        if threads == 1:
+            for j in jobs:
+                self._run(j)
+        else:
+            with ThreadPoolExecutor(max_workers=threads) as ex:
+                list(ex.map(self._run, jobs))
+        return len(jobs) * self.items_per_job, time.perf_counter() - t0
 
 
-def reference_sample(args, instances: list[int], threads: int) -> tuple[float, str]:
-    """Run the reference algorithm on a bounded sample and return the
-    extrapolated whole-workload inferences/s plus a description."""
-    from oracle import executor as OX
-    from paper_2009_13062_b200 import model_inputs
-    from paper_2009_13062_b200 import workloads as W
-
-    sample_layers = 1
-    g2 = _layer_graph(args.model, args.batch, args.dtype)
-    one = W.BertConfig(layers=sample_layers)
-    g1, _ = W._bert(args.batch, args.dtype, one)
-    jobs = []
-    for m in instances:
-        st = W.build_weights("bert-2l", dtype=args.dtype, seed=0, model=m)
-        x = model_inputs(g2, seed=0, model=m)
-        jobs.append((st, x))
-
-    def run(job):
-        st, x = job
-        return OX.execute(g1, st.tensors, x)
-
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(run, jobs))
-    dt = time.perf_counter() - t0
-    layers = W.BERT_BASE.layers
-    per_instance_s = dt * layers / sample_layers / len(jobs)
-    value = args.batch / per_instance_s
-    desc = (f"{len(jobs)} instance(s) x {sample_layers} of {layers} encoder layers, "
-            f"{threads} thread(s); extrapolated x{layers // sample_layers} layers "
-            f"(slices independent, PAPER.md:620-670); heads excluded")
-    return value, desc
-
-
-def cpu_baseline(args, graph, stores, inputs, heads) -> dict:
-    """One complete instance forward (all layers + its head) of the reference
-    algorithm on one host core: no extrapolation over layers."""
-    from oracle import executor as OX
+def cpu_baseline(args, budget_s: float = 10.0) -> dict:
+    """The reference CPU algorithm on ONE host core (a scalar port): jobs of
+    the sampler run back to back until ~`budget_s` of work is done."""
     cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    feat = OX.execute(graph, stores[0].tensors, inputs[0])[0]
-    if heads:
-        OX.execute(heads[0][0], heads[0][1].tensors, {"feat": feat})
-    dt = time.perf_counter() - t0
-    return {"value": round(args.batch / dt, 5), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"1 full instance forward ({args.model}, B={args.batch}, + head) of the "
-                      f"numpy restatement of the reference kernels, {dt:.1f} s on 1 of "
-                      f"{cores} host cores"}
+    sampler = ReferenceSampler(args, list(range(min(args.instances, 8))))
+    items, secs, n = 0.0, 0.0, 0
+    while secs < budget_s and n < 64:
+        i, dt = sampler.step(1, [sampler.jobs[n % len(sampler.jobs)]])
+        items, secs, n = items + i, secs + dt, n + 1
+    return {"value": round(items / secs, 5), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n} job(s) of [{sampler.unit}] of the numpy restatement of the "
+                      f"reference kernels ({args.model}, same seeds), {secs:.1f} s on 1 of "
+                      f"{cores} host cores; value = inference-equivalents / wall time"}
 
 
 def run_reference(args) -> dict | None:
+    """--impl reference: the reference CPU algorithm on this config with all
+    the host threads it can use (min(N, cores) instances, one per thread),
+    each step one bounded sample. Under torchrun only rank 0 runs."""
     world, rank, _ = dist_env()
     if rank != 0:
         return None
-    threads = min(args.instances, os.cpu_count() or 1)
-    inst = list(range(min(args.instances, threads)))
-    vals = []
+    cores = os.cpu_count() or 1
+    threads = max(1, min(args.instances, cores))
+    sampler = ReferenceSampler(args, list(range(threads)))
     for _ in range(args.warmup):
-        reference_sample(args, inst, threads)
+        sampler.step(threads)
+    items, secs = 0.0, 0.0
     for _ in range(args.steps):
-        v, desc = reference_sample(args, inst, threads)
-        vals.append(v)
-    value = statistics.mean(vals)
-    ms_per_step = args.instances * args.batch / value * 1e3
+        i, dt = sampler.step(threads)
+        items, secs = items + i, secs + dt
+    value = items / secs
+    ms_per_step = secs / args.steps * 1e3
+    desc = (f"{threads} instance(s) x [{sampler.unit}] per step on {threads} thread(s) "
+            f"({cores} host cores); {items / args.steps:.4g} inference-equivalents per step")
     return {
         "impl": "reference",
         "metric": METRIC,
-        "value": round(value, 4),
+        "value": round(value, 5),
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 2),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": args.dtype,
         "data": "synthetic (same seeds as our arm)",
-        "config": {"workload": f"{args.model} N={args.instances} B={args.batch} S=128",
-                   "model": args.model, "instances_per_gpu": args.instances,
-                   "batch": args.batch, "seq_len": 128,
-                   "parallelism": "host threads (reference `threaded` strategy, bench.py:112-121)"},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
+        "config": {"workload": f"{args.model} N={args.instances} B={args.batch} per GPU",
+                   "baseline_config": args.config, "model": args.model,
+                   "instances_per_gpu": args.instances, "batch": args.batch,
+                   "items_per_step": round(items / args.steps, 5),
+                   "parallelism": "host threads (reference `threaded` strategy, "
+                                  "bench.py:112-121)"},
+        "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": threads,
                          "kind": "port", "sample": desc},
-        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+        "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
 
 
 def main(argv=None) -> int:
+    from paper_2009_13062_b200.workloads import BASELINE_CONFIGS
+
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--model", default="bert-base")
-    ap.add_argument("--instances", type=int, default=8, help="merged instances per GPU")
-    ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--config", choices=sorted(BASELINE_CONFIGS), default="C5",
+                    help="BASELINE.json config (C5 = BERT-base N=32/GPU B=8, the default)")
+    ap.add_argument("--model", default=None)
+    ap.add_argument("--instances", type=int, default=None,
+                    help="merged instances per GPU (weak) / in total (strong)")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--dtype", default=None)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-heads", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-unmerged", action="store_true",
                     help="skip the N-separate-runs legs (speedup denominator)")
     args = ap.parse_args(argv)
+    model, n, batch, dtype = BASELINE_CONFIGS[args.config]
+    args.model = args.model or model
+    args.instances = args.instances or n
+    args.batch = args.batch or batch
+    args.dtype = args.dtype or dtype
+    if (args.model, args.instances, args.batch, args.dtype) != (model, n, batch, dtype):
+        args.config = None  # a custom workload, not the named BASELINE config
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":

@@ -136,6 +136,26 @@ int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups
                                 int stride, int pad, int kpad);
 
 /*
+ * fp32 merged Conv2d on the tensor cores (3xTF32): reference `grouped_conv2d`
+ * (engine.py:155-191) / `conv2d` (122-152) at fp32 accuracy for the fp32
+ * configuration. x NHWC fp32 (N, H, W, C), C = groups * cg with cg % 4 == 0;
+ * w (2 * groups, Cout/groups, kpad) fp32 K-major with K = (kh, kw, c) zero
+ * padded to kpad (a multiple of 32): groups [0, G) hold hi = w with the low
+ * 13 mantissa bits cleared, [G, 2G) lo = w - hi; bias (Cout) fp32 or NULL
+ * (BatchNorm folded); residual / y NHWC fp32 (N, Ho, Wo, Cout); y =
+ * relu?(conv + bias + residual). The activation operand is split the same
+ * way on chip; each K step issues lo*hi + hi*lo + hi*hi (fp32 accumulate in
+ * TMEM): ~2^-20 relative per product. Split-K workspace as
+ * nf_grouped_conv_tc (nf_conv_tf32_workspace_bytes; zeroed once).
+ */
+int nf_grouped_conv_tf32(const void* x, const void* w, const float* bias, const void* residual,
+                         void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
+                         int stride, int pad, int kpad, int relu, void* workspace,
+                         int64_t workspace_bytes, void* stream);
+int64_t nf_conv_tf32_workspace_bytes(int N, int H, int W, int C, int Cout, int groups, int kernel,
+                                     int stride, int pad, int kpad);
+
+/*
  * Fused merged QKV projection + attention for batch-1 encoders (the merged
  * graph's BatchMatMul(qkv) -> Attention pair: reference `batch_matmul`,
  * engine.py:215-235, then the attention restatement). x (G, S=128, D) bf16

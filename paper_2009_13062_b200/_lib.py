@@ -48,6 +48,8 @@ SIGNATURES: dict[str, list] = {
     "nf_pool2d_nhwc": [_p, _p] + [_i] * 9 + [_p],
     "nf_grouped_conv_tc": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _i64, _p],
     "nf_conv_workspace_bytes": [_i] * 10,
+    "nf_grouped_conv_tf32": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _i64, _p],
+    "nf_conv_tf32_workspace_bytes": [_i] * 10,
     "nf_qkv_attention": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f, _p],
     "nf_linear_fold_supported": [_i64, _i64, _i64, _i64],
     "nf_grouped_linear_fold": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
@@ -67,7 +69,8 @@ SIGNATURES: dict[str, list] = {
 }
 
 _RESTYPES = {"nf_status_string": ctypes.c_char_p, "nf_linear_workspace_bytes": ctypes.c_int64,
-             "nf_conv_workspace_bytes": ctypes.c_int64}
+             "nf_conv_workspace_bytes": ctypes.c_int64,
+             "nf_conv_tf32_workspace_bytes": ctypes.c_int64}
 
 _lib: ctypes.CDLL | None = None
 

@@ -156,6 +156,21 @@ int nf_grouped_conv_tc(const void* x, const void* w, const float* bias, const vo
                              static_cast<cudaStream_t>(stream));
 }
 
+int nf_grouped_conv_tf32(const void* x, const void* w, const float* bias, const void* residual,
+                         void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
+                         int stride, int pad, int kpad, int relu, void* workspace,
+                         int64_t workspace_bytes, void* stream) {
+  if (!x || !w || !y || N < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return NF_ERR_SHAPE;
+  return nf::grouped_conv_tf32(x, w, bias, residual, y, N, H, W, C, Cout, groups, kernel, stride,
+                               pad, kpad, relu, workspace, workspace_bytes,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int64_t nf_conv_tf32_workspace_bytes(int N, int H, int W, int C, int Cout, int groups, int kernel,
+                                     int stride, int pad, int kpad) {
+  return nf::conv_tf32_workspace_bytes(N, H, W, C, Cout, groups, kernel, stride, pad, kpad);
+}
+
 int64_t nf_conv_workspace_bytes(int N, int H, int W, int C, int Cout, int groups, int kernel,
                                 int stride, int pad, int kpad) {
   return nf::conv_workspace_bytes(N, H, W, C, Cout, groups, kernel, stride, pad, kpad);

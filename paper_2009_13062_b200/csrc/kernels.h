@@ -71,6 +71,15 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
 int64_t conv_workspace_bytes(int64_t N, int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t G,
                              int64_t k, int64_t stride, int64_t pad, int64_t Kpad);
 
+// conv_tf32.cu — fp32 implicit-GEMM conv, 3xTF32 on tcgen05.
+int grouped_conv_tf32(const void* x, const void* w, const float* bias, const void* residual,
+                      void* y, int N, int H, int W, int C, int Cout, int G, int k, int stride,
+                      int pad, int Kpad, int relu, void* ws, int64_t ws_bytes,
+                      cudaStream_t stream);
+int64_t conv_tf32_workspace_bytes(int64_t N, int64_t H, int64_t W, int64_t C, int64_t Cout,
+                                  int64_t G, int64_t k, int64_t stride, int64_t pad,
+                                  int64_t Kpad);
+
 // conv_nhwc.cu
 int im2col_nhwc(const void* x, void* y, int N, int H, int W, int C, int G, int k, int stride,
                 int pad, int Kpad, int dtype, cudaStream_t s);

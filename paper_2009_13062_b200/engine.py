@@ -633,6 +633,9 @@ class Plan:
         wf, bias = self._wcache[key]
         relu = 1 if ch["relu"] else 0
         other = self.vals[ch["other"]] if ch["add"] is not None else None
+        if dt == torch.float32 and coutg % 4 == 0:
+            return self._lower_conv_tf32(ch, v, key, wf, bias, other, relu, groups, cg, coutg,
+                                         k, s, pad, (n, c, h, wd), (cout, ho, wo))
         if dt != torch.bfloat16:
             # fp32: NCHW direct conv with the fused scale-free folded epilogue
             x = self._materialize(conv.id, v)
@@ -722,6 +725,42 @@ class Plan:
             self._emit(conv.id, lambda st: _lib.call(
                 "nf_conv_nhwc_direct", xp, wp, bp, rp, yp, n, h, wd, c, cout, groups, k, s, pad,
                 relu, _lib.NF_BF16, st))
+        return DVal(yn.permute(0, 3, 1, 2), (n, cout, ho, wo))
+
+    def _lower_conv_tf32(self, ch, v, key, wf, bias, other, relu, groups, cg, coutg, k, s, pad,
+                         in_dims, out_dims) -> DVal:
+        """fp32 conv chain on the tensor cores (nf_grouped_conv_tf32, 3xTF32):
+        NHWC fp32 activations (channels per group padded to a multiple of 4,
+        e.g. the RGB stem 3 -> 4), BN-folded weights (G, Cout/G, (kh, kw, c))
+        split once into TF32 hi / lo halves, residual + ReLU in the epilogue."""
+        conv = ch["conv"]
+        n, c, h, wd = in_dims
+        cout, ho, wo = out_dims
+        cg_pad = -(-cg // 4) * 4
+        xn = self._nhwc_padded(conv.id, v, groups, cg, cg_pad) if cg_pad != cg \
+            else self._nhwc(conv.id, v)
+        kk = k * k * cg_pad
+        kpad = -(-kk // 32) * 32
+        wkey = key + ("tf32",)
+        if wkey not in self._wcache:
+            w4 = wf if cg_pad == cg else torch.nn.functional.pad(wf, (0, cg_pad - cg))
+            wg = torch.nn.functional.pad(w4.reshape(groups, coutg, kk), (0, kpad - kk))
+            wg = wg.to(torch.float32).contiguous()
+            hi = (wg.view(torch.int32) & -8192).view(torch.float32)  # clear 13 low bits
+            self._wcache[wkey] = (torch.cat([hi, wg - hi], 0).contiguous(), bias.contiguous())
+        wt, bt = self._wcache[wkey]
+        yn = self._alloc((n, ho, wo, cout), torch.float32)
+        rn = self._nhwc(conv.id, other) if other is not None else None
+        c_in = groups * cg_pad
+        need = int(_lib.load().nf_conv_tf32_workspace_bytes(n, h, wd, c_in, cout, groups, k, s,
+                                                            pad, kpad))
+        ws = self._ws_buffer(need) if need > 0 else None
+        wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
+        xp, wp, bp, yp = xn.data_ptr(), wt.data_ptr(), bt.data_ptr(), yn.data_ptr()
+        rp = rn.data_ptr() if rn is not None else None
+        self._emit(conv.id, lambda st: _lib.call(
+            "nf_grouped_conv_tf32", xp, wp, bp, rp, yp, n, h, wd, c_in, cout, groups, k, s, pad,
+            kpad, relu, wsp, wsb, st))
         return DVal(yn.permute(0, 3, 1, 2), (n, cout, ho, wo))
 
     # ------------------------------------------------------ sibling heads
@@ -1595,8 +1634,15 @@ class _PlanCache:
         with entry.lock:
             if entry.free:
                 return entry, entry.free.pop()
-        # a new plan (first call, or another thread holds every free one)
-        return entry, Plan(graph, weights, mode=mode, fuse=fuse, weight_cache=entry.wcache)
+            # A new plan (first call, or other threads hold every free one).
+            # Built under the entry lock and synchronised before release: the
+            # converted weights it adds to the shared cache are produced on
+            # this thread's stream, and another thread's plan will read them
+            # from its own stream.
+            plan = Plan(graph, weights, mode=mode, fuse=fuse, weight_cache=entry.wcache)
+            if plan.device.type == "cuda":
+                torch.cuda.current_stream(plan.device).synchronize()
+            return entry, plan
 
     @staticmethod
     def checkin(entry: _PlanEntry, plan: Plan) -> None:

@@ -345,6 +345,9 @@ _BUILDERS: dict[str, Callable[[int, str], tuple[Graph, WeightPlan]]] = {
     "bert-2l": bert_layers(2),
     "xlnet-base": _xlnet,
     "xlnet-2l": lambda b, d: _xlnet(b, d, XLNetConfig(layers=2)),
+    # one encoder layer: the reference CPU path's bounded timing sample
+    "bert-1l": bert_layers(1),
+    "xlnet-1l": lambda b, d: _xlnet(b, d, XLNetConfig(layers=1)),
 }
 
 MODEL_NAMES = tuple(_BUILDERS)
@@ -493,6 +496,24 @@ def merged_workload(model: str, instances: int, batch: int, dtype: str = "bf16",
     else:
         merged, mstore = merge(graph, stores)
     return graph, stores, inputs, merged, mstore, head_list
+
+
+def layer_count(model: str) -> int | None:
+    """Encoder layers of a transformer family member (None for CNNs)."""
+    if model.startswith("bert"):
+        return BERT_BASE.layers if model == "bert-base" else int(model.split("-")[1][:-1])
+    if model.startswith("xlnet"):
+        return XLNET_BASE.layers if model == "xlnet-base" else int(model.split("-")[1][:-1])
+    return None
+
+
+def one_layer_model(model: str) -> str | None:
+    """The one-layer member of a transformer family (timing samples)."""
+    if model.startswith("bert"):
+        return "bert-1l"
+    if model.startswith("xlnet"):
+        return "xlnet-1l"
+    return None
 
 
 # BASELINE.json configs (name -> model, instances, batch, dtype)
