@@ -484,14 +484,16 @@ def _workload_key(args) -> str:
 def _ncu_traffic(args):
     """DRAM bytes per dominant-family launch from the committed ncu --set full
     capture of this workload (profiles/r02_ncu_traffic.json), or None."""
-    return _profiles_json("r02_ncu_traffic.json").get(_workload_key(args))
+    got = _profiles_json("r02_ncu_traffic.json").get(_workload_key(args)) or {}
+    return got.get("dram_bytes_per_family_launch")
 
 
 def _ncu_share(args):
     """The dominant family's share of a forward in the committed ncu launch
     list of this workload (serialised, cold cache: shares compare, absolute
     times do not), or None."""
-    return _profiles_json("r02_ncu_share.json").get(_workload_key(args))
+    got = _profiles_json("r02_ncu_share.json").get(_workload_key(args)) or {}
+    return got.get("family_share")
 
 
 def _time_steps(fn, n: int, flush, stream) -> float:
