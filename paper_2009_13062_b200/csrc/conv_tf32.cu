@@ -38,7 +38,7 @@ constexpr int kTK = 32;            // fp32 elements per 128-byte K block
 constexpr int kTThreads = 320;     // TMA + MMA warps, 4 epilogue, 4 gather warps
 constexpr int kTEpi = 128;
 constexpr int kTGather = 128;
-constexpr int kTMaxSplits = 8;
+constexpr int kTMaxSplits = 16;  // batch-1 layer3/4 convs: few tiles, long K
 constexpr int64_t kTCounterBytes = 64 * 1024;
 
 template <int BN>

@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         mbar_wait(&tfull[acc], (local >> 1) & 1);
         if (etid == 0) NF_WAIT_END(3);
       }
+      NF_WAIT_BEGIN();  // epilogue busy: accumulator ready -> buffer released
       if constexpr (kResTma && !kResEarly) issue_residual();
       tc_fence_after();
       if (etid == 0 && local == 0) NF_TRACE(4);
@@ -614,16 +615,28 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         res_phase ^= 1u;
       }
       const float* bias = p.bias ? p.bias + int64_t(c.g) * p.features : nullptr;
+      // TMEM loads run one chunk ahead: chunk cc+EC is requested before
+      // chunk cc is processed, so its latency hides behind the epilogue math
+      // (the consumer of a just-issued tcgen05.ld was the top stall).
+      // (Not in the 448-thread gather kernels: their 128-register budget
+      // would spill the second chunk.)
+      constexpr bool kLdAhead = GATHER == 0;
+      uint32_t rnext[EC];
+      if constexpr (kLdAhead) {
+        tmem_ld_cols<EC>(t_row + uint32_t(col0), rnext);
+        tmem_ld_wait();
+      }
 #pragma unroll 1
       for (int cc = col0; cc < col0 + kColsPerThread; cc += EC) {
-        float v[EC];
-        {
-          uint32_t r[EC];
-          tmem_ld_cols<EC>(t_row + uint32_t(cc), r);
+        if constexpr (!kLdAhead) {
+          tmem_ld_cols<EC>(t_row + uint32_t(cc), rnext);
           tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < EC; ++j) v[j] = __uint_as_float(r[j]);
         }
+        float v[EC];
+#pragma unroll
+        for (int j = 0; j < EC; ++j) v[j] = __uint_as_float(rnext[j]);
+        if (kLdAhead && cc + EC < col0 + kColsPerThread)
+          tmem_ld_cols<EC>(t_row + uint32_t(cc + EC), rnext);
         if (p.splits > 1) {
           // Deterministic reduction: splits summed in index order.
           float sum[EC];
@@ -780,8 +793,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
             }
           }
         }
+        if constexpr (kLdAhead) tmem_ld_wait();  // the next chunk's columns have landed
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
+      if (etid == 0) NF_WAIT_END(4);
       release_acc(acc);
       if constexpr (C::kStaged) {
         fence_proxy_async_smem();

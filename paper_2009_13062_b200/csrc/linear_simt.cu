@@ -71,6 +71,59 @@ __global__ void __launch_bounds__(kSimtThreads)
   }
 }
 
+// FAST-mode few-row GEMV (T <= 8 rows, weights (K, N) row-major): the
+// per-task classifier heads of the fp32 configs (FC 2048 -> 1000 at batch
+// 1). A CTA owns 32 output columns and splits K over its 16 warps; each lane
+// streams one column (consecutive lanes = consecutive 4-byte words, one
+// 128-byte line per k), the rows of x are warp-uniform broadcasts, and the
+// warps' partial sums are added in warp order through shared memory
+// (deterministic). Weight-streaming: one pass over W at HBM rate instead of
+// the 8-rows-per-thread kernel's N/256 CTAs.
+constexpr int kGemvCols = 32;
+constexpr int kGemvWarps = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(kGemvCols * kGemvWarps)
+    k_linear_gemv(const T* __restrict__ x, const T* __restrict__ w, const float* __restrict__ bias,
+                  const T* __restrict__ residual, T* __restrict__ y, int T_rows, int K, int N,
+                  int act, int64_t x_ld, int64_t x_gs, int64_t y_ld, int64_t y_gs) {
+  pdl_enter();
+  __shared__ float part[kGemvWarps][kSimtRows][kGemvCols];
+  const int g = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = blockIdx.x * kGemvCols + lane;
+  const T* xg = x + int64_t(g) * x_gs;
+  const T* wg = w + int64_t(g) * K * N;
+  const int per = (K + kGemvWarps - 1) / kGemvWarps;
+  const int k0 = warp * per, k1 = min(K, k0 + per);
+  float acc[kSimtRows];
+#pragma unroll
+  for (int r = 0; r < kSimtRows; ++r) acc[r] = 0.0f;
+  if (n < N) {
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+      const float wv = to_f32(__ldg(wg + int64_t(k) * N + n));
+#pragma unroll
+      for (int r = 0; r < kSimtRows; ++r)
+        if (r < T_rows) acc[r] = fmaf(to_f32(__ldg(xg + int64_t(r) * x_ld + k)), wv, acc[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kSimtRows; ++r) part[warp][r][lane] = acc[r];
+  __syncthreads();
+  if (warp != 0 || n >= N) return;
+  const float b = bias ? bias[int64_t(g) * N + n] : 0.0f;
+  for (int r = 0; r < T_rows; ++r) {
+    float v = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kGemvWarps; ++q) v += part[q][r][lane];
+    v += b;
+    const int64_t off = int64_t(g) * y_gs + int64_t(r) * y_ld + n;
+    if (residual) v += to_f32(residual[off]);
+    y[off] = from_f32<T>(apply_act(v, act));
+  }
+}
+
 template <typename T>
 static int launch_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                        const float* bias, const void* residual, void* y, int64_t y_ld,
@@ -85,7 +138,11 @@ static int launch_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   launch_pdl(k_linear_simt<T, E, L>, dim3(grid), dim3(kSimtThreads), 0, stream, xp, wp, bias, rp, yp, int(Tr), \
                                                             int(K), int(N), act, x_ld, x_gs, \
                                                             y_ld, y_gs)
-  if (exact) {
+  if (!exact && w_layout == NF_W_KN && Tr <= kSimtRows && G <= 65535) {
+    launch_pdl(k_linear_gemv<T>, dim3((N + kGemvCols - 1) / kGemvCols, G),
+               dim3(kGemvCols * kGemvWarps), 0, stream, xp, wp, bias, rp, yp, int(Tr), int(K),
+               int(N), act, x_ld, x_gs, y_ld, y_gs);
+  } else if (exact) {
     if (w_layout == NF_W_KN) NF_SIMT(true, true); else NF_SIMT(true, false);
   } else {
     if (w_layout == NF_W_KN) NF_SIMT(false, true); else NF_SIMT(false, false);

@@ -187,6 +187,8 @@ class Plan:
         self.mcode = _MODES[mode]
         self.device = torch.device(device)
         self.fuse = fuse
+        # the store's specs (a pre-tiled artifact rebuilds a spec-only store)
+        self.weight_specs = {name: tv.spec for name, tv in weights.tensors.items()}
         self.steps: list[tuple[str, Callable[[int], None], int]] = []  # (node, fn, launches)
         self.vals: dict[str, DVal] = {}
         self.input_views: dict[str, torch.Tensor] = {}
@@ -210,7 +212,10 @@ class Plan:
         self._build(weights)
 
     # ----------------------------------------------------------------- weights
-    def _w(self, weights: WeightStore, name: str, kind: str, dtype: torch.dtype) -> torch.Tensor:
+    def _w(self, weights: WeightStore, name: str, kind: str, dtype: torch.dtype,
+           cache: bool = True) -> torch.Tensor:
+        """``name`` converted to a kernel layout on the device; ``cache=False``
+        for intermediates of a derived layout (not kept in HBM)."""
         key = (name, kind, dtype)
         if key in self._wcache:
             return self._wcache[key]
@@ -227,7 +232,8 @@ class Plan:
             out = src.to(self.device, dtype).contiguous()
         else:  # pragma: no cover
             raise AssertionError(kind)
-        self._wcache[key] = out
+        if cache:
+            self._wcache[key] = out
         return out
 
     # ---------------------------------------------------------------- helpers
@@ -449,6 +455,9 @@ class Plan:
                 m, c = v.t.shape[a], v.t.shape[a + 1]
                 self._copy_step("output", v.t, buf.view(v.dims[:a] + (m, c) + v.dims[a + 1:]))
             self.out_buffers.append(buf)
+        # the BN-folded fp32 conv weights only fed the kernel layouts above
+        for key in [k for k in self._wcache if k[0] == "convchain" and len(k) == 2]:
+            del self._wcache[key]
 
     # ------------------------------------------------------- fusion helpers
     @staticmethod
@@ -628,21 +637,29 @@ class Plan:
             raise ShapeError(f"kernel {wsrc.spec.dims} incompatible with {c} channels in "
                              f"{groups} group(s)")
         key = ("convchain", conv.id)
-        if key not in self._wcache:
-            self._wcache[key] = self._folded_conv(ch, weights, dt)
-        wf, bias = self._wcache[key]
+
+        def folded():
+            # BN-folded fp32 weights: only an intermediate of the kernel
+            # layouts below (dropped from the cache once the plan is built)
+            if key not in self._wcache:
+                self._wcache[key] = self._folded_conv(ch, weights, dt)
+            return self._wcache[key]
+
         relu = 1 if ch["relu"] else 0
         other = self.vals[ch["other"]] if ch["add"] is not None else None
         if dt == torch.float32 and coutg % 4 == 0:
-            return self._lower_conv_tf32(ch, v, key, wf, bias, other, relu, groups, cg, coutg,
+            return self._lower_conv_tf32(ch, v, key, folded, other, relu, groups, cg, coutg,
                                          k, s, pad, (n, c, h, wd), (cout, ho, wo))
         if dt != torch.bfloat16:
             # fp32: NCHW direct conv with the fused scale-free folded epilogue
             x = self._materialize(conv.id, v)
-            wn = wf.permute(0, 3, 1, 2).contiguous().to(dt)
+            wkey = key + ("nchw",)
+            if wkey not in self._wcache:
+                wf, bias = folded()
+                self._wcache[wkey] = (wf.permute(0, 3, 1, 2).contiguous().to(dt), bias)
+            wn, bias = self._wcache[wkey]
             r = self._materialize(conv.id, other) if other is not None else None
             y = self._alloc((n, cout, ho, wo), dt)
-            self._wcache[key + ("nchw",)] = wn
             xp, wp, bp, yp = x.data_ptr(), wn.data_ptr(), bias.data_ptr(), y.data_ptr()
             rp = r.data_ptr() if r is not None else None
             dcode = K.dtype_code(x)
@@ -668,6 +685,7 @@ class Plan:
             # NHWC rows in place (row stride C, group stride C/G).
             wkey = key + ("gemm",)
             if wkey not in self._wcache:
+                wf, bias = folded()
                 self._wcache[wkey] = (wf.reshape(groups, coutg, cg).to(dt).contiguous(),
                                       bias.view(groups, coutg).contiguous())
             wg, bg = self._wcache[wkey]
@@ -692,6 +710,7 @@ class Plan:
             kpad = -(-kk // 8) * 8
             wkey = key + ("igemm", sup)
             if wkey not in self._wcache:
+                wf, bias = folded()
                 w4 = wf
                 if cg_pad != cg:
                     w4 = torch.nn.functional.pad(wf, (0, cg_pad - cg))
@@ -719,15 +738,16 @@ class Plan:
         else:
             wkey = key + ("direct",)
             if wkey not in self._wcache:
-                self._wcache[wkey] = wf.to(dt).contiguous()
-            wd_t = self._wcache[wkey]
+                wf, bias = folded()
+                self._wcache[wkey] = (wf.to(dt).contiguous(), bias)
+            wd_t, bias = self._wcache[wkey]
             xp, wp, bp, yp = xn.data_ptr(), wd_t.data_ptr(), bias.data_ptr(), yn.data_ptr()
             self._emit(conv.id, lambda st: _lib.call(
                 "nf_conv_nhwc_direct", xp, wp, bp, rp, yp, n, h, wd, c, cout, groups, k, s, pad,
                 relu, _lib.NF_BF16, st))
         return DVal(yn.permute(0, 3, 1, 2), (n, cout, ho, wo))
 
-    def _lower_conv_tf32(self, ch, v, key, wf, bias, other, relu, groups, cg, coutg, k, s, pad,
+    def _lower_conv_tf32(self, ch, v, key, folded, other, relu, groups, cg, coutg, k, s, pad,
                          in_dims, out_dims) -> DVal:
         """fp32 conv chain on the tensor cores (nf_grouped_conv_tf32, 3xTF32):
         NHWC fp32 activations (channels per group padded to a multiple of 4,
@@ -743,6 +763,7 @@ class Plan:
         kpad = -(-kk // 32) * 32
         wkey = key + ("tf32",)
         if wkey not in self._wcache:
+            wf, bias = folded()
             w4 = wf if cg_pad == cg else torch.nn.functional.pad(wf, (0, cg_pad - cg))
             wg = torch.nn.functional.pad(w4.reshape(groups, coutg, kk), (0, kpad - kk))
             wg = wg.to(torch.float32).contiguous()
@@ -864,14 +885,17 @@ class Plan:
         npad = -(-max(widths) // 8) * 8
         G = len(members)
         dev, dt = self.device, t0.dtype
-        w = self._own(torch.zeros((G, npad, k_in), dtype=dt, device=dev))
-        bias = self._own(torch.zeros((G, npad), dtype=torch.float32, device=dev))
         has_bias = all(len(m.weights) > 1 for m in members)
-        for j, m in enumerate(members):
-            w[j, :widths[j]] = weights[m.weights[0]].data.to(dev, dt).t()
-            if has_bias:
-                bias[j, :widths[j]] = weights[m.weights[1]].data.to(dev, torch.float32)
-        self._wcache[("siblings", first.id)] = (w, bias)
+        skey = ("siblings", first.id, npad, has_bias)
+        if skey not in self._wcache:
+            w = torch.zeros((G, npad, k_in), dtype=dt, device=dev)
+            bias = torch.zeros((G, npad), dtype=torch.float32, device=dev)
+            for j, m in enumerate(members):
+                w[j, :widths[j]] = weights[m.weights[0]].data.to(dev, dt).t()
+                if has_bias:
+                    bias[j, :widths[j]] = weights[m.weights[1]].data.to(dev, torch.float32)
+            self._wcache[skey] = (w, bias)
+        w, bias = self._wcache[skey]
         act, act_users = _lib.NF_ACT_NONE, []
         us = [users.get(m.id, []) for m in members]
         if all(len(u) == 1 and u[0].kind in _ACT_OF and m.id not in outputs
@@ -1020,19 +1044,22 @@ class Plan:
                 continue
             return us[0].kind is OpKind.ADD
 
-    def _folded_weights(self, weights, wname, bname, fo: _FoldedNorm, dt):
+    def _folded_weights(self, weights, wname, bname, fo: _FoldedNorm, dt, cache: bool = True):
         """Weights / bias / column sums of a Linear consuming a folded norm:
         W' = W * gamma (over K), b' = b + W beta, colsum = sum_k W'."""
         key = ("fold", wname, bname, fo.gamma_name)
         if key not in self._wcache:
-            w = self._w(weights, wname, "linear_nk", dt)  # (G, N, K)
+            w = self._w(weights, wname, "linear_nk", dt, cache=False)  # (G, N, K)
             g, n, k = w.shape
             wf = w.float()
             w2 = (wf * fo.gamma.reshape(g, 1, k)).to(dt).contiguous()
             b = torch.einsum("gnk,gk->gn", wf, fo.beta.reshape(g, k))
             if bname:
                 b = b + self._w(weights, bname, "vec_f32", dt).reshape(g, n)
-            self._wcache[key] = (w2, b.contiguous(), w2.float().sum(-1).contiguous())
+            out = (w2, b.contiguous(), w2.float().sum(-1).contiguous())
+            if not cache:
+                return out
+            self._wcache[key] = out
         return self._wcache[key]
 
     def _qkv_attention_pair(self, node, ins, weights, users, outputs):
@@ -1075,12 +1102,17 @@ class Plan:
         if fo is None:
             self._flush_deferred(x)
         bname = node.weights[1] if len(node.weights) > 1 else None
-        if fo is not None:
-            w, bias, colsum = self._folded_weights(weights, wname, bname, fo, x.dtype)
-        else:
-            w = self._w(weights, wname, "linear_nk", x.dtype)
-            bias = self._w(weights, bname, "vec_f32", x.dtype) if bname else None
-        w = self._head_major(w, heads, ("qkv_hm", wname, fo.gamma_name if fo else None))
+        key = ("qkv_hm", wname, bname, fo.gamma_name if fo else None)
+        if key not in self._wcache:
+            if fo is not None:
+                w, bias, colsum = self._folded_weights(weights, wname, bname, fo, x.dtype,
+                                                       cache=False)
+            else:
+                w = self._w(weights, wname, "linear_nk", x.dtype, cache=False)
+                bias = self._w(weights, bname, "vec_f32", x.dtype) if bname else None
+                colsum = None
+            self._wcache[key] = (self._head_major(w, heads), bias, colsum)
+        w, bias, colsum = self._wcache[key]
         y = self._alloc(attn.output_spec.dims, x.dtype)
         scale = 1.0 / math.sqrt(d // heads)
         xp = fo.raw.data_ptr() if fo is not None else x.data_ptr()
@@ -1096,15 +1128,13 @@ class Plan:
                 float(scale), st))
         return DVal(y, attn.output_spec.dims)
 
-    def _head_major(self, w: torch.Tensor, heads: int, key) -> torch.Tensor:
+    @staticmethod
+    def _head_major(w: torch.Tensor, heads: int) -> torch.Tensor:
         """(G, 3D, D) q|k|v rows -> head-major rows (G, H, 3, 64, D) for the
         fused QKV+attention kernel (one TMA box per head)."""
-        if key not in self._wcache:
-            g, n3, k = w.shape
-            dh = n3 // (3 * heads)
-            self._wcache[key] = w.reshape(g, 3, heads, dh, k).permute(0, 2, 1, 3, 4) \
-                .reshape(g, n3, k).contiguous()
-        return self._wcache[key]
+        g, n3, k = w.shape
+        dh = n3 // (3 * heads)
+        return w.reshape(g, 3, heads, dh, k).permute(0, 2, 1, 3, 4).reshape(g, n3, k).contiguous()
 
     def _attention(self, node, v):
         x = self._materialize(node.id, v)

@@ -251,3 +251,108 @@ def load_merged(directory: str | Path):
     directory = Path(directory)
     graph = load_graph(directory / "graph.json")
     return MergedGraph.from_graph(graph), load_weight_store(directory / "weights")
+
+
+# ----------------------------------------------------------------------------
+# Pre-tiled plan artifacts (device layouts, loaded without conversion)
+# ----------------------------------------------------------------------------
+# A compiled Plan holds every weight in its kernel layout: Linear weights
+# K-major (G, N, K) bf16, the fused QKV weights head-major, LayerNorm-folded
+# weights with their column sums, conv weights NHWC (G, Cout/G, kh*kw*Cg)
+# with BatchNorm folded in (ResNeXt super-group slabs block-diagonal; fp32
+# convs split into TF32 hi/lo halves), per-task heads stacked. save_plan
+# writes exactly those tensors (TNSR blobs, reference serialize.py:168-207
+# format + bf16) beside the graph, keyed by the plan's layout keys; load_plan
+# copies them straight to the device and compiles the graph against a
+# spec-only store, so no transpose / fold / einsum runs at load time — and a
+# layout the artifact lacks fails loudly (the spec-only store has no data).
+
+PLAN_SCHEMA = 1
+
+
+def _enc_key(k):
+    if isinstance(k, tuple):
+        return {"tuple": [_enc_key(x) for x in k]}
+    if isinstance(k, torch.dtype):
+        return {"dtype": str(k).removeprefix("torch.")}
+    if k is None or isinstance(k, (str, int, float, bool)):
+        return k
+    raise GraphFormatError(f"cannot encode plan layout key element {k!r}")
+
+
+def _dec_key(obj):
+    if isinstance(obj, dict):
+        if "tuple" in obj:
+            return tuple(_dec_key(x) for x in obj["tuple"])
+        if "dtype" in obj:
+            return getattr(torch, obj["dtype"])
+        raise GraphFormatError(f"bad plan layout key {obj!r}")
+    return obj
+
+
+def save_plan(plan, directory: str | Path) -> None:
+    """Write ``plan``'s graph and its device-layout weights (see above)."""
+    from .tensors import DTYPE_NAMES
+    directory = Path(directory)
+    (directory / "tiled").mkdir(parents=True, exist_ok=True)
+    save_graph(plan.graph, directory / "graph.json")
+    taken: set[str] = set()
+    entries = []
+
+    def enc_val(v, stem):
+        if v is None:
+            return None
+        if isinstance(v, tuple):
+            return {"tuple": [enc_val(x, f"{stem}.{i}") for i, x in enumerate(v)]}
+        if not isinstance(v, torch.Tensor) or v.dtype not in DTYPE_NAMES:
+            raise GraphFormatError(f"plan layout {stem!r}: unsupported value {type(v)}")
+        fname = _blob_name(stem, taken)
+        tv = TensorValue(TensorSpec(DTYPE_NAMES[v.dtype], tuple(v.shape)), v.detach().cpu())
+        (directory / "tiled" / fname).write_bytes(tensor_to_bytes(tv))
+        return fname
+
+    for i, (key, val) in enumerate(plan._wcache.items()):
+        stem = "_".join(str(x) for x in (key if isinstance(key, tuple) else (key,)))
+        entries.append({"key": _enc_key(key), "value": enc_val(val, stem)})
+    doc = {"schema": PLAN_SCHEMA, "mode": plan.mode, "fuse": plan.fuse, "fold_ln": plan.fold_ln,
+           "weights": {n: _spec_json(s) for n, s in sorted(plan.weight_specs.items())},
+           "layouts": entries}
+    (directory / "plan.json").write_text(json.dumps(doc, indent=1) + "\n")
+
+
+def load_plan(directory: str | Path, device: str = "cuda"):
+    """Compile the artifact written by :func:`save_plan` into a Plan on
+    ``device``; the weights go host -> device once, already tiled."""
+    from .engine import Plan
+    directory = Path(directory)
+    try:
+        doc = json.loads((directory / "plan.json").read_text())
+    except json.JSONDecodeError as exc:
+        raise GraphFormatError(f"plan.json: not valid JSON: {exc.msg}", offset=exc.pos) from exc
+    if not isinstance(doc, dict) or doc.get("schema") != PLAN_SCHEMA:
+        raise GraphFormatError("plan.json: unsupported schema")
+    graph = load_graph(directory / "graph.json")
+    dev = torch.device(device)
+
+    def dec_val(obj):
+        if obj is None:
+            return None
+        if isinstance(obj, dict):
+            return tuple(dec_val(x) for x in obj["tuple"])
+        try:
+            blob = (directory / "tiled" / obj).read_bytes()
+        except OSError as exc:
+            raise GraphFormatError(f"cannot read layout blob {obj!r}: {exc}") from exc
+        return tensor_from_bytes(blob).data.to(dev)
+
+    cache = {_dec_key(e["key"]): dec_val(e["value"]) for e in doc["layouts"]}
+    specs = {n: _spec_of(s, f"weights[{n!r}]") for n, s in doc["weights"].items()}
+    store = WeightStore({n: TensorValue(s, torch.empty(s.dims, dtype=TORCH_DTYPES[s.dtype],
+                                                       device="meta"))
+                         for n, s in specs.items()})
+    try:
+        return Plan(graph, store, mode=doc["mode"], device=dev, fuse=doc["fuse"],
+                    fold_ln=doc["fold_ln"], weight_cache=cache)
+    except NotImplementedError as exc:  # a meta tensor was read: layout missing
+        raise GraphFormatError(f"plan artifact lacks a weight layout the graph needs: {exc}") \
+            from exc

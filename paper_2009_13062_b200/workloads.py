@@ -498,6 +498,26 @@ def merged_workload(model: str, instances: int, batch: int, dtype: str = "bf16",
     return graph, stores, inputs, merged, mstore, head_list
 
 
+def instance_workload(model: str, m: int, batch: int, dtype: str = "bf16",
+                      heads: bool = True, total: int | None = None):
+    """Instance ``m`` of ``merged_workload`` on its own (unmerged serving
+    strategies): the same seeded weights, inputs and per-task head.
+    ``total`` = the instance count the head widths are drawn for.
+
+    Returns (graph, store, inputs, head or None)."""
+    graph = build_graph(model, batch=batch, dtype=dtype)
+    store = build_weights(model, dtype=dtype, seed=0, model=m)
+    inputs = model_inputs(graph, seed=0, model=m)
+    head = None
+    if heads:
+        out = graph.node_map()[graph.graph_outputs[0].rsplit(":", 1)[0]].output_spec
+        if len(out.dims) == 4:
+            head = fc_head(out, 1000, seed=100 + m)
+        else:
+            head = classifier_head(out, head_widths(max(total or 0, m + 1))[m], seed=100 + m)
+    return graph, store, inputs, head
+
+
 def layer_count(model: str) -> int | None:
     """Encoder layers of a transformer family member (None for CNNs)."""
     if model.startswith("bert"):

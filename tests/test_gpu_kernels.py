@@ -268,3 +268,26 @@ def test_norm_residual_must_match_x():
                                                                 device="cuda"))
     with pytest.raises(ShapeError):
         KK.layer_norm(x, g, g, eps=1e-5, residual=torch.zeros(4, 64, device="cuda"))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,k,n,g", [(1, 2048, 1000, 2), (3, 768, 130, 1), (8, 100, 33, 3)])
+def test_linear_few_row_gemv_fast(dtype, rows, k, n, g):
+    """FAST-mode few-row GEMV (k_linear_gemv: fp32 per-task heads) against a
+    float64 torch reference, with bias + residual + ReLU fused."""
+    from paper_2009_13062_b200 import _lib
+    gen = torch.Generator().manual_seed(rows * 7 + n)
+    x = (torch.rand(g, rows, k, generator=gen) - 0.5).to(dtype).cuda()
+    w = ((torch.rand(g, k, n, generator=gen) - 0.5) / k ** 0.5).to(dtype).cuda()
+    b = (torch.rand(g, n, generator=gen) - 0.5).float().cuda()
+    r = (torch.rand(g, rows, n, generator=gen) - 0.5).to(dtype).cuda()
+    y = torch.empty(g, rows, n, dtype=dtype, device="cuda")
+    dcode = _lib.NF_F32 if dtype == torch.float32 else _lib.NF_BF16
+    _lib.call("nf_grouped_linear_ws", x.data_ptr(), k, rows * k, w.data_ptr(), b.data_ptr(),
+              r.data_ptr(), y.data_ptr(), n, rows * n, g, rows, k, n, dcode, _lib.NF_W_KN,
+              _lib.NF_ACT_RELU, _lib.NF_MODE_FAST, None, 0,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    want = torch.relu(torch.bmm(x.double(), w.double()) + b.double()[:, None] + r.double())
+    err = (y.double() - want).abs().max().item() / want.abs().max().item()
+    assert err < (1e-5 if dtype == torch.float32 else 1e-2), err

@@ -25,6 +25,10 @@ SHAPES = {
     "bert_b8_ff1_gelu": (32, 1024, 768, 3072),
     "bert_b8_qkv": (32, 1024, 768, 2304),
     "bert_b8_ff2": (32, 1024, 3072, 768),
+    "bert_b8_proj_res": (32, 1024, 768, 768),
+    "bert_b8_ff2_res": (32, 1024, 3072, 768),
+    "xlnet_b4_ff1_gelu": (32, 512, 768, 3072),
+    "xlnet_b4_proj_res": (32, 512, 768, 768),
 }
 
 
@@ -57,13 +61,14 @@ def run(name, G, T, K, N, reps, flush):
         return g
 
     act = _lib.NF_ACT_GELU if name.endswith("gelu") else _lib.NF_ACT_NONE
+    res = torch.zeros_like(y) if name.endswith("_res") else None
 
     wsb = int(_lib.load().nf_linear_workspace_bytes(G, T, K, N))
     ws = torch.zeros(max(wsb, 1), dtype=torch.uint8, device=dev)
 
     def launch_on(st):
         _lib.call("nf_grouped_linear_ws", x.data_ptr(), K, T * K, w.data_ptr(), b.data_ptr(),
-                  None, y.data_ptr(), N, T * N, G, T, K, N, _lib.NF_BF16, _lib.NF_W_NK, act,
+                  res.data_ptr() if res is not None else None, y.data_ptr(), N, T * N, G, T, K, N, _lib.NF_BF16, _lib.NF_W_NK, act,
                   _lib.NF_MODE_FAST, ws.data_ptr() if wsb else None, wsb, st)
 
     def timed(g):

@@ -34,22 +34,23 @@ int main(int argc, char** argv) {
   const char* names[8] = {"entry", "setup", "first_stage|ln_partials", "last_mma", "acc0_ready",
                           "epi_done", "exit", "ln_stats"};
   const bool warm = getenv("NF_TRACE_WARM") != nullptr;  // keep operands L2-resident
+  const char* acts = getenv("NF_TRACE_ACT");            // none | relu | gelu
+  const int act = !acts ? NF_ACT_NONE : (acts[0] == 'g' ? NF_ACT_GELU : acts[0] == 'r' ? NF_ACT_RELU : NF_ACT_NONE);
+  void* res = nullptr;
+  if (getenv("NF_TRACE_RES")) { cudaMalloc(&res, ny * 2); cudaMemset(res, 0, ny * 2); }
+  float* bias = nullptr;
+  cudaMalloc(&bias, size_t(G) * N * 4);
+  cudaMemset(bias, 0, size_t(G) * N * 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
   for (int it = 0; it < 3; ++it) {
     if (!warm) cudaMemset(flush, it, 256 << 20);
     stamp_kernel<<<1, 1>>>();
-    int st;
-    if (getenv("NF_TRACE_LN")) {
-      static float* gb = nullptr;
-      if (!gb) {
-        cudaMalloc(&gb, size_t(G) * N * 4 * 2);
-        cudaMemset(gb, 0, size_t(G) * N * 4 * 2);
-      }
-      st = nf::grouped_linear_ln_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, gb, gb + size_t(G) * N,
-                                    1e-5f, y, N, int64_t(T) * N, G, T, K, N, 0);
-    } else {
-      st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, nullptr, nullptr, y, N,
-                                 int64_t(T) * N, G, T, K, N, NF_BF16, 0, ws, ws_bytes, 0);
-    }
+    cudaEventRecord(e0);
+    int st = nf::grouped_linear_tc(x, K, int64_t(T) * K, w, bias, res, y, N, int64_t(T) * N, G, T,
+                                   K, N, NF_BF16, act, ws, ws_bytes, 0);
+    cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     if (st || e) { printf("status %d err %s\n", st, cudaGetErrorString(e)); return 1; }
     if (it < 2) continue;
@@ -57,15 +58,19 @@ int main(int argc, char** argv) {
     unsigned long long t0;
     cudaMemcpyFromSymbol(tr.data(), nf::g_gemm_trace, sizeof(unsigned long long) * 148 * 8);
     cudaMemcpyFromSymbol(&t0, g_stamp, sizeof(t0));
-    printf("G=%d T=%d K=%d N=%d workspace=%lld\n", G, T, K, N, (long long)ws_bytes);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("G=%d T=%d K=%d N=%d act=%d res=%d workspace=%lld  kernel %.2f us  %.1f TFLOP/s\n", G, T, K,
+           N, act, res != nullptr, (long long)ws_bytes, ms * 1e3,
+           2.0 * G * T * K * N / (ms * 1e-3) / 1e12);
     {
       std::vector<unsigned long long> wt(148 * 8);
       cudaMemcpyFromSymbol(wt.data(), nf::g_gemm_wait, sizeof(unsigned long long) * 148 * 8);
-      const char* wn[4] = {"prod<-empty", "mma<-full", "mma<-tempty", "epi<-tfull"};
-      for (int s = 0; s < 4; ++s) {
+      const char* wn[5] = {"prod<-empty", "mma<-full", "mma<-tempty", "epi<-tfull", "epi busy"};
+      for (int s = 0; s < 5; ++s) {
         double tot = 0, mx = 0;
         for (int b = 0; b < 148; ++b) { tot += wt[b * 8 + s]; mx = std::max(mx, double(wt[b * 8 + s])); }
-        printf("  wait %-12s mean %8.2f us  max %8.2f us (summed over 3 runs)\n", wn[s], tot / 148 * 1e-3, mx * 1e-3);
+        printf("  wait %-12s mean %8.2f us  max %8.2f us (summed over 3 runs; mma/epi rows: lane 0 / thread 0 only)\n", wn[s], tot / 148 * 1e-3, mx * 1e-3);
       }
     }
     for (int s = 0; s < 8; ++s) {
