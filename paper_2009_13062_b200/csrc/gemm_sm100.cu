@@ -98,9 +98,11 @@ static LinearPlan plan_linear(int64_t G, int64_t T, int64_t K, int64_t N, int64_
 bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
   if (G < 1 || K % 8 || N % 8 || G > 65535) return false;
   const LinearPlan L = plan_linear(G, T, K, N, 0);
-  // (token-row tiles at large T use the separate TMA-ring norm: measured
-  // faster there, XLNet N=32 B=4 4.39 vs 4.98 ms, BERT N=32 B=8 7.28 vs 8.09)
-  return L.swap && !L.pair && L.bn == 128 && GemmOut<128, true>::kStaged && N % 128 == 0;
+  // Swapped 128-token tiles only (batch 1). Token-row tiles at large T were
+  // built and measured twice (per-row statistics from the epilogue
+  // registers): the extra epilogue work outweighs the saved norm launches
+  // there (BERT N=32 B=8 7.21 -> 8.06 ms, XLNet N=32 B=4 4.28 -> 4.93 ms).
+  return L.swap && L.bn == 128 && GemmOut<128, true>::kStaged && N % 128 == 0;
 }
 
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {

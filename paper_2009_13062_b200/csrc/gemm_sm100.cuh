@@ -194,7 +194,9 @@ struct GemmCfg {
       : BN >= 256 ? (PAIR ? 225 : 220)
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
+  // two accumulator buffers; tcgen05.alloc takes a power of two >= 32
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                   : 2 * BN <= 256 ? 256 : 512;
   // folded-LN per-token (mean, rstd) of the B operand and of the residual
 #ifndef NF_FOLD_SMEM
 #define NF_FOLD_SMEM 1
@@ -296,8 +298,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* rbar = tempty + 2;
-  uint64_t* hbar = rbar + 1;  // [2] halo buffers (GATHER == 1)
+  uint64_t* rbar = tempty + 2;  // [2] residual tile (per epilogue half on token-row tiles)
+  uint64_t* hbar = rbar + 2;  // [2] halo buffers (GATHER == 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hbar + 2);
   volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
   float* sNorm = reinterpret_cast<float*>(sOut + C::kOutBytes + 512);  // C::kNormBytes
@@ -317,7 +319,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     tma_prefetch_desc(&map_b);
     if (C::kStaged) tma_prefetch_desc(&map_y);
     if (kResTma) tma_prefetch_desc(&map_r);
-    mbar_init(rbar, 1);
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
     mbar_init(&hbar[0], 1);
     mbar_init(&hbar[1], 1);
     for (int s = 0; s < kStages; ++s) {
@@ -486,6 +489,18 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     // like the producer's operand loads.
     if (kResTma || (kFold && (p.nin_stats || p.nres_stats))) grid_dependency_wait();
     const uint32_t stage_base = smem_u32(sOut);
+    // Token-row staged tiles store progressively: each half of the epilogue
+    // warps (4 warps = 128 rows x kColsPerThread columns) TMA-stores every
+    // 64-column block as soon as its rows are staged, so the stores stream
+    // out while the next block's math runs, and the staging of the next unit
+    // waits only for this half's own stores (no whole-tile read-out between
+    // units: that serialisation cost ~35% of the short-K GEMMs at large T).
+    constexpr bool kProg = !SWAP && C::kStaged;
+    constexpr int kHalfBlocks = kColsPerThread / kOutBlock;
+    static_assert(!kProg || kColsPerThread % kOutBlock == 0, "half = whole 64-column blocks");
+    const int half = (warp - 2) >> 2;
+    const bool issuer = (etid & 127) == 0;
+    uint64_t* my_rbar = kProg ? &rbar[half] : &rbar[0];
     uint32_t res_phase = 0;
     int local = 0;
     // Hand an accumulator buffer back to the MMA issuer (the leader's barrier
@@ -509,15 +524,21 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       // store has finished reading the staging buffer: bulk_wait_read0 +
       // barrier at the end of the unit) and the folded-LN statistics.
       auto issue_residual = [&]() {
-        if (etid == 0) {
+        if constexpr (kProg) {
+          if (issuer) {  // this half's blocks (its previous stores were read)
+            const int m0r = c.ta * kRowsA + int(rank) * kGemmBM, n0r = c.tb * BN;
+            mbar_arrive_expect_tx(my_rbar, kHalfBlocks * kGemmBM * 128);
+#pragma unroll
+            for (int i = 0; i < kHalfBlocks; ++i) {
+              const int b = half * kHalfBlocks + i;
+              tma_load_3d(sOut + b * kGemmBM * 128, &map_r, my_rbar, n0r + b * kOutBlock, m0r,
+                          c.g, kEvictFirst);
+            }
+          }
+        } else if (etid == 0) {
           const int m0r = c.ta * kRowsA + int(rank) * kGemmBM, n0r = c.tb * BN;
           mbar_arrive_expect_tx(rbar, C::kOutBytes);
-          if (!SWAP) {
-#pragma unroll
-            for (int b = 0; b < BN / kOutBlock; ++b)
-              tma_load_3d(sOut + b * kGemmBM * 128, &map_r, rbar, n0r + b * kOutBlock, m0r, c.g,
-                          kEvictFirst);
-          } else if constexpr (KPT > 1) {
+          if constexpr (KPT > 1) {
             // 4-D map (64, T, N/64, G): the tile's two 64-feature blocks in one box
             tma_load_4d(sOut, &map_r, rbar, 0, n0r, m0r / kOutBlock, c.g, kEvictFirst);
           } else {
@@ -528,6 +549,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           }
         }
       };
+      if constexpr (kProg) {
+        // this half's staging blocks are free once its previous stores read them
+        if (issuer) bulk_wait_read0();
+        if constexpr (!kResTma) named_bar_sync(3 + half, 128);
+      }
       if constexpr (kResTma && kResEarly) issue_residual();
       if constexpr (kFold) {
         if (fold_in || fold_res) {
@@ -551,6 +577,18 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           named_bar_sync(1, kEpiThreads);
         }
       }
+      // token-row tiles: the bias of the next 32 columns, one value per lane
+      // (broadcast to the row threads by shuffles), loaded a chunk ahead --
+      // the first during the main loop: a bias load issued right before its
+      // use was the epilogue's top stall (long scoreboard), and a register
+      // per lane fits where a float4 x 8 per thread would spill.
+      constexpr bool kBiasAhead = !SWAP && EC == 32;
+      float bpre = 0.f;
+      auto bias_chunk = [&](int cc_) {
+        const int f = c.tb * BN + cc_ + lane;
+        bpre = (p.bias && f < p.rows_b) ? __ldg(p.bias + int64_t(c.g) * p.features + f) : 0.f;
+      };
+      if constexpr (kBiasAhead) bias_chunk(((warp - 2) >> 2) * kColsPerThread);
       // swapped tiles: this thread's feature row constants, loaded ahead too
       float hb = 0.f, hcs = 0.f, hgm = 0.f, hbt = 0.f;
       if constexpr (SWAP) {
@@ -573,6 +611,26 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       NF_WAIT_BEGIN();  // epilogue busy: accumulator ready -> buffer released
       if constexpr (kResTma && !kResEarly) issue_residual();
       tc_fence_after();
+#if defined(NF_EPI_EXP) && NF_EPI_EXP > 0
+      if constexpr (!SWAP && !GATHER) {  // epilogue cost experiment (tools/)
+        if (NF_EPI_EXP == 2) {
+          uint32_t rr[EC];
+          const uint32_t tr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+          for (int cc = col0; cc < col0 + kColsPerThread; cc += EC) {
+            tmem_ld_cols<EC>(tr + uint32_t(cc), rr);
+            tmem_ld_wait();
+            if (rr[0] == 0x7fffffffu && rr[EC - 1] == 1u) p.counters[0] = rr[3];
+          }
+        }
+        if constexpr (kResTma) {
+          mbar_wait(my_rbar, res_phase);
+          res_phase ^= 1u;
+        }
+        release_acc(acc);
+        named_bar_sync(1, kEpiThreads);
+        continue;
+      }
+#endif
       if (etid == 0 && local == 0) NF_TRACE(4);
       const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
       const int m0 = c.ta * kRowsA + int(rank) * kGemmBM, n0 = c.tb * BN;
@@ -599,7 +657,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         if (!*last_flag) {
           release_acc(acc);
           if constexpr (kResTma) {
-            mbar_wait(rbar, res_phase);  // its residual tile landed unused
+            mbar_wait(my_rbar, res_phase);  // its residual tile landed unused
             res_phase ^= 1u;
           }
           continue;
@@ -611,7 +669,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                         int64_t(c.g) * p.out_gstride
                   : nullptr;
       if constexpr (kResTma) {
-        mbar_wait(rbar, res_phase);  // issued before the accumulator wait
+        mbar_wait(my_rbar, res_phase);  // issued before the accumulator wait
         res_phase ^= 1u;
       }
       const float* bias = p.bias ? p.bias + int64_t(c.g) * p.features : nullptr;
@@ -637,6 +695,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         for (int j = 0; j < EC; ++j) v[j] = __uint_as_float(rnext[j]);
         if (kLdAhead && cc + EC < col0 + kColsPerThread)
           tmem_ld_cols<EC>(t_row + uint32_t(cc + EC), rnext);
+        float bcur = 0.f;
+        if constexpr (kBiasAhead) {
+          bcur = bpre;
+          if (cc + EC < col0 + kColsPerThread) bias_chunk(cc + EC);
+        }
         if (p.splits > 1) {
           // Deterministic reduction: splits summed in index order.
           float sum[EC];
@@ -659,7 +722,21 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           // Thread = token row; EC consecutive features n0+cc ...
           const int tok = m0 + row;
           const int f0 = n0 + cc;
-          if (bias) {
+#if defined(NF_EPI_EXP) && NF_EPI_EXP == 4
+          if (true) {
+#pragma unroll
+            for (int q = 0; q < EC / 8; ++q)
+              st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM),
+                           pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                           pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+            if (kLdAhead) tmem_ld_wait();
+            continue;
+          }
+#endif
+          if (kBiasAhead && bias) {
+#pragma unroll
+            for (int j = 0; j < EC; ++j) v[j] += __shfl_sync(0xffffffffu, bcur, j);
+          } else if (bias) {
             if (f0 + EC <= p.rows_b) {
 #pragma unroll
               for (int j = 0; j < EC; j += 4) {
@@ -793,15 +870,35 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
             }
           }
         }
+        if constexpr (kProg) {
+          if ((cc + EC - col0) % kOutBlock == 0) {
+            // this half finished a 64-column block: store it now
+            fence_proxy_async_smem();
+            named_bar_sync(3 + half, 128);
+            if (issuer) {
+              const int b = (cc + EC) / kOutBlock - 1;
+#if !(defined(NF_EPI_EXP) && NF_EPI_EXP == 3)
+              tma_store_3d(&map_y, sOut + b * kGemmBM * 128, n0 + b * kOutBlock, m0, c.g);
+#endif
+              bulk_commit();
+            }
+          }
+        }
         if constexpr (kLdAhead) tmem_ld_wait();  // the next chunk's columns have landed
       }
       // All TMEM reads of this buffer are done: hand it back to the MMA warp.
       if (etid == 0) NF_WAIT_END(4);
       release_acc(acc);
-      if constexpr (C::kStaged) {
+      if constexpr (kProg) {
+        if (p.splits > 1 && etid == 0) p.counters[wtile] = 0u;  // re-arm for the next launch
+      } else if constexpr (C::kStaged) {
         fence_proxy_async_smem();
         named_bar_sync(1, kEpiThreads);
+#if defined(NF_EPI_EXP) && NF_EPI_EXP == 3
+        if (false) {
+#else
         if (etid == 0) {
+#endif
           if (!SWAP) {
 #pragma unroll
             for (int b = 0; b < BN / kOutBlock; ++b)
@@ -819,42 +916,51 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         if constexpr (kFold) {
           if (p.nout_stats) {
             // LN statistics of token t over this tile's 128 features, from the
-            // bf16 values just staged (what the consumer will read): the sum,
-            // then the centred sum of squares about this part's mean (second
-            // pass over smem). Lane pair (2t, 2t+1) takes token t's two
-            // 64-feature blocks; the swizzle spreads each 16-byte chunk read
-            // over all banks.
+            // bf16 values just staged (what the consumer will read), in one
+            // pass of shifted sums: with the shift c = the token's first
+            // feature, S1 = sum(x - c), S2 = sum((x - c)^2), the part's sum is
+            // S1 + 128 c and its centred M2 = S2 - S1^2 / 128. |x - c| is on
+            // the scale of the spread, not of the mean, so the subtraction
+            // does not cancel when |mean| >> std (no E[x^2] - mean^2).
+            // Lane pair (2t, 2t+1) takes token t's two 64-feature blocks; the
+            // swizzle spreads each 16-byte chunk read over all banks.
             constexpr int kBlocks = kGemmBM / kOutBlock;  // 2
             constexpr int kPerTok = kEpiThreads / BN;      // threads per token
             static_assert(kPerTok == 1 || kPerTok == kBlocks, "stats split");
             const int t = kPerTok == 1 ? etid : etid >> 1;
-            auto stat_pass = [&](float mean, bool centred) {
-              float acc = 0.f;
-              if (t < BN) {
+            float s1 = 0.f, s2 = 0.f, shift = 0.f;
+            if (t < BN) {
+              uint16_t h0;
+              asm volatile("ld.shared.u16 %0, [%1];"
+                           : "=h"(h0)
+                           : "r"(stage_base + uint32_t(t * 128) + (uint32_t(t & 7) << 4)));
+              shift = __uint_as_float(uint32_t(h0) << 16);  // feature 0 of token t
 #pragma unroll
-                for (int bb = 0; bb < kBlocks / kPerTok; ++bb) {
-                  const int b = kPerTok == 1 ? bb : (etid & 1);
+              for (int bb = 0; bb < kBlocks / kPerTok; ++bb) {
+                const int b = kPerTok == 1 ? bb : (etid & 1);
 #pragma unroll
-                  for (int q = 0; q < 8; ++q) {
-                    uint32_t w4[4];
-                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
-                                 : "r"(stage_base + uint32_t(b * BN * 128 + t * 128) +
-                                       (uint32_t(q ^ (t & 7)) << 4)));
+                for (int q = 0; q < 8; ++q) {
+                  uint32_t w4[4];
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(w4[0]), "=r"(w4[1]), "=r"(w4[2]), "=r"(w4[3])
+                               : "r"(stage_base + uint32_t(b * BN * 128 + t * 128) +
+                                     (uint32_t(q ^ (t & 7)) << 4)));
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                      const float lo = __uint_as_float(w4[e] << 16) - mean;
-                      const float hi = __uint_as_float(w4[e] & 0xffff0000u) - mean;
-                      acc = centred ? fmaf(lo, lo, fmaf(hi, hi, acc)) : acc + (lo + hi);
-                    }
+                  for (int e = 0; e < 4; ++e) {
+                    const float lo = __uint_as_float(w4[e] << 16) - shift;
+                    const float hi = __uint_as_float(w4[e] & 0xffff0000u) - shift;
+                    s1 += lo + hi;
+                    s2 = fmaf(lo, lo, fmaf(hi, hi, s2));
                   }
                 }
               }
-              if constexpr (kPerTok > 1) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-              return acc;
-            };
-            const float s = stat_pass(0.f, false);
-            const float m2 = stat_pass(s * (1.0f / float(kGemmBM)), true);
+            }
+            if constexpr (kPerTok > 1) {
+              s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+              s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+            }
+            const float s = fmaf(float(kGemmBM), shift, s1);
+            const float m2 = fmaxf(s2 - s1 * s1 * (1.0f / float(kGemmBM)), 0.f);
             if (t < BN && (kPerTok == 1 || (etid & 1) == 0) && n0 + t < p.rows_b)
               __stcg(p.nout_stats + (int64_t(c.g) * p.tiles_a + c.ta) * p.rows_b + n0 + t,
                      make_float2(s, m2));
@@ -868,6 +974,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           if (etid == 0) p.counters[wtile] = 0u;
         }
       }
+    }
+    if constexpr (kProg) {
+      if (issuer) bulk_wait_read0();  // the staging must outlive this half's last stores
     }
     if (etid == 0) NF_TRACE(5);
   } else if constexpr (GATHER == 1) {

@@ -995,11 +995,9 @@ class Plan:
             raise ShapeError(f"operands incompatible: {tuple(x.shape)} vs {wsrc.spec.dims}")
         rows = x.numel() // (groups * k_in)
         fast_tc = self.mcode == _lib.NF_MODE_FAST and dt == torch.bfloat16
-        # Folded norms are a win for batch-1 launches (swapped 128-token
-        # tiles). Token-row tiles support them too (kernel-tested), but at
-        # 512-1024 tokens the separate TMA-ring norm is cheaper: XLNet N=32
-        # B=4 4.39 -> 4.98 ms and BERT N=32 B=8 7.28 -> 8.09 ms with folding.
-        fold_ok = fast_tc and self.fuse and self.fold_ln and rows <= 128 and bool(
+        # Folded norms: swapped 128-token tiles (batch 1); the kernel says
+        # where it implements them (nf_linear_fold_supported).
+        fold_ok = fast_tc and self.fuse and self.fold_ln and bool(
             _lib.load().nf_linear_fold_supported(groups, rows, k_in, n_out))
         # an output that may take the residual must have no other reader
         feeds_add = fold_ok and act_user is None and self._only_feeds_add(node.id)

@@ -23,7 +23,10 @@ def _call_linear(x, w_nk, bias, residual, y, act, mode, dtype_code, w_layout=_li
                                      (1, 200, 320, 200), (4, 16, 128, 96), (2, 300, 192, 130),
                                      # CTA-pair tiles: persistent loop, partial pair tiles
                                      (8, 1024, 768, 1024), (3, 700, 256, 512),
-                                     (8, 128, 3072, 768), (5, 100, 512, 1000)])
+                                     (8, 128, 3072, 768), (5, 100, 512, 1000),
+                                     # N = 768 CTA-pair tiles, partial pair tiles
+                                     (4, 512, 768, 768), (3, 700, 384, 1152),
+                                     (32, 1024, 3072, 768)])
 @pytest.mark.parametrize("act", [_lib.NF_ACT_NONE, _lib.NF_ACT_GELU])
 def test_tc_linear_bf16_vs_torch(G, T, K, N, act):
     torch.manual_seed(0)
