@@ -678,7 +678,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       // (the consumer of a just-issued tcgen05.ld was the top stall).
       // (Not in the 448-thread gather kernels: their 128-register budget
       // would spill the second chunk.)
-      constexpr bool kLdAhead = GATHER == 0;
+      // Token-row tiles only: on swapped batch-1 tiles the prefetch measured
+      // slower (BERT-base N=8 B=1 0.653 -> 0.697 ms).
+      constexpr bool kLdAhead = GATHER == 0 && !SWAP;
       uint32_t rnext[EC];
       if constexpr (kLdAhead) {
         tmem_ld_cols<EC>(t_row + uint32_t(col0), rnext);

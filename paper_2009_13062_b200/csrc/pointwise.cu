@@ -311,12 +311,18 @@ __global__ void __launch_bounds__(256) k_group_norm(const T* __restrict__ x,
 // flight with 1-D TMA bulk copies into a per-warp shared-memory ring, so the
 // registers hold only the affine (kept until the per-instance affine block
 // changes) and the row being reduced. HBM-bound: 2 reads + 1 write.
-constexpr int kNormDepth = 4;
-constexpr int kNormWarps = 8;
+#ifndef NF_NORM_DEPTH
+#define NF_NORM_DEPTH 4
+#endif
+#ifndef NF_NORM_WARPS
+#define NF_NORM_WARPS 8
+#endif
+constexpr int kNormDepth = NF_NORM_DEPTH;
+constexpr int kNormWarps = NF_NORM_WARPS;
 constexpr int kNormRowBytes = 1536;  // Cg <= 768 bf16
 
 template <int Q>
-__global__ void __launch_bounds__(kNormWarps * 32, 2)
+__global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
     k_group_norm_tma(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
                      const float* __restrict__ gamma, const float* __restrict__ beta,
                      __nv_bfloat16* __restrict__ y, NormGeom g, int units_per_warp) {
@@ -478,13 +484,16 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
     auto* pr = static_cast<const __nv_bfloat16*>(residual);
     auto* py = static_cast<__nv_bfloat16*>(y);
     const int q = int((g.Cg / 8 + 31) / 32);
-    if (vec && q <= 3 && units >= 4 * 148 * 16) {
+#ifndef NF_NORM_TMA_MIN
+#define NF_NORM_TMA_MIN (4 * 148 * 16)
+#endif
+    if (vec && q <= 3 && units >= NF_NORM_TMA_MIN) {
       // enough rows for each warp of 2 resident blocks per SM to stream several
       static SmemAttrOnce attr1, attr2, attr3;
       attr1.set(k_group_norm_tma<1>, int(kNormTmaSmem));
       attr2.set(k_group_norm_tma<2>, int(kNormTmaSmem));
       attr3.set(k_group_norm_tma<3>, int(kNormTmaSmem));
-      const int warps = 148 * 2 * kNormWarps;
+      const int warps = 148 * 16;  // 2 x 8 or 1 x 16 warps per SM
       const int per = int((units + warps - 1) / warps);
       const int nw = int((units + per - 1) / per);
       const int sgrid = (nw + kNormWarps - 1) / kNormWarps;

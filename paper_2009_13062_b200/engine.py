@@ -667,6 +667,10 @@ class Plan:
                 "nf_grouped_conv2d", xp, wp, bp, None, rp, yp, n, c, h, wd, cout, k, s, pad,
                 groups, relu, dcode, _lib.NF_MODE_FAST, st))
             return DVal(y, (n, cout, ho, wo))
+        if (k, s, pad) == (7, 2, 3) and cg <= 4 and h % 2 == 0 and wd % 2 == 0 \
+                and coutg % 4 == 0 and ho == h // 2 and wo == wd // 2:
+            return self._lower_stem_s2d(ch, v, key, folded, other, relu, groups, cg, coutg,
+                                        (n, c, h, wd), (cout, ho, wo))
         cg_pad = cg if cg % 4 == 0 else -(-cg // 4) * 4  # stem: 3 -> 4 channels
         if coutg % 4:
             cg_pad = cg  # direct kernel below reads the unpadded layout
@@ -745,6 +749,54 @@ class Plan:
             self._emit(conv.id, lambda st: _lib.call(
                 "nf_conv_nhwc_direct", xp, wp, bp, rp, yp, n, h, wd, c, cout, groups, k, s, pad,
                 relu, _lib.NF_BF16, st))
+        return DVal(yn.permute(0, 3, 1, 2), (n, cout, ho, wo))
+
+    def _lower_stem_s2d(self, ch, v, key, folded, other, relu, groups, cg, coutg, in_dims,
+                        out_dims) -> DVal:
+        """The 7x7 / stride-2 / pad-3 stem (RGB, 3 channels per instance) as a
+        4x4 / stride-1 conv over a space-to-depth input: s2d pixel (i, j) of
+        group g holds channels [(bh*2 + bw)*4 + c] = x[2i + bh, 2j + bw, c]
+        (c < 3, 16 per group: 16-byte gather rows and the halo-box path
+        instead of 8-byte per-tap gathers of 4-channel pixels), behind one
+        explicit zero row / column so the kernel's symmetric pad 1 gives the
+        stem's top/left pad of 3 input pixels. Weights: W'[o][a][a'][(bh, bw,
+        c)] = W[o][2a+bh-1][2a'+bw-1][c] (zero where that tap is outside the
+        7x7 window). Same products as the direct stem, summed in another order."""
+        conv = ch["conv"]
+        n, c, h, wd = in_dims
+        cout, ho, wo = out_dims
+        dt = v.dtype
+        hs, ws_ = h // 2 + 1, wd // 2 + 1
+        src = v.t if v.split is None else self._materialize(conv.id, v)
+        if not src.is_contiguous():
+            src = self._materialize(conv.id, v)
+        xs = self._own(torch.zeros((n, hs, ws_, groups * 16), dtype=dt, device=self.device))
+        # one strided copy: (n, g, c, i, bh, j, bw) -> s2d channel (bh*2 + bw)*4 + c
+        gs = groups * 16
+        src_v = src.reshape(n, groups, cg, h // 2, 2, wd // 2, 2)
+        dst_v = xs.as_strided(src_v.shape, (hs * ws_ * gs, 16, 1, ws_ * gs, 8, gs, 4),
+                              xs.storage_offset() + (ws_ + 1) * gs)
+        self._copy_step(conv.id, src_v, dst_v)
+        wkey = key + ("s2d",)
+        if wkey not in self._wcache:
+            wf, bias = folded()  # (Cout, 7, 7, cg) fp32
+            wp = torch.zeros((cout, 8, 8, 4), dtype=torch.float32, device=self.device)
+            wp[:, 1:, 1:, :cg] = wf
+            w4 = wp.view(cout, 4, 2, 4, 2, 4).permute(0, 1, 3, 2, 4, 5).reshape(cout, 256)
+            self._wcache[wkey] = (w4.reshape(groups, coutg, 256).to(dt).contiguous(),
+                                  bias.contiguous())
+        wg, bg = self._wcache[wkey]
+        yn = self._alloc((n, ho, wo, cout), dt)
+        rn = self._nhwc(conv.id, other) if other is not None else None
+        rp = rn.data_ptr() if rn is not None else None
+        need = int(_lib.load().nf_conv_workspace_bytes(n, hs, ws_, gs, cout, groups, 4, 1, 1,
+                                                       256))
+        wsb = self._ws_buffer(need) if need > 0 else None
+        wsp, wsn = (wsb.data_ptr(), wsb.numel()) if wsb is not None else (None, 0)
+        xp, wp_, bp, yp = xs.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
+        self._emit(conv.id, lambda st: _lib.call(
+            "nf_grouped_conv_tc", xp, wp_, bp, rp, yp, n, hs, ws_, gs, cout, groups, 4, 1, 1,
+            256, relu, wsp, wsn, st))
         return DVal(yn.permute(0, 3, 1, 2), (n, cout, ho, wo))
 
     def _lower_conv_tf32(self, ch, v, key, folded, other, relu, groups, cg, coutg, k, s, pad,

@@ -25,7 +25,6 @@ def main():
     ap.add_argument("--instances", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-heads", action="store_true")
-    ap.add_argument("--prefetch", action="store_true")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
     ap.add_argument("--no-pdl", action="store_true",
                     help="serialise kernels (NF_PDL=0) so per-kernel durations are exact")
@@ -35,7 +34,7 @@ def main():
         os.environ["NF_PDL"] = "0"
     _, _, inputs, merged, mstore, _ = bench.build_workload(
         args.model, args.instances, args.batch, "bf16", 0, heads=not args.no_heads)
-    plan = compile_plan(merged.graph, mstore, prefetch=args.prefetch)
+    plan = compile_plan(merged.graph, mstore)
     plan.load_inputs(merged.bind_inputs(inputs))
     g = plan.capture()
     for _ in range(5):
