@@ -211,6 +211,12 @@ def linear_launch_bytes(merged, mstore, step_ids=None) -> dict[str, tuple[int, i
             pix = y.dims[0] * y.dims[2] * y.dims[3]
             b = (math.prod(w.dims) + math.prod(x.dims) + math.prod(y.dims)) * esz
             out[n.id] = (b, 2 * pix * math.prod(w.dims))
+    # chained launches (engine._ChainStep, id "chain:a+b+c"): their members' sum
+    for sid in step_ids or ():
+        if sid.startswith("chain:"):
+            mem = sid[len("chain:"):].split("+")
+            if all(m in out for m in mem):
+                out[sid] = (sum(out[m][0] for m in mem), sum(out[m][1] for m in mem))
     return out
 
 

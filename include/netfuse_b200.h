@@ -201,6 +201,49 @@ int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void*
                           int64_t d_model, int64_t heads, float scale, const float* in_stats,
                           int in_parts, const float* in_colsum, float in_eps, void* stream);
 
+/*
+ * Chained batch-1 merged Linears: n_ops (1..3) consecutive merged-Linear
+ * nodes of one instance-packed model -- e.g. a BERT layer's attention
+ * projection -> FF1 (+GELU) -> FF2, each the reference's `batch_matmul`
+ * (engine.py:215-235) with the fused epilogue / folded LayerNorm operands of
+ * nf_grouped_linear_fold -- in ONE persistent launch. Op j's units of
+ * instance g start once op j-1 has stored all of g's output tiles; weight
+ * tiles are requested before that, so the weight stream never pauses at an op
+ * boundary. Results are bit-identical to calling nf_grouped_linear_fold per
+ * op. Every op must satisfy nf_linear_chain_supported (the swapped 128-token
+ * tile of batch-1 shapes: k % 64 == 0,
+ * n % 128 == 0) and take at most one of the in_/res_ folds. `counters` holds
+ * nf_linear_chain_counter_bytes(n_ops, groups) bytes, zeroed once; the
+ * kernel leaves them zeroed (replayable). Each op's workspace enables its
+ * split-K exactly as for nf_grouped_linear_ws.
+ */
+typedef struct nf_linear_op {
+  const void* x;
+  int64_t x_ld, x_gs;
+  const void* w;
+  const float* bias;
+  const void* residual;
+  void* y;
+  int64_t y_ld, y_gs, rows, k, n;
+  int act;
+  void* workspace;
+  int64_t workspace_bytes;
+  const float* in_stats;
+  int in_parts;
+  const float* in_colsum;
+  float in_eps;
+  const float* res_stats;
+  int res_parts;
+  const float* res_gamma;
+  const float* res_beta;
+  float res_eps;
+  float* out_stats;
+} nf_linear_op;
+int nf_linear_chain_supported(int64_t groups, int64_t rows, int64_t k, int64_t n);
+int64_t nf_linear_chain_counter_bytes(int n_ops, int64_t groups);
+int nf_grouped_linear_chain(int n_ops, const nf_linear_op* ops, int64_t groups, void* counters,
+                            void* stream);
+
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream);

@@ -56,6 +56,9 @@ SIGNATURES: dict[str, list] = {
                                _i64, _i, _p, _i64, _p, _i, _p, _f, _p, _i, _p, _p, _f, _p, _p],
     "nf_qkv_attention_fold": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f,
                               _p, _i, _p, _f, _p],
+    "nf_linear_chain_supported": [_i64, _i64, _i64, _i64],
+    "nf_linear_chain_counter_bytes": [_i, _i64],
+    "nf_grouped_linear_chain": [_i, _p, _i64, _p, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],
@@ -70,7 +73,20 @@ SIGNATURES: dict[str, list] = {
 
 _RESTYPES = {"nf_status_string": ctypes.c_char_p, "nf_linear_workspace_bytes": ctypes.c_int64,
              "nf_conv_workspace_bytes": ctypes.c_int64,
-             "nf_conv_tf32_workspace_bytes": ctypes.c_int64}
+             "nf_conv_tf32_workspace_bytes": ctypes.c_int64,
+             "nf_linear_chain_counter_bytes": ctypes.c_int64}
+
+
+class LinearOp(ctypes.Structure):
+    """`nf_linear_op` (include/netfuse_b200.h): one op of a chained launch."""
+    _fields_ = [
+        ("x", _p), ("x_ld", _i64), ("x_gs", _i64), ("w", _p), ("bias", _p), ("residual", _p),
+        ("y", _p), ("y_ld", _i64), ("y_gs", _i64), ("rows", _i64), ("k", _i64), ("n", _i64),
+        ("act", _i), ("workspace", _p), ("workspace_bytes", _i64),
+        ("in_stats", _p), ("in_parts", _i), ("in_colsum", _p), ("in_eps", _f),
+        ("res_stats", _p), ("res_parts", _i), ("res_gamma", _p), ("res_beta", _p),
+        ("res_eps", _f), ("out_stats", _p),
+    ]
 
 _lib: ctypes.CDLL | None = None
 

@@ -217,6 +217,35 @@ int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void*
                               static_cast<cudaStream_t>(stream), &fold);
 }
 
+int nf_linear_chain_supported(int64_t groups, int64_t rows, int64_t k, int64_t n) {
+  return nf::linear_chain_supported(groups, rows, k, n) ? 1 : 0;
+}
+
+int64_t nf_linear_chain_counter_bytes(int n_ops, int64_t groups) {
+  if (n_ops < 1 || groups < 1) return 0;
+  return (int64_t(n_ops) * groups + 1) * int64_t(sizeof(unsigned));
+}
+
+int nf_grouped_linear_chain(int n_ops, const nf_linear_op* ops, int64_t groups, void* counters,
+                            void* stream) {
+  if (!ops || !counters || n_ops < 1 || n_ops > 3 || groups < 1) return NF_ERR_SHAPE;
+  nf::LinearOpDesc d[3];
+  for (int j = 0; j < n_ops; ++j) {
+    const nf_linear_op& o = ops[j];
+    if (o.rows < 1 || o.k < 1 || o.n < 1 || o.x_ld < o.k || o.y_ld < o.n) return NF_ERR_SHAPE;
+    if (groups > 1 && (o.x_gs < 1 || o.y_gs < 1)) return NF_ERR_SHAPE;
+    if (o.act < NF_ACT_NONE || o.act > NF_ACT_TANH) return NF_ERR_UNSUPPORTED;
+    d[j] = nf::LinearOpDesc{o.x, o.x_ld, o.x_gs, o.w, o.bias, o.residual, o.y, o.y_ld, o.y_gs,
+                            groups, o.rows, o.k, o.n, o.act, o.workspace, o.workspace_bytes,
+                            (o.in_stats || o.res_stats || o.out_stats) ? 1 : 0,
+                            nf::NormFold{o.in_stats, o.in_colsum, o.in_parts, o.in_eps,
+                                         o.res_stats, o.res_gamma, o.res_beta, o.res_parts,
+                                         o.res_eps, o.out_stats}};
+  }
+  return nf::grouped_linear_chain_tc(n_ops, d, static_cast<unsigned*>(counters),
+                                     static_cast<cudaStream_t>(stream));
+}
+
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream) {
   if (!x || !y || N < 1 || H < 1 || W < 1 || C < 1) return NF_ERR_SHAPE;

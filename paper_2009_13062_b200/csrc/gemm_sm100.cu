@@ -1,6 +1,6 @@
 // Merged Linear host entry (tcgen05 grouped GEMM; kernel in gemm_sm100.cuh).
 // Replaces the reference's `batch_matmul` (pkg/src/modelmerge/engine.py:215-235).
-#include "gemm_sm100.cuh"
+#include "gemm_chain.cuh"
 
 namespace nf {
 
@@ -112,20 +112,17 @@ int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
   return kCounterBytes + cta_tiles * L.splits * int64_t(kGemmBM) * L.bn * 4;
 }
 
-// Entry used by the C ABI. x rows at x + g*x_gs + t*x_ld (bf16); w (G, N, K)
-// K-major bf16; bias fp32 (G, N) or null; y / residual rows at
-// y + g*y_gs + t*y_ld (bf16). `ws` (zero-initialised once; the kernel
-// restores its semaphores) enables split-K; null disables it.
-int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
-                      const float* bias, const void* residual, void* y, int64_t y_ld,
-                      int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
-                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const NormFold* fold) {
+// Validation and kernel parameters of one merged Linear (shared by the
+// single-op entry and the chained launch).
+static int linear_setup(const void* ws, int64_t ws_bytes, int64_t G, int64_t T, int64_t K,
+                        int64_t N, int out_dtype, int act, const float* bias,
+                        const void* residual, void* y, int64_t y_ld, int64_t y_gs,
+                        const NormFold* fold, GemmParams& p, LinearPlan& L) {
   // TMA needs 16-byte aligned row strides for x, w and y.
   if (out_dtype != NF_BF16 || K % 8 != 0 || N % 8 != 0) return NF_ERR_UNSUPPORTED;
   if (G > 65535 || T > (int64_t(1) << 30) || N > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
   if (ws && (reinterpret_cast<uintptr_t>(ws) & 255)) return NF_ERR_SHAPE;
-  GemmParams p{};
+  p = GemmParams{};
   p.act = act;
   p.bias = bias;
   p.residual = residual;
@@ -135,7 +132,7 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
   p.groups = int(G);
   p.y_direct = y;
   p.kb_total = int((K + kGemmBK - 1) / kGemmBK);
-  const LinearPlan L = plan_linear(G, T, K, N, ws ? ws_bytes : 0);
+  L = plan_linear(G, T, K, N, ws ? ws_bytes : 0);
   if (fold) {
     if (!linear_fold_supported(G, T, K, N)) return NF_ERR_UNSUPPORTED;
     if ((fold->in_stats && (!fold->in_colsum || fold->in_parts < 1)) ||
@@ -155,6 +152,35 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
     p.nres_eps = fold->res_eps;
     p.nout_stats = reinterpret_cast<float2*>(fold->out_stats);
   }
+  p.rows_a = int(L.swap ? N : T);
+  p.rows_b = int(L.swap ? T : N);
+  p.tiles_a = int(L.tiles_a);
+  p.tiles_b = int(L.tiles_b);
+  p.splits = L.splits;
+  p.kb_per_split = (p.kb_total + p.splits - 1) / p.splits;
+  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  if (L.tiles * p.splits * 2 > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
+  p.units = int(L.tiles * p.splits);
+  p.counters = static_cast<unsigned*>(const_cast<void*>(ws));
+  p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(const_cast<void*>(ws)) + kCounterBytes)
+            : nullptr;
+  return NF_OK;
+}
+
+// Entry used by the C ABI. x rows at x + g*x_gs + t*x_ld (bf16); w (G, N, K)
+// K-major bf16; bias fp32 (G, N) or null; y / residual rows at
+// y + g*y_gs + t*y_ld (bf16). `ws` (zero-initialised once; the kernel
+// restores its semaphores) enables split-K; null disables it.
+int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                      const float* bias, const void* residual, void* y, int64_t y_ld,
+                      int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
+                      int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
+                      const NormFold* fold) {
+  GemmParams p;
+  LinearPlan L;
+  const int st = linear_setup(ws, ws_bytes, G, T, K, N, out_dtype, act, bias, residual, y, y_ld,
+                              y_gs, fold, p, L);
+  if (st != NF_OK) return st;
   const bool swap = L.swap;
   const int bn = L.bn;
   const int bbox = L.pair ? bn / 2 : bn;  // B rows each CTA loads
@@ -164,31 +190,17 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
         !make_bf16_map(&mb, x, G, T, K, kGemmBK, bbox, x_ld, x_gs) ||
         !make_bf16_map(&my, y, G, T, N, kOutBlock, bn, y_ld, y_gs))
       return NF_ERR_UNSUPPORTED;
-    p.rows_a = int(N);
-    p.rows_b = int(T);
   } else {
     if (!make_bf16_map(&ma, x, G, T, K, kGemmBK, kGemmBM, x_ld, x_gs) ||
         !make_bf16_map(&mb, w, G, N, K, kGemmBK, bbox, 0, 0) ||
         !make_bf16_map(&my, y, G, T, N, kOutBlock, kGemmBM, y_ld, y_gs))
       return NF_ERR_UNSUPPORTED;
-    p.rows_a = int(T);
-    p.rows_b = int(N);
   }
   mr = my;
   if (residual &&
       !(swap ? make_bf16_map(&mr, residual, G, T, N, kOutBlock, bn, y_ld, y_gs)
              : make_bf16_map(&mr, residual, G, T, N, kOutBlock, kGemmBM, y_ld, y_gs)))
     return NF_ERR_UNSUPPORTED;
-  p.tiles_a = int(L.tiles_a);
-  p.tiles_b = int(L.tiles_b);
-  const int64_t tiles = L.tiles;
-  p.splits = L.splits;
-  p.kb_per_split = (p.kb_total + p.splits - 1) / p.splits;
-  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
-  if (tiles * p.splits * 2 > (int64_t(1) << 31) - 1) return NF_ERR_UNSUPPORTED;
-  p.units = int(tiles * p.splits);
-  p.counters = static_cast<unsigned*>(ws);
-  p.ws = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kCounterBytes) : nullptr;
   if (L.pair) {
     const int clusters = p.units < kNumSMs / 2 ? p.units : kNumSMs / 2;
     const int grid = 2 * clusters;
@@ -229,4 +241,69 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
 #undef NF_TC
 }
 
+// Ops the chained launch implements: the swapped 128-token tile with two
+// k-blocks per stage (batch-1 weight-streaming shapes).
+bool linear_chain_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
+  if (G < 1 || G > 65535 || K % 64 || N % 128) return false;
+  const LinearPlan L = plan_linear(G, T, K, N, 0);
+  return L.swap && L.bn == 128;
+}
+
+// Consecutive merged Linears of one instance-packed model in one persistent
+// launch (gemm_chain.cuh). ops[j] reads only what ops[< j] or earlier
+// kernels wrote, instance by instance. `counters` holds n_ops * G + 1 zeroed
+// words; the kernel leaves them zeroed.
+int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counters,
+                            cudaStream_t stream) {
+  if (nops < 1 || nops > kChainMaxOps || !ops || !counters) return NF_ERR_SHAPE;
+  ChainParams cp{};
+  cp.nops = nops;
+  cp.groups = int(ops[0].G);
+  int units = 0;
+  for (int j = 0; j < nops; ++j) {
+    const LinearOpDesc& d = ops[j];
+    if (!d.x || !d.w || !d.y || d.G != ops[0].G) return NF_ERR_SHAPE;
+    if (!linear_chain_supported(d.G, d.T, d.K, d.N)) return NF_ERR_UNSUPPORTED;
+    const NormFold* fold = d.has_fold ? &d.fold : nullptr;
+    if (fold && fold->in_stats && fold->res_stats) return NF_ERR_UNSUPPORTED;
+    ChainOp& o = cp.ops[j];
+    LinearPlan L;
+    const int st = linear_setup(d.ws, d.ws_bytes, d.G, d.T, d.K, d.N, NF_BF16, d.act, d.bias,
+                                d.residual, d.y, d.y_ld, d.y_gs, fold, o.p, L);
+    if (st != NF_OK) return st;
+    if (!make_bf16_map_kpt2(&o.ma, d.w, d.G, d.N, d.K, kGemmBM, 0, 0, 2) ||
+        !make_bf16_map_kpt2(&o.mb, d.x, d.G, d.T, d.K, 128, d.x_ld, d.x_gs, 2) ||
+        !make_bf16_map_kpt2(&o.my, d.y, d.G, d.T, d.N, 128, d.y_ld, d.y_gs, 2))
+      return NF_ERR_UNSUPPORTED;
+    o.mr = o.my;
+    if (d.residual &&
+        !make_bf16_map_kpt2(&o.mr, d.residual, d.G, d.T, d.N, 128, d.y_ld, d.y_gs, 2))
+      return NF_ERR_UNSUPPORTED;
+    o.unit0 = units;
+    o.dep_tiles = j ? cp.ops[j - 1].p.tiles_a * cp.ops[j - 1].p.tiles_b : 0;
+    if (int64_t(units) + o.p.units > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
+    units += o.p.units;
+  }
+  cp.units = units;
+  cp.done_tiles = counters;
+  cp.exit_count = counters + int64_t(nops) * cp.groups;
+  using C = GemmCfg<128, true, false, 0, 2>;
+  static SmemAttrOnce smem_attr;
+  smem_attr.set(k_linear_chain_tc, int(C::kBytes));
+  const int grid = units < kNumSMs ? units : kNumSMs;
+  return launch_pdl(k_linear_chain_tc, dim3(grid), dim3(64 + 32 * epi_warps<128>()), C::kBytes,
+                    stream, cp) == cudaSuccess
+             ? NF_OK
+             : NF_ERR_LAUNCH;
+}
+
 }  // namespace nf
+
+#ifdef NF_CHAIN_TRACE
+extern "C" int nf_debug_chain_trace(void* host, int bytes) {
+  return int(cudaMemcpyFromSymbol(host, nf::g_chain_trace, size_t(bytes)));
+}
+extern "C" int nf_debug_chain_wtrace(void* host, int bytes) {
+  return int(cudaMemcpyFromSymbol(host, nf::g_chain_wtrace, size_t(bytes)));
+}
+#endif

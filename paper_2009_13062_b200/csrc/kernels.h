@@ -31,6 +31,24 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
                       const NormFold* fold = nullptr);
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
+// One op of a chained launch (same operands as grouped_linear_tc).
+struct LinearOpDesc {
+  const void* x;
+  int64_t x_ld, x_gs;
+  const void* w;
+  const float* bias;
+  const void* residual;
+  void* y;
+  int64_t y_ld, y_gs, G, T, K, N;
+  int act;
+  void* ws;
+  int64_t ws_bytes;
+  int has_fold;
+  NormFold fold;
+};
+bool linear_chain_supported(int64_t G, int64_t T, int64_t K, int64_t N);
+int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counters,
+                            cudaStream_t stream);
 
 // linear_simt.cu — CUDA-core grouped linear (exact reference order or FMA).
 int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,

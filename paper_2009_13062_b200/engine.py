@@ -88,6 +88,35 @@ class _LinearStep:
                   *fin, *fres, self.out_stats, st)
 
 
+class _ChainStep:
+    """Consecutive batch-1 merged Linears of one model run as ONE persistent
+    launch (``nf_grouped_linear_chain``): weight tiles of op j+1 stream while
+    op j finishes, units wait on per-instance completion counters. Built by
+    :meth:`Plan._chain_linears` from finished :class:`_LinearStep` s."""
+
+    def __init__(self, members: list[tuple[str, "_LinearStep"]], counters: torch.Tensor):
+        self.members = members
+        self.counters = counters
+        self.groups = members[0][1].groups
+        ops = (_lib.LinearOp * len(members))()
+        for o, (_, ls) in zip(ops, members):
+            k, n, rows = ls.k, ls.n, ls.rows
+            o.x, o.x_ld, o.x_gs, o.w, o.bias = ls.x, k, rows * k, ls.w, ls.b
+            o.residual, o.y, o.y_ld, o.y_gs = ls.residual, ls.y, n, rows * n
+            o.rows, o.k, o.n, o.act = rows, k, n, ls.act
+            o.workspace, o.workspace_bytes = ls.ws, ls.wsb
+            if ls.fin is not None:
+                o.in_stats, o.in_parts, o.in_colsum, o.in_eps = ls.fin
+            if ls.fres is not None:
+                o.res_stats, o.res_parts, o.res_gamma, o.res_beta, o.res_eps = ls.fres
+            o.out_stats = ls.out_stats
+        self.ops = ops
+
+    def __call__(self, st):
+        _lib.call("nf_grouped_linear_chain", len(self.members), self.ops, self.groups,
+                  self.counters.data_ptr(), st)
+
+
 @dataclass
 class _FoldedNorm:
     """A per-instance LayerNorm that is not launched: ``raw`` (G, T, D) holds
@@ -175,7 +204,7 @@ class Plan:
 
     def __init__(self, graph: Graph, weights: WeightStore, *, mode: str = "fast",
                  device: str | torch.device = "cuda", fuse: bool = True,
-                 fold_ln: bool = True, weight_cache: dict | None = None):
+                 fold_ln: bool = True, chain: bool = True, weight_cache: dict | None = None):
         if mode not in _MODES:
             raise ValueError(f"mode must be one of {sorted(_MODES)}")
         if torch.device(device).type == "cuda" and not torch.cuda.is_available():
@@ -203,6 +232,7 @@ class Plan:
         # Batch-1 LayerNorms folded into their producing / consuming GEMMs (no
         # norm launch; include/netfuse_b200.h "Folded LayerNorm")
         self.fold_ln = fold_ln
+        self.chain = chain
         self._add_into_norm: dict[str, str] = {}
         self._lin_out: dict[int, _LinearStep] = {}  # output data_ptr -> its launch
         self._folded: dict[int, _FoldedNorm] = {}   # out data_ptr -> folded norm (not launched)
@@ -458,6 +488,56 @@ class Plan:
         # the BN-folded fp32 conv weights only fed the kernel layouts above
         for key in [k for k in self._wcache if k[0] == "convchain" and len(k) == 2]:
             del self._wcache[key]
+        if self.fuse and self.chain and self.mcode == _lib.NF_MODE_FAST:
+            self._chain_linears()
+
+    def _chainable(self, ls, run) -> bool:
+        if not isinstance(ls, _LinearStep) or ls.dcode != _lib.NF_BF16 \
+                or ls.layout != _lib.NF_W_NK or ls.mcode != _lib.NF_MODE_FAST:
+            return False
+        if ls.fin is not None and ls.fres is not None:
+            return False
+        if not _lib.load().nf_linear_chain_supported(ls.groups, ls.rows, ls.k, ls.n):
+            return False
+        if not run:
+            return True
+        head = run[0][1]
+        # consumes the previous op's output; at most one op uses split-K
+        # (they would share the plan's workspace)
+        return (ls.groups == head.groups and ls.rows == head.rows and ls.x == run[-1][1].y
+                and not (ls.wsb and any(m.wsb for _, m in run)))
+
+    def _chain_linears(self) -> None:
+        """Merge runs of 2-3 consecutive chainable merged-Linear launches
+        (e.g. attention projection -> FF1 -> FF2 of a batch-1 encoder layer)
+        into one persistent launch each."""
+        out, i, steps = [], 0, self.steps
+        while i < len(steps):
+            run = []
+            while i + len(run) < len(steps) and len(run) < 3:
+                nid, fn, _ = steps[i + len(run)]
+                if not self._chainable(fn, run):
+                    break
+                run.append((nid, fn))
+            if len(run) >= 2:
+                nbytes = int(_lib.load().nf_linear_chain_counter_bytes(len(run), run[0][1].groups))
+                ctr = self._own(torch.zeros(nbytes // 4, dtype=torch.int32, device=self.device))
+                out.append(("chain:" + "+".join(n for n, _ in run), _ChainStep(run, ctr), 1))
+                i += len(run)
+            else:
+                out.append(steps[i])
+                i += 1
+        self.steps = out
+
+    def linear_steps(self) -> dict[str, "_LinearStep"]:
+        """node id -> its merged-Linear launch description (chained or not)."""
+        got = {}
+        for nid, fn, _ in self.steps:
+            if isinstance(fn, _ChainStep):
+                got.update(dict(fn.members))
+            elif isinstance(fn, _LinearStep):
+                got[nid] = fn
+        return got
 
     # ------------------------------------------------------- fusion helpers
     @staticmethod
@@ -1741,11 +1821,11 @@ _PLANS = _PlanCache()
 
 
 def compile_plan(graph: Graph, weights: WeightStore, *, mode: str = "fast",
-                 fuse: bool = True, fold_ln: bool = True) -> Plan:
+                 fuse: bool = True, fold_ln: bool = True, chain: bool = True) -> Plan:
     """Compile ``graph`` with ``weights`` into a caller-owned :class:`Plan`
     (weights converted to kernel layouts in HBM, buffers preallocated).
     Every call builds a new plan: the handle is the cache."""
-    return Plan(graph, weights, mode=mode, fuse=fuse, fold_ln=fold_ln)
+    return Plan(graph, weights, mode=mode, fuse=fuse, fold_ln=fold_ln, chain=chain)
 
 
 def execute(graph: Graph, weights: WeightStore, inputs: dict[str, TensorValue], *,

@@ -23,12 +23,16 @@ def test_bert_glue_is_zero_copy():
     assert OpKind.TRANSPOSE not in kinds and OpKind.RESHAPE not in kinds
     # outputs are views of plan-owned buffers: no copy launch at all
     assert _copies(plan) == 0
-    # per layer at batch 1: qkv+attn (fused), proj(+residual), ff1(+gelu),
-    # ff2(+residual); the LayerNorms are folded into those launches, only the
-    # last one (a graph output) runs as a norm kernel
-    assert len(plan.steps) == 2 * 4 + 1
+    # per layer at batch 1: qkv+attn (fused), then proj(+residual) ->
+    # ff1(+gelu) -> ff2(+residual) chained in one persistent launch; the
+    # LayerNorms are folded into those launches, only the last one (a graph
+    # output) runs as a norm kernel
+    assert len(plan.steps) == 2 * 2 + 1
     ids = [nid for nid, _, _ in plan.steps]
     assert "merged::l00.attn" in ids and "merged::l00.qkv" not in ids
+    assert "chain:merged::l00.proj+merged::l00.ff1+merged::l00.ff2" in ids
+    unchained = Plan(merged.graph, mstore, device="cpu", chain=False)
+    assert len(unchained.steps) == 2 * 4 + 1
     assert not any("res" in nid for nid, _, _ in plan.steps)
     with pytest.raises(UnsupportedOpError):
         plan.launch()
@@ -44,6 +48,7 @@ def test_layernorms_fold_into_neighbouring_linears():
     merged, mstore = merge(graph, stores)
     plan = Plan(merged.graph, mstore, device="cpu")
     st = dict((nid, fn) for nid, fn, _ in plan.steps)
+    st.update(plan.linear_steps())
     # producers add the residual and write the norm statistics
     for nid in ("merged::l00.proj", "merged::l00.ff2", "merged::l01.proj", "merged::l01.ff2"):
         assert st[nid].residual is not None and st[nid].out_stats is not None
@@ -57,11 +62,35 @@ def test_layernorms_fold_into_neighbouring_linears():
     assert [nid for nid in st if ".ln" in nid] == ["merged::l01.ln2"]
 
 
+def test_batch1_linears_chain_only_when_consecutive_and_supported():
+    graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    chains = [fn for _, fn, _ in plan.steps if type(fn).__name__ == "_ChainStep"]
+    assert len(chains) == 2
+    for ch in chains:
+        names = [n.split(".")[-1] for n, _ in ch.members]
+        assert names == ["proj", "ff1", "ff2"]
+        # each op reads the previous op's output
+        for (_, a), (_, b) in zip(ch.members, ch.members[1:]):
+            assert b.x == a.y
+        # the ctypes op table mirrors the launch descriptions
+        assert [o.n for o in ch.ops] == [m.n for _, m in ch.members]
+    # batch 4 (token-row tiles): nothing chains
+    graph, stores = W.build_zoo("bert-2l", num_models=2, batch=4, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    assert not any(nid.startswith("chain:") for nid, _, _ in plan.steps)
+
+
 def test_layernorm_fold_opt_out():
     graph, stores = W.build_zoo("bert-2l", num_models=3, dtype="bf16")
     merged, mstore = merge(graph, stores)
-    plan = Plan(merged.graph, mstore, device="cpu", fold_ln=False)
+    plan = Plan(merged.graph, mstore, device="cpu", fold_ln=False, chain=False)
     assert len(plan.steps) == 2 * 6
+    # unfolded norms split the layer: only ff1 -> ff2 stays consecutive
+    plan = Plan(merged.graph, mstore, device="cpu", fold_ln=False)
+    assert len(plan.steps) == 2 * 5
 
 
 def test_qkv_attention_fusion_needs_batch_one():
@@ -76,7 +105,7 @@ def test_gelu_fused_into_linear_epilogue():
     graph, stores = W.build_zoo("bert-2l", num_models=2, dtype="bf16")
     merged, mstore = merge(graph, stores)
     plan = Plan(merged.graph, mstore, device="cpu")
-    ids = [nid for nid, _, _ in plan.steps]
+    ids = list(plan.linear_steps())
     assert "merged::l00.gelu" not in ids and "merged::l00.ff1" in ids
     assert plan.vals["merged::l00.gelu"] is plan.vals["merged::l00.ff1"]
 
