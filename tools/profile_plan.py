@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--model", default="bert-base")
     ap.add_argument("--instances", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-heads", action="store_true")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
     ap.add_argument("--no-pdl", action="store_true",
@@ -33,7 +34,7 @@ def main():
         import os
         os.environ["NF_PDL"] = "0"
     _, _, inputs, merged, mstore, _ = bench.build_workload(
-        args.model, args.instances, args.batch, "bf16", 0, heads=not args.no_heads)
+        args.model, args.instances, args.batch, args.dtype, 0, heads=not args.no_heads)
     plan = compile_plan(merged.graph, mstore)
     plan.load_inputs(merged.bind_inputs(inputs))
     g = plan.capture()

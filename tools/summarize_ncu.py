@@ -22,7 +22,7 @@ from pathlib import Path
 # the dominant (weight-streaming / tensor) family, as bench.family_roofline
 # defines it: merged Linear + implicit-GEMM conv launches, the fused
 # QKV+attention launch, the fp32 3xTF32 conv
-FAMILY = re.compile(r"k_grouped_gemm_tc|k_qkv_attention_tc|k_conv_tf32|k_linear_tf32")
+FAMILY = re.compile(r"k_grouped_gemm_tc|k_linear_chain_tc|k_qkv_attention_tc|k_conv_tf32|k_linear_tf32")
 OURS = re.compile(r"^(nf::|k_)|nf::")
 SCALE = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
