@@ -409,8 +409,12 @@ def run_ours(args) -> dict | None:
     lin = linear_launch_bytes(merged, mstore, {nid for nid, _, _ in plan.steps})
     roofline = family_roofline(plan, lin, ms_per_step, peaks)
     is_cnn = "res" in args.model
-    roofline["kernel"] = ("k_grouped_gemm_tc (implicit-GEMM merged conv + Linear)" if is_cnn
-                          else "k_grouped_gemm_tc (merged Linear) + k_qkv_attention_tc")
+    chained = any(nid.startswith("chain:") for nid, _, _ in plan.steps)
+    roofline["kernel"] = (
+        ("k_conv_tf32x3 (3xTF32 merged conv) + fp32 heads" if args.dtype == "f32" else
+         "k_grouped_gemm_tc (implicit-GEMM merged conv + Linear)") if is_cnn
+        else "k_linear_chain_tc (chained merged Linears) + k_qkv_attention_tc" if chained
+        else "k_grouped_gemm_tc (merged Linear) + k_qkv_attention_tc")
     roofline["peak_source"] = peak_src
     roofline["traffic"] = _ncu_traffic(args)
     roofline["ncu_share"] = _ncu_share(args)

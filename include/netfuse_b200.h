@@ -206,10 +206,10 @@ int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void*
  * nodes of one instance-packed model -- e.g. a BERT layer's attention
  * projection -> FF1 (+GELU) -> FF2, each the reference's `batch_matmul`
  * (engine.py:215-235) with the fused epilogue / folded LayerNorm operands of
- * nf_grouped_linear_fold -- in ONE persistent launch. Op j's units of
- * instance g start once op j-1 has stored all of g's output tiles; weight
- * tiles are requested before that, so the weight stream never pauses at an op
- * boundary. Results are bit-identical to calling nf_grouped_linear_fold per
+ * nf_grouped_linear_fold -- in ONE persistent launch. ops[j].x must be
+ * ops[j-1].y: op j's units of instance g load activations once op j-1 has
+ * stored all of g's output tiles; weight tiles are requested before that,
+ * so the weight stream never pauses at an op boundary. Results are bit-identical to calling nf_grouped_linear_fold per
  * op. Every op must satisfy nf_linear_chain_supported (the swapped 128-token
  * tile of batch-1 shapes: k % 64 == 0,
  * n % 128 == 0) and take at most one of the in_/res_ folds. `counters` holds

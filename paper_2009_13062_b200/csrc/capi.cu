@@ -223,6 +223,7 @@ int nf_linear_chain_supported(int64_t groups, int64_t rows, int64_t k, int64_t n
 
 int64_t nf_linear_chain_counter_bytes(int n_ops, int64_t groups) {
   if (n_ops < 1 || groups < 1) return 0;
+  // per-(op, instance) tile counters and the exit counter
   return (int64_t(n_ops) * groups + 1) * int64_t(sizeof(unsigned));
 }
 

@@ -10,11 +10,11 @@
 // weight stream. Here the operand ring runs across op boundaries: a unit's
 // WEIGHT tiles (independent of any activation) are requested as soon as ring
 // slots free up, and only its ACTIVATION tiles wait for the producing op.
-// Dependencies are per instance: op j's units of instance g wait until op
-// j-1 has stored all its output tiles of g (a release counter per (op, g),
-// bumped after the tile's TMA store completed); instances never read each
-// other's rows, and everything op j reads from ops < j-1 of the same
-// instance is complete by transitivity.
+// Dependencies are per instance: op j's activation tiles of instance g wait
+// until op j-1 has stored all of g's output tiles (a release counter per
+// (op, g), bumped after each tile's TMA store completed); the epilogue waits
+// likewise for the chain op its residual / LayerNorm statistics come from.
+// Instances never read each other's rows.
 //
 // Forward progress: dependencies point to lower unit indices only and every
 // CTA walks its units in increasing order with its producer at most one unit
@@ -40,7 +40,8 @@ struct alignas(64) ChainOp {
   CUtensorMap ma, mb, my, mr;  // 4-D (64, rows, K/64 | N/64, G) maps, two blocks per box
   GemmParams p;
   int unit0;      // first global unit index of this op
-  int dep_tiles;  // output tiles per instance of the previous op (op > 0)
+  int epi_dep;    // chain op whose results the epilogue reads (residual / LN
+                  // statistics), -1: only earlier kernels
 };
 
 struct ChainParams {
@@ -193,7 +194,14 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
           grid_dependency_wait();
           first = false;
         }
-        if (op > 0) wait_counter(cp.done_tiles + (op - 1) * cp.groups + c.g, unsigned(o.dep_tiles));
+        // Activations of op > 0 are the previous op's output: wait until it
+        // has stored all of this instance's tiles. (Per-tile flags checked
+        // per stage measured slower: a blocking L2 round trip per stage.)
+        if (op > 0) {
+          const ChainOp& d = cp.ops[op - 1];
+          wait_counter(cp.done_tiles + (op - 1) * cp.groups + c.g,
+                       unsigned(d.p.tiles_a * d.p.tiles_b));
+        }
 #ifdef NF_CHAIN_TRACE
         NF_CT(local, 1, chain_clock());
 #endif
@@ -291,9 +299,12 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
       }
       // Everything below reads the producing op's results (residual tile,
       // LN statistics): one thread acquires, the barrier orders the rest.
-      if (op > 0) {
-        if (etid == 0)
-          wait_counter(cp.done_tiles + (op - 1) * cp.groups + c.g, unsigned(o.dep_tiles));
+      if (o.epi_dep >= 0) {
+        if (etid == 0) {
+          const ChainOp& d = cp.ops[o.epi_dep];
+          wait_counter(cp.done_tiles + o.epi_dep * cp.groups + c.g,
+                       unsigned(d.p.tiles_a * d.p.tiles_b));
+        }
         named_bar_sync(1, kEpiThreads);
       }
 #ifdef NF_CHAIN_TRACE

@@ -280,7 +280,18 @@ int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counter
         !make_bf16_map_kpt2(&o.mr, d.residual, d.G, d.T, d.N, 128, d.y_ld, d.y_gs, 2))
       return NF_ERR_UNSUPPORTED;
     o.unit0 = units;
-    o.dep_tiles = j ? cp.ops[j - 1].p.tiles_a * cp.ops[j - 1].p.tiles_b : 0;
+    if (o.p.tiles_b != 1) return NF_ERR_UNSUPPORTED;
+    // the epilogue's inputs: a residual or LN statistics written by an
+    // earlier op of this chain (else by earlier kernels)
+    o.epi_dep = -1;
+    for (int i = 0; i < j; ++i) {
+      const void* out_stats = ops[i].has_fold ? ops[i].fold.out_stats : nullptr;
+      const bool reads = (d.residual && d.residual == ops[i].y) ||
+                         (fold && out_stats &&
+                          (fold->in_stats == out_stats || fold->res_stats == out_stats));
+      if (reads) o.epi_dep = i;
+    }
+    if (j && d.x != ops[j - 1].y) return NF_ERR_UNSUPPORTED;  // activations = previous output
     if (int64_t(units) + o.p.units > (int64_t(1) << 30)) return NF_ERR_UNSUPPORTED;
     units += o.p.units;
   }

@@ -92,7 +92,9 @@ def main():
     ap.add_argument("--src", default="gpurun_out")
     args = ap.parse_args()
     src, dst = Path(args.src), Path("profiles")
-    shares, traffics = {}, {}
+    # configs without a new capture keep their committed summaries
+    old = lambda n: json.loads((dst / n).read_text()) if (dst / n).exists() else {}  # noqa: E731
+    shares, traffics = old(f"{args.tag}_ncu_share.json"), old(f"{args.tag}_ncu_traffic.json")
     for f in sorted(src.glob(f"{args.tag}_ncu_C*.csv")):
         cfg = f.stem.rsplit("_", 1)[-1]
         mf = src / f"{args.tag}_ncu_{cfg}_meta.json"
