@@ -40,6 +40,7 @@ constexpr int kTEpi = 128;
 constexpr int kTGather = 128;
 constexpr int kTMaxSplits = 16;  // batch-1 layer3/4 convs: few tiles, long K
 constexpr int64_t kTCounterBytes = 64 * 1024;
+constexpr int kTLeaveOff = 8192;  // second semaphore bank: [tile] splits done reducing
 
 template <int BN>
 struct TfCfg {
@@ -114,7 +115,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -193,9 +193,45 @@ __global__ void __launch_bounds__(kTThreads, 1)
     mbar_wait(tfull, 0);
     tc_fence_after();
     const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16);
-    float* part = nullptr;
-    if (p.splits > 1) {
-      part = p.ws + int64_t(tile) * p.splits * BN * kTM;
+    // bias / residual / ReLU and the 16-byte NHWC stores of 4 channels
+    auto store4 = [&](int chl, float4 v4) {  // chl: channel offset within the tile
+      if (!pix_ok || tn * BN + chl >= p.coutg) return;
+      const int ch = c0 + chl;
+      if (p.bias) {
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + ch));
+        v4.x += b4.x; v4.y += b4.y; v4.z += b4.z; v4.w += b4.w;
+      }
+      const int64_t off = int64_t(pix) * p.Cout + ch;
+      if (p.residual) {
+        const float4 r4 = __ldcg(reinterpret_cast<const float4*>(p.residual + off));
+        v4.x += r4.x; v4.y += r4.y; v4.z += r4.z; v4.w += r4.w;
+      }
+      if (p.relu) {
+        v4.x = fmaxf(v4.x, 0.f); v4.y = fmaxf(v4.y, 0.f);
+        v4.z = fmaxf(v4.z, 0.f); v4.w = fmaxf(v4.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(p.y + off) = v4;
+    };
+    if (p.splits == 1) {
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + uint32_t(cc), r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          store4(cc + j, make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                     __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+      }
+    } else {
+      // Split-K: every split publishes its fp32 partial ([split][col][row]
+      // in an L2 workspace), waits until all splits of the tile have, then
+      // reduces and stores ITS OWN slice of the tile's columns, summing the
+      // partials in split order (deterministic). The split CTAs of a tile
+      // are co-resident (units <= #SMs, one CTA per SM), so the wait is
+      // safe; the reduction is spread over the splits instead of serialised
+      // in the last arriver (16 splits: 1 MB of L2 reads for one CTA).
+      float* part = p.ws + int64_t(tile) * p.splits * BN * kTM;
       float* mine = part + int64_t(split) * BN * kTM + row;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
@@ -207,71 +243,40 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
       __threadfence();
       named_bar_sync(1, kTEpi);
-      if (etid == 0) *last_flag = (atomicAdd(p.counters + tile, 1u) == unsigned(p.splits - 1));
+      unsigned* arrive = p.counters + tile;
+      unsigned* leave = p.counters + kTLeaveOff + tile;
+      if (etid == 0) {
+        atomicAdd(arrive, 1u);
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
+          if (seen < unsigned(p.splits)) __nanosleep(64);
+        } while (seen < unsigned(p.splits));
+      }
       named_bar_sync(1, kTEpi);
-      __threadfence();
-    }
-    // without split-K every CTA finishes its tile; with it, the last arriver
-    const bool finish = p.splits == 1 || *last_flag;
+      // columns [c_lo, c_hi) of the tile, a multiple of 4 per split
+      const int per = ((BN / 4 + p.splits - 1) / p.splits) * 4;
+      const int c_lo = split * per, c_hi = min(BN, c_lo + per);
 #pragma unroll 1
-    for (int cc = 0; finish && cc < BN; cc += 32) {
-      float v[32];
-      {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + uint32_t(cc), r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      }
-      if (p.splits > 1) {  // deterministic: partials summed in split order
-        float sum[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) sum[j] = 0.f;
+      for (int cc = c_lo; cc < c_hi; cc += 4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int s2 = 0; s2 < p.splits; ++s2) {
-          if (s2 == split) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) sum[j] += v[j];
-          } else {
-            const float* src = part + int64_t(s2) * BN * kTM + int64_t(cc) * kTM + row;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) sum[j] += __ldcg(src + j * kTM);
-          }
+          const float* src = part + int64_t(s2) * BN * kTM + int64_t(cc) * kTM + row;
+          acc.x += __ldcg(src);
+          acc.y += __ldcg(src + kTM);
+          acc.z += __ldcg(src + 2 * kTM);
+          acc.w += __ldcg(src + 3 * kTM);
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = sum[j];
+        store4(cc, acc);
       }
-      const int nvalid = min(32, p.coutg - (tn * BN + cc));
-      if (pix_ok && nvalid > 0) {
-        const int ch = c0 + cc;
-        if (p.bias) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            if (j < nvalid) {
-              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + ch + j));
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
-        }
-        const int64_t off = int64_t(pix) * p.Cout + ch;
-        if (p.residual) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            if (j < nvalid) {
-              const float4 r4 = __ldcg(reinterpret_cast<const float4*>(p.residual + off + j));
-              v[j] += r4.x; v[j + 1] += r4.y; v[j + 2] += r4.z; v[j + 3] += r4.w;
-            }
-        }
-        if (p.relu) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          if (j < nvalid)
-            *reinterpret_cast<float4*>(p.y + off + j) = make_float4(v[j], v[j + 1], v[j + 2],
-                                                                   v[j + 3]);
+      named_bar_sync(1, kTEpi);
+      // the last split out re-arms both counters for the next launch (every
+      // split has passed its wait on `arrive` by then)
+      if (etid == 0 && atomicAdd(leave, 1u) == unsigned(p.splits - 1)) {
+        *arrive = 0u;
+        *leave = 0u;
       }
     }
-    if (finish && p.splits > 1 && etid == 0) p.counters[tile] = 0u;  // re-arm for the next launch
   } else {
     // --------------------------- im2col gather ----------------------------
     const int gt = threadIdx.x - (64 + kTEpi);
@@ -387,7 +392,7 @@ TfPlan tf_plan(int64_t pix, int64_t coutg, int64_t G, int64_t Kpad, int64_t ws_b
   t.kb_total = int((Kpad + kTK - 1) / kTK);
   const int64_t tiles = G * t.tiles_m * t.tiles_n;
   int s = 1;
-  if (ws_bytes > kTCounterBytes && tiles < kNumSMs && tiles <= kTCounterBytes / 4) {
+  if (ws_bytes > kTCounterBytes && tiles < kNumSMs && tiles <= kTLeaveOff) {
     s = int(kNumSMs / tiles);
     s = s < kTMaxSplits ? s : kTMaxSplits;
     s = s < t.kb_total / 4 ? s : t.kb_total / 4;  // >= 4 K blocks per split

@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(kGemvCols * kGemvWarps)
 #pragma unroll
   for (int r = 0; r < kSimtRows; ++r) acc[r] = 0.0f;
   if (n < N) {
-#pragma unroll 4
+    // 16 independent weight loads in flight per lane: the kernel is bound by
+    // bytes in flight (32 CTAs for N = 1000), not by the FMAs
+#pragma unroll 16
     for (int k = k0; k < k1; ++k) {
       const float wv = to_f32(__ldg(wg + int64_t(k) * N + n));
 #pragma unroll

@@ -994,9 +994,12 @@ class Plan:
         if any(v.split is not None for v in ins):
             return False
         t0 = ins[0].t
-        if t0.dtype != torch.bfloat16 or any(v.t.shape != t0.shape or
-                                              v.t.stride() != t0.stride() for v in ins):
+        if t0.dtype not in (torch.bfloat16, torch.float32) or any(
+                v.t.shape != t0.shape or v.t.stride() != t0.stride() for v in ins):
             return False
+        # bf16: K-major (G, N, K) for the tensor-core GEMM; fp32 heads (few
+        # rows): (G, K, N) for the weight-streaming GEMV
+        f32 = t0.dtype == torch.float32
         esz = t0.element_size()
         ptrs = [v.t.data_ptr() for v in ins]
         gaps = {(b - a) for a, b in zip(ptrs, ptrs[1:])}
@@ -1018,12 +1021,16 @@ class Plan:
         G = len(members)
         dev, dt = self.device, t0.dtype
         has_bias = all(len(m.weights) > 1 for m in members)
-        skey = ("siblings", first.id, npad, has_bias)
+        skey = ("siblings", first.id, npad, has_bias, f32)
         if skey not in self._wcache:
-            w = torch.zeros((G, npad, k_in), dtype=dt, device=dev)
+            w = torch.zeros((G, k_in, npad) if f32 else (G, npad, k_in), dtype=dt, device=dev)
             bias = torch.zeros((G, npad), dtype=torch.float32, device=dev)
             for j, m in enumerate(members):
-                w[j, :widths[j]] = weights[m.weights[0]].data.to(dev, dt).t()
+                wj = weights[m.weights[0]].data.to(dev, dt)
+                if f32:
+                    w[j, :, :widths[j]] = wj
+                else:
+                    w[j, :widths[j]] = wj.t()
                 if has_bias:
                     bias[j, :widths[j]] = weights[m.weights[1]].data.to(dev, torch.float32)
             self._wcache[skey] = (w, bias)
@@ -1039,9 +1046,10 @@ class Plan:
             y.data_ptr()
         yld, ygs = npad, rows * npad
         mcode = self.mcode
+        dcode, layout = (_lib.NF_F32, _lib.NF_W_KN) if f32 else (_lib.NF_BF16, _lib.NF_W_NK)
         self._emit(first.id, lambda st: _lib.call(
             "nf_grouped_linear_strided", xp, xld, gstride, wp, bp, None, yp, yld, ygs, G, rows,
-            k_in, npad, _lib.NF_BF16, _lib.NF_W_NK, act, mcode, st))
+            k_in, npad, dcode, layout, act, mcode, st))
         for j, m in enumerate(members):
             view = y[j].narrow(-1, 0, widths[j])
             self.vals[m.id] = DVal(view, m.output_spec.dims)
