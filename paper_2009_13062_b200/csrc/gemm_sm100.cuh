@@ -136,34 +136,21 @@ inline int balanced_grid(int64_t units, int slots) {
   return int((units + waves - 1) / waves);
 }
 
-#ifndef NF_RES_EARLY
-#define NF_RES_EARLY 1
-#endif
-
 #ifndef NF_GEMM_LITE_KB
 #define NF_GEMM_LITE_KB 100  // swapped (weight-streaming) tiles: 2 CTAs per SM
 #endif
 
 // Output path of a tile configuration: staged = registers -> swizzled smem ->
-// TMA store (wide normal tiles, swapped 256-token tiles); otherwise the
-// epilogue stores straight from registers (narrow normal tiles; swapped
-// tiles, where a warp's lanes are consecutive features of one token, so the
-// stores coalesce without staging).
-// Direct swapped stores measured slower (4 us vs 1.8 us per 128x128 tile
-// epilogue on B200) than staging + TMA store, so they are opt-in.
-#ifndef NF_GEMM_DIRECT_SWAP
-#define NF_GEMM_DIRECT_SWAP 0
-#endif
+// TMA store for tiles of >= 64 columns; narrow tiles (grouped convs with
+// 4..32 channels per group) store straight from registers. (Direct stores
+// from swapped tiles measured slower: 4 us vs 1.8 us per 128x128 epilogue.)
 template <int BN, bool SWAP>
 struct GemmOut {
-  static constexpr bool kStaged = BN >= 64 && !(NF_GEMM_DIRECT_SWAP && SWAP && BN <= 128);
+  static constexpr bool kStaged = BN >= 64;
 };
 
 #ifndef NF_GEMM_GATHER_KB
 #define NF_GEMM_GATHER_KB NF_GEMM_BUDGET_KB
-#endif
-#ifndef NF_GATHER_CA
-#define NF_GATHER_CA 0
 #endif
 #ifndef NF_GEMM_HALO_KB
 #define NF_GEMM_HALO_KB 120  // operand ring of halo-gather convs (2 halo buffers follow)
@@ -198,11 +185,8 @@ struct GemmCfg {
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                    : 2 * BN <= 256 ? 256 : 512;
   // folded-LN per-token (mean, rstd) of the B operand and of the residual
-#ifndef NF_FOLD_SMEM
-#define NF_FOLD_SMEM 1
-#endif
   static constexpr int kNormBytes =
-      (NF_FOLD_SMEM && SWAP && kStaged && !PAIR && !GATHER) ? (KPT > 1 ? 2 : 4) * BN * 4 : 0;
+      (SWAP && kStaged && !PAIR && !GATHER) ? (KPT > 1 ? 2 : 4) * BN * 4 : 0;
   // KPT > 1 leaves room for one (mean, rstd) pair: input OR residual fold
   static constexpr int kResNormOff = KPT > 1 ? 0 : 2 * BN;
   static constexpr size_t kBytes =
@@ -250,14 +234,9 @@ NF_DEVICE UnitCoord decode_unit(const GemmParams& p, int u, bool swap) {
 template <int BYTES>
 NF_DEVICE void cp_async_zfill(uint32_t dst, const void* src, int src_bytes) {
   if constexpr (BYTES == 16)
-    if (NF_GATHER_CA)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                   "r"(src_bytes)
-                   : "memory");
-    else
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                   "r"(src_bytes)
-                   : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
                  "r"(src_bytes)
@@ -284,9 +263,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
   // Residual tiles arrive by TMA into the output staging buffer (same
   // swizzled layout as the result), so the epilogue adds them from smem.
   constexpr bool kResTma = HAS_RES && C::kStaged;
-  // residual tile requested at the top of the unit (ahead of the accumulator)
-  // or once the accumulator is ready (NF_RES_EARLY=0: swapped tiles only)
-  constexpr bool kResEarly = SWAP || NF_RES_EARLY;
+  // the residual tile is requested at the top of the unit, ahead of the
+  // accumulator
   constexpr int EC = BN < 32 ? BN : 32;  // epilogue column chunk
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -554,7 +532,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         if (issuer) bulk_wait_read0();
         if constexpr (!kResTma) named_bar_sync(3 + half, 128);
       }
-      if constexpr (kResTma && kResEarly) issue_residual();
+      if constexpr (kResTma) issue_residual();
       if constexpr (kFold) {
         if (fold_in || fold_res) {
           // (mean, rstd) of this tile's BN tokens, once per unit
@@ -609,28 +587,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         if (etid == 0) NF_WAIT_END(3);
       }
       NF_WAIT_BEGIN();  // epilogue busy: accumulator ready -> buffer released
-      if constexpr (kResTma && !kResEarly) issue_residual();
       tc_fence_after();
-#if defined(NF_EPI_EXP) && NF_EPI_EXP > 0
-      if constexpr (!SWAP && !GATHER) {  // epilogue cost experiment (tools/)
-        if (NF_EPI_EXP == 2) {
-          uint32_t rr[EC];
-          const uint32_t tr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-          for (int cc = col0; cc < col0 + kColsPerThread; cc += EC) {
-            tmem_ld_cols<EC>(tr + uint32_t(cc), rr);
-            tmem_ld_wait();
-            if (rr[0] == 0x7fffffffu && rr[EC - 1] == 1u) p.counters[0] = rr[3];
-          }
-        }
-        if constexpr (kResTma) {
-          mbar_wait(my_rbar, res_phase);
-          res_phase ^= 1u;
-        }
-        release_acc(acc);
-        named_bar_sync(1, kEpiThreads);
-        continue;
-      }
-#endif
       if (etid == 0 && local == 0) NF_TRACE(4);
       const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
       const int m0 = c.ta * kRowsA + int(rank) * kGemmBM, n0 = c.tb * BN;
@@ -724,17 +681,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           // Thread = token row; EC consecutive features n0+cc ...
           const int tok = m0 + row;
           const int f0 = n0 + cc;
-#if defined(NF_EPI_EXP) && NF_EPI_EXP == 4
-          if (true) {
-#pragma unroll
-            for (int q = 0; q < EC / 8; ++q)
-              st_shared_v4(stage_base + stage_offset(row, cc + 8 * q, kGemmBM),
-                           pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                           pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
-            if (kLdAhead) tmem_ld_wait();
-            continue;
-          }
-#endif
           if (kBiasAhead && bias) {
 #pragma unroll
             for (int j = 0; j < EC; ++j) v[j] += __shfl_sync(0xffffffffu, bcur, j);
@@ -879,9 +825,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
             named_bar_sync(3 + half, 128);
             if (issuer) {
               const int b = (cc + EC) / kOutBlock - 1;
-#if !(defined(NF_EPI_EXP) && NF_EPI_EXP == 3)
               tma_store_3d(&map_y, sOut + b * kGemmBM * 128, n0 + b * kOutBlock, m0, c.g);
-#endif
               bulk_commit();
             }
           }
@@ -896,11 +840,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       } else if constexpr (C::kStaged) {
         fence_proxy_async_smem();
         named_bar_sync(1, kEpiThreads);
-#if defined(NF_EPI_EXP) && NF_EPI_EXP == 3
-        if (false) {
-#else
         if (etid == 0) {
-#endif
           if (!SWAP) {
 #pragma unroll
             for (int b = 0; b < BN / kOutBlock; ++b)

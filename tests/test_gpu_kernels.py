@@ -108,7 +108,8 @@ def test_grouped_conv_exact_criterion1_generator(seed):
 
 
 @pytest.mark.parametrize("bt,s,h", [(8, 128, 12), (3, 77, 4), (2, 128, 2), (5, 16, 3),
-                                    (64, 128, 12), (100, 77, 4)])  # persistent kernel
+                                    # persistent kernel (> 296 units), up to the C5 size
+                                    (100, 77, 4), (64, 128, 12), (160, 77, 4), (256, 128, 12)])
 def test_attention_tensor_core_vs_oracle(bt, s, h):
     rng = np.random.default_rng(bt * s + h)
     d = 64 * h
