@@ -288,6 +288,17 @@ int nf_elementwise(int op, const void* a, const void* b, void* y, int64_t n, int
                    void* stream);
 
 /*
+ * Space-to-depth repack of a merged RGB stem input (layout glue of the
+ * 7x7/s2 stem lowered to a 4x4/s1 conv over 2x2 pixel blocks): x bf16 NCHW
+ * (N, groups*cg, H, W) with cg <= 4 channels per instance and even H, W;
+ * y bf16 NHWC (N, H/2+1, W/2+1, groups*16), row 0 and column 0 left untouched
+ * (the caller zeroes them once): y[n, i+1, j+1, g*16 + (bh*2+bw)*4 + c] =
+ * x[n, g*cg + c, 2i+bh, 2j+bw], channels c >= cg written as zero.
+ */
+int nf_space_to_depth_stem(const void* x, void* y, int N, int groups, int cg, int H, int W,
+                           void* stream);
+
+/*
  * Layout glue: y[i0..] = x[i0..] over an up-to-8-D index space with
  * arbitrary element strides on both sides. Realises the merger's
  * Transpose/Reshape junctions (merger.py:237-301) and Pack/Unpack

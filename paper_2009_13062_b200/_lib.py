@@ -56,6 +56,7 @@ SIGNATURES: dict[str, list] = {
                                _i64, _i, _p, _i64, _p, _i, _p, _f, _p, _i, _p, _p, _f, _p, _p],
     "nf_qkv_attention_fold": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f,
                               _p, _i, _p, _f, _p],
+    "nf_space_to_depth_stem": [_p, _p, _i, _i, _i, _i, _i, _p],
     "nf_linear_chain_supported": [_i64, _i64, _i64, _i64],
     "nf_linear_chain_counter_bytes": [_i, _i64],
     "nf_grouped_linear_chain": [_i, _p, _i64, _p, _p],

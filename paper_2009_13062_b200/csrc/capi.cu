@@ -217,6 +217,12 @@ int nf_qkv_attention_fold(const void* x, int64_t x_ld, int64_t x_gs, const void*
                               static_cast<cudaStream_t>(stream), &fold);
 }
 
+int nf_space_to_depth_stem(const void* x, void* y, int N, int groups, int cg, int H, int W,
+                           void* stream) {
+  if (!x || !y) return NF_ERR_SHAPE;
+  return nf::s2d_stem(x, y, N, groups, cg, H, W, static_cast<cudaStream_t>(stream));
+}
+
 int nf_linear_chain_supported(int64_t groups, int64_t rows, int64_t k, int64_t n) {
   return nf::linear_chain_supported(groups, rows, k, n) ? 1 : 0;
 }

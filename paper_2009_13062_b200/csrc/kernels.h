@@ -63,6 +63,7 @@ struct NormGeomC {
 };
 int elementwise(int op, const void* a, const void* b, void* y, int64_t n, int dtype,
                 cudaStream_t s);
+int s2d_stem(const void* x, void* y, int N, int G, int cg, int H, int W, cudaStream_t s);
 int copy_strided(const void* src, void* dst, int rank, const int64_t* dims,
                  const int64_t* src_strides, const int64_t* dst_strides, int elem_bytes,
                  cudaStream_t s);

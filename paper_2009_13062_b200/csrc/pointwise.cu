@@ -123,6 +123,59 @@ __global__ void k_copy_strided(const uint8_t* __restrict__ src, uint8_t* __restr
   }
 }
 
+// Space-to-depth repack of the merged stem input (layout glue for the 7x7/s2
+// stem run as a 4x4/s1 conv, engine.py _lower_stem_s2d): x NCHW bf16
+// (N, G*cg, H, W), cg <= 4, H and W even; y NHWC (N, H/2+1, W/2+1, G*16) whose
+// row 0 / column 0 stay zero; y[n, i+1, j+1, g*16 + (bh*2 + bw)*4 + c] =
+// x[n, g*cg + c, 2i + bh, 2j + bw], channels c >= cg zero. One thread per
+// (s2d pixel, group): 4-byte reads coalesced along j, one full 32-byte sector
+// written per thread (the generic strided copy moved it 2 bytes at a time).
+__global__ void k_s2d_stem(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                           int G, int cg, int H, int W) {
+  pdl_enter();
+  const int w2 = W / 2, hs = H / 2 + 1, ws = w2 + 1;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  const int ng = blockIdx.z, n = ng / G, g = ng - n * G;
+  if (j >= w2) return;
+  uint32_t v[4][2];  // [(bh, bw) pairs per channel c][bh]: bf16x2 (bw = 0, 1)
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int bh = 0; bh < 2; ++bh)
+      v[c][bh] = c < cg ? __ldg(reinterpret_cast<const uint32_t*>(
+                              x + ((int64_t(n) * G * cg + g * cg + c) * H + 2 * i + bh) * W +
+                              2 * j))
+                        : 0u;
+  // channel k = (bh*2 + bw)*4 + c
+  uint32_t o[8];
+#pragma unroll
+  for (int bh = 0; bh < 2; ++bh)
+#pragma unroll
+    for (int bw = 0; bw < 2; ++bw)
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        const uint32_t lo = bw ? v[c][bh] >> 16 : v[c][bh] & 0xffffu;
+        const uint32_t hi = bw ? v[c + 1][bh] >> 16 : v[c + 1][bh] & 0xffffu;
+        o[((bh * 2 + bw) * 4 + c) / 2] = lo | (hi << 16);
+      }
+  uint4* dst = reinterpret_cast<uint4*>(
+      y + ((int64_t(n) * hs + i + 1) * ws + j + 1) * int64_t(G) * 16 + g * 16);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+int s2d_stem(const void* x, void* y, int N, int G, int cg, int H, int W, cudaStream_t s) {
+  if (N < 1 || G < 1 || cg < 1 || H < 2 || W < 2) return NF_ERR_SHAPE;
+  if (cg > 4 || H % 2 || W % 2 || (reinterpret_cast<uintptr_t>(x) & 3) ||
+      (reinterpret_cast<uintptr_t>(y) & 15) || int64_t(N) * G > 65535)
+    return NF_ERR_UNSUPPORTED;
+  const dim3 grid((W / 2 + 127) / 128, H / 2, N * G);
+  launch_pdl(k_s2d_stem, grid, dim3(128), 0, s, static_cast<const __nv_bfloat16*>(x),
+             static_cast<__nv_bfloat16*>(y), G, cg, H, W);
+  return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+}
+
 int copy_strided(const void* src, void* dst, int rank, const int64_t* dims,
                  const int64_t* src_strides, const int64_t* dst_strides, int elem_bytes,
                  cudaStream_t s) {

@@ -851,12 +851,12 @@ class Plan:
         if not src.is_contiguous():
             src = self._materialize(conv.id, v)
         xs = self._own(torch.zeros((n, hs, ws_, groups * 16), dtype=dt, device=self.device))
-        # one strided copy: (n, g, c, i, bh, j, bw) -> s2d channel (bh*2 + bw)*4 + c
+        # (n, g, c, i, bh, j, bw) -> s2d channel (bh*2 + bw)*4 + c at pixel (i+1, j+1)
         gs = groups * 16
-        src_v = src.reshape(n, groups, cg, h // 2, 2, wd // 2, 2)
-        dst_v = xs.as_strided(src_v.shape, (hs * ws_ * gs, 16, 1, ws_ * gs, 8, gs, 4),
-                              xs.storage_offset() + (ws_ + 1) * gs)
-        self._copy_step(conv.id, src_v, dst_v)
+        self._flush_deferred(src)
+        sp, xsp = src.data_ptr(), xs.data_ptr()
+        self._emit(conv.id, lambda st: _lib.call(
+            "nf_space_to_depth_stem", sp, xsp, n, groups, cg, h, wd, st))
         wkey = key + ("s2d",)
         if wkey not in self._wcache:
             wf, bias = folded()  # (Cout, 7, 7, cg) fp32

@@ -11,6 +11,7 @@ import pytest
 import torch
 
 from oracle import kernels as OK
+from paper_2009_13062_b200 import _lib
 from paper_2009_13062_b200 import kernels as GK
 from paper_2009_13062_b200.errors import ShapeError
 
@@ -292,3 +293,23 @@ def test_linear_few_row_gemv_fast(dtype, rows, k, n, g):
     want = torch.relu(torch.bmm(x.double(), w.double()) + b.double()[:, None] + r.double())
     err = (y.double() - want).abs().max().item() / want.abs().max().item()
     assert err < (1e-5 if dtype == torch.float32 else 1e-2), err
+
+
+@pytest.mark.parametrize("n,g,cg,h,w", [(1, 32, 3, 224, 224), (2, 3, 3, 18, 30), (1, 2, 4, 8, 6)])
+def test_space_to_depth_stem_is_an_exact_repack(n, g, cg, h, w):
+    """nf_space_to_depth_stem (the s2d stem's layout glue) vs the same index
+    map in torch: pure data movement, byte-identical; row 0 / column 0 and
+    channels >= cg stay zero."""
+    x = torch.randn(n, g * cg, h, w, device="cuda").bfloat16()
+    hs, ws = h // 2 + 1, w // 2 + 1
+    y = torch.zeros(n, hs, ws, g * 16, device="cuda", dtype=torch.bfloat16)
+    _lib.call("nf_space_to_depth_stem", x.data_ptr(), y.data_ptr(), n, g, cg, h, w,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    want = torch.zeros_like(y)
+    src = x.reshape(n, g, cg, h // 2, 2, w // 2, 2)            # n g c i bh j bw
+    blk = src.permute(0, 3, 5, 1, 4, 6, 2)                      # n i j g bh bw c
+    body = torch.zeros(n, h // 2, w // 2, g, 2, 2, 4, dtype=x.dtype, device="cuda")
+    body[..., :cg] = blk
+    want[:, 1:, 1:] = body.reshape(n, h // 2, w // 2, g * 16)
+    assert torch.equal(y, want)
