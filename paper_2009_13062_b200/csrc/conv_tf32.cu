@@ -31,6 +31,26 @@
 #include "kernels.h"
 
 namespace nf {
+
+#ifdef NF_TF32_TRACE
+// Per-CTA timeline (globaltimer ns) of the last launch, tools/tf32_trace.cu:
+// 0 entry, 1 setup done, 2 first stage landed, 3 last MMA issued, 4 accumulator
+// ready, 5 partial published, 6 all partials in
+__device__ unsigned long long g_tf32_trace[148 * 8];
+#define NF_TT(slot)                                                                   \
+  do {                                                                                \
+    if (blockIdx.x < 148) {                                                           \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_tf32_trace[blockIdx.x * 8 + (slot)] = t_;                                     \
+    }                                                                                 \
+  } while (0)
+#else
+#define NF_TT(slot) \
+  do {              \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kTM = 128;           // output pixels per tile
@@ -128,6 +148,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
   const int nkb = kb1 - kb0;
 
+  if (threadIdx.x == 0) NF_TT(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_w);
     for (int s = 0; s < kStages; ++s) {
@@ -142,6 +163,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) NF_TT(1);
   grid_dependents_launch();
 
   if (warp == 0) {
@@ -162,6 +184,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const int s = i % kStages;
       mbar_wait(&full[s], (i / kStages) & 1);
       tc_fence_after();
+      if (lane == 0 && i == 0) NF_TT(2);
       if (lane == 0) {
         const uint32_t ah = smem_u32(a_hi(s)), al = smem_u32(a_lo(s));
         const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
@@ -180,6 +203,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       __syncwarp();
     }
     if (lane == 0) umma_commit(tfull);
+    if (lane == 0) NF_TT(3);
     __syncwarp();
   } else if (warp < 2 + kTEpi / 32) {
     // ------------------------------ epilogue ------------------------------
@@ -192,6 +216,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
     grid_dependency_wait();                // residual / y / workspace follow the producer grid
     mbar_wait(tfull, 0);
     tc_fence_after();
+    if (etid == 0) NF_TT(4);
     const uint32_t t_row = tmem_base + (uint32_t(quarter * 32) << 16);
     // bias / residual / ReLU and the 16-byte NHWC stores of 4 channels
     auto store4 = [&](int chl, float4 v4) {  // chl: channel offset within the tile
@@ -246,6 +271,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       unsigned* arrive = p.counters + tile;
       unsigned* leave = p.counters + kTLeaveOff + tile;
       if (etid == 0) {
+        NF_TT(5);
         atomicAdd(arrive, 1u);
         unsigned seen;
         do {
@@ -254,6 +280,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         } while (seen < unsigned(p.splits));
       }
       named_bar_sync(1, kTEpi);
+      if (etid == 0) NF_TT(6);
       // columns [c_lo, c_hi) of the tile, a multiple of 4 per split
       const int per = ((BN / 4 + p.splits - 1) / p.splits) * 4;
       const int c_lo = split * per, c_hi = min(BN, c_lo + per);
