@@ -60,6 +60,9 @@ SIGNATURES: dict[str, list] = {
     "nf_linear_chain_supported": [_i64, _i64, _i64, _i64],
     "nf_linear_chain_counter_bytes": [_i, _i64],
     "nf_grouped_linear_chain": [_i, _p, _i64, _p, _p],
+    "nf_grouped_linear_chain_keep": [_i, _p, _i64, _p, _p],
+    "nf_qkv_attention_after": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f,
+                               _p, _i, _p, _f, _p, ctypes.c_uint32, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],

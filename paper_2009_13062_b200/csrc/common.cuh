@@ -524,6 +524,22 @@ NF_DEVICE void pdl_enter() {
   grid_dependents_launch();
 }
 
+// Cross-CTA / cross-kernel completion counters (chained launches): spin
+// until `*ctr >= target` with acquire loads, then order later async-proxy
+// (TMA) reads of the producer's data after it. The spin is bounded (~2 s):
+// a counter that never arrives is a bug, and trapping turns it into a launch
+// error instead of a hung device.
+NF_DEVICE void wait_counter(const unsigned* ctr, unsigned target) {
+  unsigned v;
+  for (uint32_t n = 0;; ++n) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    if (n > (1u << 25)) __trap();
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Per-token (mean, rstd) of a folded LayerNorm over D features from its
 // producer's statistics of `parts` equal parts (the producer's 128-feature
 // tiles): (sum, M2 = centred sum of squares about the part's own mean).

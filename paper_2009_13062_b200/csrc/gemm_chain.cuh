@@ -22,7 +22,10 @@
 // runnable. All CTAs are co-resident (grid <= #SMs, one CTA per SM).
 //
 // Counters are zero at launch; the last CTA to exit re-arms them (every CTA
-// has finished waiting by then), so the launch is CUDA-graph replayable.
+// has finished waiting by then), so the launch is CUDA-graph replayable --
+// unless a later kernel waits on them (the next layer's fused QKV+attention
+// starts instance g once FF2 has stored g's tiles): then the caller zeroes
+// them before each forward.
 //
 // Replaces the reference's per-node `batch_matmul` calls
 // (pkg/src/modelmerge/engine.py:215-235) for a run of consecutive merged
@@ -49,22 +52,12 @@ struct ChainParams {
   int nops, units, groups;
   unsigned* done_tiles;  // [op][g] output tiles published
   unsigned* exit_count;  // CTAs finished (re-arm barrier)
+  int rearm;             // 1: the last CTA zeroes the counters; 0: a later
+                         // kernel still reads them (the caller zeroes them)
 };
 
-NF_DEVICE unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 NF_DEVICE void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-// Spin until `*ctr >= target` (acquire), then order later async-proxy (TMA)
-// reads of the producer's data after it. (Measured: relaxed polls + one
-// fence.acq_rel, or a longer sleep, are slower on the C2 chain.)
-NF_DEVICE void wait_counter(const unsigned* ctr, unsigned target) {
-  while (ld_acquire_gpu(ctr) < target) __nanosleep(64);
-  fence_proxy_async_global();
 }
 
 #ifdef NF_CHAIN_TRACE
@@ -529,7 +522,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && cp.rearm) {
     __threadfence();
     if (atomicAdd(cp.exit_count, 1u) == gridDim.x - 1) {
       // every CTA is past its last wait: re-arm for the next launch

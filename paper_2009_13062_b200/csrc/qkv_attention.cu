@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(192, 1)
                        const __grid_constant__ CUtensorMap map_w, const float* __restrict__ bias,
                        __nv_bfloat16* __restrict__ out, int H, int kb_total, float scale_log2,
                        const float2* nin_stats,
-                       const float* nin_colsum, int nin_parts, float nin_eps) {
+                       const float* nin_colsum, int nin_parts, float nin_eps,
+                       const unsigned* dep, unsigned dep_target) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -105,7 +106,11 @@ __global__ void __launch_bounds__(192, 1)
         mbar_arrive_expect_tx(&full[i], kQStageBytes);
         load_w(i, i);
       }
-      grid_dependency_wait();
+      // x (and its statistics) come from the previous launch -- or, when it
+      // is a chained launch that counts instance g's stored output tiles,
+      // from that counter: this head starts as soon as ITS instance is done
+      if (dep) wait_counter(dep + g, dep_target);
+      else grid_dependency_wait();
       for (int i = 0; i < pre; ++i) load_x(i, i);
       for (int st = pre; st < n_st; ++st) {
         const int stage = st % kQStages;
@@ -157,7 +162,13 @@ __global__ void __launch_bounds__(192, 1)
     }
     float2 ms = make_float2(0.f, 1.f);
     if (nin_stats) {
-      grid_dependency_wait();  // the stats come from the previous launch
+      // the stats come from the previous launch (or its instance-g counter)
+      if (dep) {
+        if (etid == 0) wait_counter(dep + g, dep_target);
+        named_bar_sync(1, 128);
+      } else {
+        grid_dependency_wait();
+      }
       ms = fold_stats(nin_stats, nin_parts, kQS, g, t, 1.0f / float(D), nin_eps);
     }
     named_bar_sync(1, 128);
@@ -296,7 +307,8 @@ __global__ void __launch_bounds__(192, 1)
 // null; out (G, 128, D) bf16 context. heads * 64 == D.
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
-                     cudaStream_t stream, const NormFold* fold) {
+                     cudaStream_t stream, const NormFold* fold, const unsigned* dep,
+                     unsigned dep_target) {
   if (G < 1 || heads < 1 || D != heads * kQD) return NF_ERR_SHAPE;
   const float2* nin = fold ? reinterpret_cast<const float2*>(fold->in_stats) : nullptr;
   if (nin && (!fold->in_colsum || fold->in_parts < 1)) return NF_ERR_SHAPE;
@@ -312,7 +324,7 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
                              stream, mx, mw, bias, static_cast<__nv_bfloat16*>(out), int(heads),
                              int(D / 64), sl2, nin,
                              nin ? fold->in_colsum : nullptr, nin ? fold->in_parts : 0,
-                             nin ? fold->in_eps : 0.f);
+                             nin ? fold->in_eps : 0.f, dep, dep_target);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 

@@ -112,9 +112,37 @@ class _ChainStep:
             o.out_stats = ls.out_stats
         self.ops = ops
 
+        self.keep = False  # a later launch reads the counters (Plan._link_chains)
+
     def __call__(self, st):
-        _lib.call("nf_grouped_linear_chain", len(self.members), self.ops, self.groups,
-                  self.counters.data_ptr(), st)
+        _lib.call("nf_grouped_linear_chain_keep" if self.keep else "nf_grouped_linear_chain",
+                  len(self.members), self.ops, self.groups, self.counters.data_ptr(), st)
+
+
+class _QKVStep:
+    """One fused QKV-projection + attention launch at batch 1. When its input
+    is the last output of a chained launch, :meth:`Plan._link_chains` points
+    ``dep`` at that chain's per-instance completion counters: instance g's
+    heads start once the chain stored g's tiles (nf_qkv_attention_after)."""
+
+    def __init__(self, x, d, w, b, y, groups, heads, scale, fold):
+        self.x, self.d, self.w, self.b, self.y = x, d, w, b, y
+        self.groups, self.heads, self.scale = groups, heads, scale
+        self.fold = fold  # (stats, parts, colsum, eps) or None
+        self.dep = None   # (counters ptr, target) or None
+
+    def __call__(self, st):
+        x, d, g, h, sc = self.x, self.d, self.groups, self.heads, float(self.scale)
+        if self.dep is not None:
+            sp, parts, cp, eps = self.fold if self.fold else (None, 0, None, 0.0)
+            _lib.call("nf_qkv_attention_after", x, d, 128 * d, self.w, self.b, self.y, g, 128, d,
+                      h, sc, sp, parts, cp, eps, self.dep[0], self.dep[1], st)
+        elif self.fold is not None:
+            _lib.call("nf_qkv_attention_fold", x, d, 128 * d, self.w, self.b, self.y, g, 128, d,
+                      h, sc, *self.fold, st)
+        else:
+            _lib.call("nf_qkv_attention", x, d, 128 * d, self.w, self.b, self.y, g, 128, d, h,
+                      sc, st)
 
 
 @dataclass
@@ -511,7 +539,7 @@ class Plan:
         """Merge runs of 2-3 consecutive chainable merged-Linear launches
         (e.g. attention projection -> FF1 -> FF2 of a batch-1 encoder layer)
         into one persistent launch each."""
-        out, i, steps = [], 0, self.steps
+        out, i, steps, runs = [], 0, self.steps, []
         while i < len(steps):
             run = []
             while i + len(run) < len(steps) and len(run) < 3:
@@ -520,14 +548,54 @@ class Plan:
                     break
                 run.append((nid, fn))
             if len(run) >= 2:
-                nbytes = int(_lib.load().nf_linear_chain_counter_bytes(len(run), run[0][1].groups))
-                ctr = self._own(torch.zeros(nbytes // 4, dtype=torch.int32, device=self.device))
-                out.append(("chain:" + "+".join(n for n, _ in run), _ChainStep(run, ctr), 1))
+                runs.append((len(out), run))
+                out.append(None)
                 i += len(run)
             else:
                 out.append(steps[i])
                 i += 1
+        if runs:
+            # every chain's counters in one buffer (one memset re-arms them all)
+            lib = _lib.load()
+            sizes = [int(lib.nf_linear_chain_counter_bytes(len(r), r[0][1].groups)) // 4
+                     for _, r in runs]
+            sizes = [-(-n // 64) * 64 for n in sizes]  # 256-byte aligned slices
+            buf = self._own(torch.zeros(sum(sizes), dtype=torch.int32, device=self.device))
+            self._chain_counters = buf
+            off = 0
+            for (pos, run), n in zip(runs, sizes):
+                out[pos] = ("chain:" + "+".join(m for m, _ in run),
+                            _ChainStep(run, buf[off:off + n]), 1)
+                off += n
         self.steps = out
+        self._link_chains()
+
+    def _link_chains(self) -> None:
+        """A fused QKV+attention launch whose input is a chain's last output
+        waits on that chain's per-instance counters instead of the whole
+        launch; those chains keep their counters set, so one memset at the
+        start of the forward re-arms them."""
+        linked = False
+        for i in range(1, len(self.steps)):
+            fn, prev = self.steps[i][1], self.steps[i - 1][1]
+            if not (isinstance(fn, _QKVStep) and isinstance(prev, _ChainStep)):
+                continue
+            last = prev.members[-1][1]
+            if fn.x != last.y or fn.groups != prev.groups or \
+                    (fn.fold is not None and fn.fold[0] != last.out_stats):
+                continue
+            j = len(prev.members) - 1
+            ptr = prev.counters.data_ptr() + 4 * j * prev.groups
+            fn.dep = (ptr, (last.n + 127) // 128)
+            prev.keep = True
+            linked = True
+        if linked:
+            buf = self._chain_counters
+
+            def rearm(st, buf=buf):
+                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=buf.device)):
+                    buf.zero_()
+            self.steps.insert(0, ("chain:rearm", rearm, 0))
 
     def linear_steps(self) -> dict[str, "_LinearStep"]:
         """node id -> its merged-Linear launch description (chained or not)."""
@@ -1255,15 +1323,9 @@ class Plan:
         scale = 1.0 / math.sqrt(d // heads)
         xp = fo.raw.data_ptr() if fo is not None else x.data_ptr()
         wp, bp, yp = w.data_ptr(), bias.data_ptr() if bias is not None else None, y.data_ptr()
-        if fo is not None:
-            sp, parts, cp, eps = fo.stats.data_ptr(), fo.parts, colsum.data_ptr(), fo.eps
-            self._emit(attn.id, lambda st: _lib.call(
-                "nf_qkv_attention_fold", xp, d, 128 * d, wp, bp, yp, groups, 128, d, heads,
-                float(scale), sp, parts, cp, eps, st))
-        else:
-            self._emit(attn.id, lambda st: _lib.call(
-                "nf_qkv_attention", xp, d, 128 * d, wp, bp, yp, groups, 128, d, heads,
-                float(scale), st))
+        fold = ((fo.stats.data_ptr(), fo.parts, colsum.data_ptr(), fo.eps)
+                if fo is not None else None)
+        self._emit(attn.id, _QKVStep(xp, d, wp, bp, yp, groups, heads, scale, fold))
         return DVal(y, attn.output_spec.dims)
 
     @staticmethod

@@ -35,7 +35,7 @@ def test_chain_bit_identical_to_separate_launches(m, fold_ln):
     inputs = [model_inputs(graph, seed=3, model=j) for j in range(m)]
     bound = merged.bind_inputs(inputs)
     chained = compile_plan(merged.graph, mstore, fold_ln=fold_ln)
-    assert any(nid.startswith("chain:") for nid, _, _ in chained.steps)
+    assert any(nid.startswith("chain:merged") for nid, _, _ in chained.steps)
     ref = compile_plan(merged.graph, mstore, fold_ln=fold_ln, chain=False)
     assert not any(nid.startswith("chain:") for nid, _, _ in ref.steps)
     got = _run(chained, bound, replays=3)
@@ -50,7 +50,9 @@ def test_chain_full_depth_bert_base():
     merged, mstore = merge(graph, stores)
     bound = merged.bind_inputs([model_inputs(graph, seed=1, model=j) for j in range(2)])
     chained = compile_plan(merged.graph, mstore)
-    assert sum(nid.startswith("chain:") for nid, _, _ in chained.steps) == 12
+    assert sum(nid.startswith("chain:merged") for nid, _, _ in chained.steps) == 12
+    # layers 1..11 start their QKV+attention per instance after the previous chain
+    assert sum(getattr(fn, "dep", None) is not None for _, fn, _ in chained.steps) == 11
     ref = compile_plan(merged.graph, mstore, chain=False)
     for a, b in zip(_run(chained, bound)[0], _run(ref, bound)[0]):
         assert torch.equal(a, b)
