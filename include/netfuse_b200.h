@@ -244,24 +244,33 @@ int64_t nf_linear_chain_counter_bytes(int n_ops, int64_t groups);
 int nf_grouped_linear_chain(int n_ops, const nf_linear_op* ops, int64_t groups, void* counters,
                             void* stream);
 /*
- * Same, but the counters stay set after the launch (counters[j*groups + g] =
- * op j's output tiles of instance g): a later kernel may wait on them (see
- * nf_qkv_attention_after). The caller zeroes them before every launch.
+ * Chained launch with options. flags: NF_CHAIN_KEEP_COUNTERS leaves the
+ * per-instance counters set after the launch (counters[j*groups + g] = op
+ * j's output tiles of instance g) for a later kernel to wait on (see
+ * nf_qkv_attention_after); the caller zeroes them before every launch.
+ * dep_counters (or NULL): a [groups] completion counter of the kernel that
+ * produces ops[0]'s inputs (e.g. nf_qkv_attention_after's done_counters);
+ * instance g's units of ops[0] start once dep_counters[g] >= dep_target
+ * instead of waiting for that whole launch.
  */
-int nf_grouped_linear_chain_keep(int n_ops, const nf_linear_op* ops, int64_t groups,
-                                 void* counters, void* stream);
+#define NF_CHAIN_KEEP_COUNTERS 1
+int nf_grouped_linear_chain_ex(int n_ops, const nf_linear_op* ops, int64_t groups,
+                               void* counters, int flags, const void* dep_counters,
+                               uint32_t dep_target, void* stream);
 /*
- * nf_qkv_attention_fold whose input x (and its LayerNorm statistics) is the
- * output of an earlier chained launch (nf_grouped_linear_chain_keep): the
- * CTAs of instance g start once dep_counters[g] >= dep_target (that launch's
- * output tiles of g are stored) instead of waiting for the whole launch, so
- * attention of early instances overlaps the chain's tail.
+ * nf_qkv_attention_fold with per-instance ordering. dep_counters (or NULL):
+ * x (and its LayerNorm statistics) is the output of an earlier chained launch
+ * (NF_CHAIN_KEEP_COUNTERS); instance g's CTAs start once dep_counters[g] >=
+ * dep_target (that launch stored g's output tiles) instead of waiting for the
+ * whole launch. done_counters (or NULL): each CTA adds 1 to done_counters[g]
+ * once its head's context is stored (heads per instance = all done).
  */
 int nf_qkv_attention_after(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                            const float* bias, void* out, int64_t groups, int64_t seq,
                            int64_t d_model, int64_t heads, float scale, const float* in_stats,
                            int in_parts, const float* in_colsum, float in_eps,
-                           const void* dep_counters, uint32_t dep_target, void* stream);
+                           const void* dep_counters, uint32_t dep_target,
+                           void* done_counters, void* stream);
 
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,

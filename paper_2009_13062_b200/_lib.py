@@ -26,6 +26,7 @@ NF_MODE_FAST, NF_MODE_EXACT = 0, 1
 NF_W_NK, NF_W_KN = 0, 1
 NF_EW_ADD, NF_EW_MUL, NF_EW_RELU, NF_EW_TANH, NF_EW_GELU = 0, 1, 2, 3, 4
 NF_POOL_MAX, NF_POOL_MEAN = 0, 1
+NF_CHAIN_KEEP_COUNTERS = 1
 NF_MAX_RANK = 8
 
 _p = ctypes.c_void_p
@@ -60,9 +61,9 @@ SIGNATURES: dict[str, list] = {
     "nf_linear_chain_supported": [_i64, _i64, _i64, _i64],
     "nf_linear_chain_counter_bytes": [_i, _i64],
     "nf_grouped_linear_chain": [_i, _p, _i64, _p, _p],
-    "nf_grouped_linear_chain_keep": [_i, _p, _i64, _p, _p],
+    "nf_grouped_linear_chain_ex": [_i, _p, _i64, _p, _i, _p, ctypes.c_uint32, _p],
     "nf_qkv_attention_after": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f,
-                               _p, _i, _p, _f, _p, ctypes.c_uint32, _p],
+                               _p, _i, _p, _f, _p, ctypes.c_uint32, _p, _p],
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],

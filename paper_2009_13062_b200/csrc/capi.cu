@@ -234,7 +234,8 @@ int64_t nf_linear_chain_counter_bytes(int n_ops, int64_t groups) {
 }
 
 static int chain_entry(int n_ops, const nf_linear_op* ops, int64_t groups, void* counters,
-                       void* stream, bool rearm) {
+                       void* stream, bool rearm, const unsigned* ext_dep = nullptr,
+                       unsigned ext_target = 0) {
   if (!ops || !counters || n_ops < 1 || n_ops > 3 || groups < 1) return NF_ERR_SHAPE;
   nf::LinearOpDesc d[3];
   for (int j = 0; j < n_ops; ++j) {
@@ -250,7 +251,8 @@ static int chain_entry(int n_ops, const nf_linear_op* ops, int64_t groups, void*
                                          o.res_eps, o.out_stats}};
   }
   return nf::grouped_linear_chain_tc(n_ops, d, static_cast<unsigned*>(counters),
-                                     static_cast<cudaStream_t>(stream), rearm);
+                                     static_cast<cudaStream_t>(stream), rearm, ext_dep,
+                                     ext_target);
 }
 
 int nf_grouped_linear_chain(int n_ops, const nf_linear_op* ops, int64_t groups, void* counters,
@@ -262,18 +264,24 @@ int nf_qkv_attention_after(const void* x, int64_t x_ld, int64_t x_gs, const void
                            const float* bias, void* out, int64_t groups, int64_t seq,
                            int64_t d_model, int64_t heads, float scale, const float* in_stats,
                            int in_parts, const float* in_colsum, float in_eps,
-                           const void* dep_counters, uint32_t dep_target, void* stream) {
-  if (!x || !w || !out || !dep_counters || dep_target < 1) return NF_ERR_SHAPE;
+                           const void* dep_counters, uint32_t dep_target,
+                           void* done_counters, void* stream) {
+  if (!x || !w || !out || (dep_counters && dep_target < 1)) return NF_ERR_SHAPE;
   const nf::NormFold fold{in_stats, in_colsum, in_parts, in_eps, nullptr,
                           nullptr, nullptr, 0, 0.f, nullptr};
   return nf::qkv_attention_tc(x, x_ld, x_gs, w, bias, out, groups, seq, d_model, heads, scale,
                               static_cast<cudaStream_t>(stream), in_stats ? &fold : nullptr,
-                              static_cast<const unsigned*>(dep_counters), dep_target);
+                              static_cast<const unsigned*>(dep_counters), dep_target,
+                              static_cast<unsigned*>(done_counters));
 }
 
-int nf_grouped_linear_chain_keep(int n_ops, const nf_linear_op* ops, int64_t groups,
-                                 void* counters, void* stream) {
-  return chain_entry(n_ops, ops, groups, counters, stream, false);
+int nf_grouped_linear_chain_ex(int n_ops, const nf_linear_op* ops, int64_t groups,
+                               void* counters, int flags, const void* dep_counters,
+                               uint32_t dep_target, void* stream) {
+  if (flags & ~NF_CHAIN_KEEP_COUNTERS) return NF_ERR_UNSUPPORTED;
+  if (dep_counters && dep_target < 1) return NF_ERR_SHAPE;
+  return chain_entry(n_ops, ops, groups, counters, stream, !(flags & NF_CHAIN_KEEP_COUNTERS),
+                     static_cast<const unsigned*>(dep_counters), dep_target);
 }
 
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,

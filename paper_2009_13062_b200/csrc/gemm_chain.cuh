@@ -54,6 +54,8 @@ struct ChainParams {
   unsigned* exit_count;  // CTAs finished (re-arm barrier)
   int rearm;             // 1: the last CTA zeroes the counters; 0: a later
                          // kernel still reads them (the caller zeroes them)
+  const unsigned* ext_dep;  // [g] completion counter of the kernel producing
+  unsigned ext_target;      // op 0's inputs (e.g. attention heads), or null
 };
 
 NF_DEVICE void fence_proxy_async_global() {
@@ -183,7 +185,12 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
           tma_load_4d(sA + stage * C::kABytes, &o.ma, &full[stage], 0, a_row, c.kb0 + i * KPT,
                       c.g, kEvictFirst);
         }
-        if (first) {
+        if (op == 0 && cp.ext_dep) {
+          // op 0's activations come from a launch that counts instance g's
+          // finished work: start as soon as g is done, not the whole launch
+          wait_counter(cp.ext_dep + c.g, cp.ext_target);
+        } else if (first && !cp.ext_dep) {
+          // (with ext_dep, ops > 0 depend on earlier kernels only through op 0)
           grid_dependency_wait();
           first = false;
         }
@@ -264,7 +271,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
     const uint32_t stage_base = smem_u32(sOut);
     uint32_t res_phase = 0;
     int local = 0;
-    grid_dependency_wait();  // residual tiles / statistics of the previous kernel
+    // residual tiles / statistics of earlier kernels: behind the grid
+    // dependency, or per instance behind ext_dep for op 0 (whose producer
+    // acquired what op 0 reads, transitively)
+    if (!cp.ext_dep) grid_dependency_wait();
     for (int u = blockIdx.x; u < cp.units; u += gridDim.x, ++local) {
       const int op = chain_op_of(cp, u);
       const ChainOp& o = cp.ops[op];
@@ -298,6 +308,10 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
           wait_counter(cp.done_tiles + o.epi_dep * cp.groups + c.g,
                        unsigned(d.p.tiles_a * d.p.tiles_b));
         }
+        named_bar_sync(1, kEpiThreads);
+      } else if (cp.ext_dep) {
+        // op reading only earlier kernels' results: behind ext_dep for g
+        if (etid == 0) wait_counter(cp.ext_dep + c.g, cp.ext_target);
         named_bar_sync(1, kEpiThreads);
       }
 #ifdef NF_CHAIN_TRACE

@@ -254,7 +254,8 @@ bool linear_chain_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
 // kernels wrote, instance by instance. `counters` holds n_ops * G + 1 zeroed
 // words; the kernel leaves them zeroed.
 int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counters,
-                            cudaStream_t stream, bool rearm) {
+                            cudaStream_t stream, bool rearm, const unsigned* ext_dep,
+                            unsigned ext_target) {
   if (nops < 1 || nops > kChainMaxOps || !ops || !counters) return NF_ERR_SHAPE;
   ChainParams cp{};
   cp.nops = nops;
@@ -299,6 +300,8 @@ int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counter
   cp.done_tiles = counters;
   cp.exit_count = counters + int64_t(nops) * cp.groups;
   cp.rearm = rearm ? 1 : 0;
+  cp.ext_dep = ext_dep;
+  cp.ext_target = ext_target;
   using C = GemmCfg<128, true, false, 0, 2>;
   static SmemAttrOnce smem_attr;
   smem_attr.set(k_linear_chain_tc, int(C::kBytes));

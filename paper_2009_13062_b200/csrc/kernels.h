@@ -48,7 +48,8 @@ struct LinearOpDesc {
 };
 bool linear_chain_supported(int64_t G, int64_t T, int64_t K, int64_t N);
 int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counters,
-                            cudaStream_t stream, bool rearm = true);
+                            cudaStream_t stream, bool rearm = true,
+                            const unsigned* ext_dep = nullptr, unsigned ext_target = 0);
 
 // linear_simt.cu — CUDA-core grouped linear (exact reference order or FMA).
 int grouped_linear_simt(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
@@ -112,7 +113,8 @@ int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int 
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
                      cudaStream_t stream, const NormFold* fold = nullptr,
-                     const unsigned* dep = nullptr, unsigned dep_target = 0);
+                     const unsigned* dep = nullptr, unsigned dep_target = 0,
+                     unsigned* done = nullptr);
 
 // attention.cu
 int attention(const void* qkv, void* out, int64_t Bt, int64_t S, int64_t H, int64_t dh,

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(192, 1)
                        __nv_bfloat16* __restrict__ out, int H, int kb_total, float scale_log2,
                        const float2* nin_stats,
                        const float* nin_colsum, int nin_parts, float nin_eps,
-                       const unsigned* dep, unsigned dep_target) {
+                       const unsigned* dep, unsigned dep_target, unsigned* done) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -290,6 +290,15 @@ __global__ void __launch_bounds__(192, 1)
           *reinterpret_cast<uint4*>(dst + c * 32 + q * 8) = u;
         }
     }
+    if (done) {
+      // this head's context is stored: count it for instance g (a chained
+      // launch's first op starts g's units at H heads)
+      named_bar_sync(1, 128);
+      if (etid == 0) {
+        __threadfence();
+        atomicAdd(done + g, 1u);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(192, 1)
 int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, const float* bias,
                      void* out, int64_t G, int64_t S, int64_t D, int64_t heads, float scale,
                      cudaStream_t stream, const NormFold* fold, const unsigned* dep,
-                     unsigned dep_target) {
+                     unsigned dep_target, unsigned* done) {
   if (G < 1 || heads < 1 || D != heads * kQD) return NF_ERR_SHAPE;
   const float2* nin = fold ? reinterpret_cast<const float2*>(fold->in_stats) : nullptr;
   if (nin && (!fold->in_colsum || fold->in_parts < 1)) return NF_ERR_SHAPE;
@@ -324,7 +333,7 @@ int qkv_attention_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w, c
                              stream, mx, mw, bias, static_cast<__nv_bfloat16*>(out), int(heads),
                              int(D / 64), sl2, nin,
                              nin ? fold->in_colsum : nullptr, nin ? fold->in_parts : 0,
-                             nin ? fold->in_eps : 0.f, dep, dep_target);
+                             nin ? fold->in_eps : 0.f, dep, dep_target, done);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 

@@ -113,10 +113,17 @@ class _ChainStep:
         self.ops = ops
 
         self.keep = False  # a later launch reads the counters (Plan._link_chains)
+        self.dep = None    # (ptr, target): per-instance completion of op 0's producer
 
     def __call__(self, st):
-        _lib.call("nf_grouped_linear_chain_keep" if self.keep else "nf_grouped_linear_chain",
-                  len(self.members), self.ops, self.groups, self.counters.data_ptr(), st)
+        if not self.keep and self.dep is None:
+            _lib.call("nf_grouped_linear_chain", len(self.members), self.ops, self.groups,
+                      self.counters.data_ptr(), st)
+            return
+        dp, dt = self.dep if self.dep is not None else (None, 0)
+        _lib.call("nf_grouped_linear_chain_ex", len(self.members), self.ops, self.groups,
+                  self.counters.data_ptr(), _lib.NF_CHAIN_KEEP_COUNTERS if self.keep else 0,
+                  dp, dt, st)
 
 
 class _QKVStep:
@@ -130,13 +137,15 @@ class _QKVStep:
         self.groups, self.heads, self.scale = groups, heads, scale
         self.fold = fold  # (stats, parts, colsum, eps) or None
         self.dep = None   # (counters ptr, target) or None
+        self.done = None  # [groups] counters this launch bumps per stored head
 
     def __call__(self, st):
         x, d, g, h, sc = self.x, self.d, self.groups, self.heads, float(self.scale)
-        if self.dep is not None:
+        if self.dep is not None or self.done is not None:
             sp, parts, cp, eps = self.fold if self.fold else (None, 0, None, 0.0)
+            dp, dt = self.dep if self.dep is not None else (None, 0)
             _lib.call("nf_qkv_attention_after", x, d, 128 * d, self.w, self.b, self.y, g, 128, d,
-                      h, sc, sp, parts, cp, eps, self.dep[0], self.dep[1], st)
+                      h, sc, sp, parts, cp, eps, dp, dt, self.done, st)
         elif self.fold is not None:
             _lib.call("nf_qkv_attention_fold", x, d, 128 * d, self.w, self.b, self.y, g, 128, d,
                       h, sc, *self.fold, st)
@@ -576,6 +585,14 @@ class Plan:
         launch; those chains keep their counters set, so one memset at the
         start of the forward re-arms them."""
         linked = False
+        # attention -> chain: op 0 (proj) of instance g starts once g's heads
+        # are stored (the QKV launch counts them in a slice of the same buffer)
+        qkv_links = []
+        for i in range(len(self.steps) - 1):
+            fn, nxt = self.steps[i][1], self.steps[i + 1][1]
+            if isinstance(fn, _QKVStep) and isinstance(nxt, _ChainStep) and \
+                    nxt.members[0][1].x == fn.y and nxt.groups == fn.groups:
+                qkv_links.append((fn, nxt))
         for i in range(1, len(self.steps)):
             fn, prev = self.steps[i][1], self.steps[i - 1][1]
             if not (isinstance(fn, _QKVStep) and isinstance(prev, _ChainStep)):
@@ -589,12 +606,23 @@ class Plan:
             fn.dep = (ptr, (last.n + 127) // 128)
             prev.keep = True
             linked = True
+        if qkv_links:
+            n = -(-sum(q.groups for q, _ in qkv_links) // 64) * 64
+            done = self._own(torch.zeros(n, dtype=torch.int32, device=self.device))
+            off = 0
+            for q, ch in qkv_links:
+                q.done = done[off:].data_ptr()
+                ch.dep = (q.done, q.heads)
+                off += q.groups
+            self._qkv_done = done
+            linked = True
         if linked:
-            buf = self._chain_counters
+            bufs = [self._chain_counters] + ([self._qkv_done] if qkv_links else [])
 
-            def rearm(st, buf=buf):
-                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=buf.device)):
-                    buf.zero_()
+            def rearm(st, bufs=bufs):
+                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=bufs[0].device)):
+                    for b in bufs:
+                        b.zero_()
             self.steps.insert(0, ("chain:rearm", rearm, 0))
 
     def linear_steps(self) -> dict[str, "_LinearStep"]:

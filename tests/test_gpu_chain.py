@@ -51,8 +51,11 @@ def test_chain_full_depth_bert_base():
     bound = merged.bind_inputs([model_inputs(graph, seed=1, model=j) for j in range(2)])
     chained = compile_plan(merged.graph, mstore)
     assert sum(nid.startswith("chain:merged") for nid, _, _ in chained.steps) == 12
-    # layers 1..11 start their QKV+attention per instance after the previous chain
-    assert sum(getattr(fn, "dep", None) is not None for _, fn, _ in chained.steps) == 11
+    # layers 1..11 start their QKV+attention per instance after the previous
+    # chain, and every chain starts instance g once g's attention heads are in
+    kinds = [(type(fn).__name__, getattr(fn, "dep", None) is not None)
+             for _, fn, _ in chained.steps]
+    assert kinds.count(("_QKVStep", True)) == 11 and kinds.count(("_ChainStep", True)) == 12
     ref = compile_plan(merged.graph, mstore, chain=False)
     for a, b in zip(_run(chained, bound)[0], _run(ref, bound)[0]):
         assert torch.equal(a, b)
