@@ -584,6 +584,16 @@ class Plan:
         waits on that chain's per-instance counters instead of the whole
         launch; those chains keep their counters set, so one memset at the
         start of the forward re-arms them."""
+        # Linked launches of consecutive layers overlap instance by instance,
+        # and every split-K GEMM of the plan shares one workspace indexed by
+        # (instance, tile): only safe when those GEMMs all tile alike (work on
+        # the same (instance, tile) is ordered through the counters).
+        splitk = {(m.groups, m.rows, m.k, m.n) for _, fn, _ in self.steps
+                  if isinstance(fn, _ChainStep) for _, m in fn.members if m.wsb}
+        splitk |= {(fn.groups, fn.rows, fn.k, fn.n) for _, fn, _ in self.steps
+                   if isinstance(fn, _LinearStep) and fn.wsb}
+        if len(splitk) > 1:
+            return
         linked = False
         # attention -> chain: op 0 (proj) of instance g starts once g's heads
         # are stored (the QKV launch counts them in a slice of the same buffer)
