@@ -272,6 +272,35 @@ int nf_qkv_attention_after(const void* x, int64_t x_ld, int64_t x_gs, const void
                            const void* dep_counters, uint32_t dep_target,
                            void* done_counters, void* stream);
 
+/*
+ * Per-instance launch linking for merged CNN / GEMM pipelines. Counters are
+ * uint32 per instance (zeroed by the caller before each forward); instance of
+ * group g = g / groups_per_instance. dep_x / dep_r (or NULL): counters of the
+ * launches that produced x / the residual, with the number of output tiles
+ * one instance of them publishes (dep_*_target, from nf_linear_link_units /
+ * nf_conv_link_units x their groups per instance); a unit of instance m
+ * starts once those counts are reached instead of waiting for the whole
+ * previous launch. done (or NULL): this launch's counters, bumped once per
+ * stored output tile. NULL dependencies wait for the previous launch as the
+ * plain entry points do. Results are bit-identical to the plain entry points.
+ */
+int nf_linear_link_units(int64_t groups, int64_t rows, int64_t k, int64_t n);
+int nf_conv_link_units(int N, int H, int W, int C, int Cout, int groups, int kernel, int stride,
+                       int pad);
+int nf_grouped_linear_linked(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                             const void* bias, const void* residual, void* y, int64_t y_ld,
+                             int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                             int act, void* workspace, int64_t workspace_bytes,
+                             const void* dep_x, uint32_t dep_x_target, const void* dep_r,
+                             uint32_t dep_r_target, void* done, int groups_per_instance,
+                             void* stream);
+int nf_grouped_conv_tc_linked(const void* x, const void* w, const float* bias,
+                              const void* residual, void* y, int N, int H, int W, int C, int Cout,
+                              int groups, int kernel, int stride, int pad, int kpad, int relu,
+                              void* workspace, int64_t workspace_bytes, const void* dep_x,
+                              uint32_t dep_x_target, const void* dep_r, uint32_t dep_r_target,
+                              void* done, int groups_per_instance, void* stream);
+
 /* NHWC 2-D pooling (max: -inf padding; mean: window sum / k^2). */
 int nf_pool2d_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int kernel,
                    int stride, int pad, int dtype, void* stream);

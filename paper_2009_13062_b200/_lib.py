@@ -61,6 +61,13 @@ SIGNATURES: dict[str, list] = {
     "nf_linear_chain_supported": [_i64, _i64, _i64, _i64],
     "nf_linear_chain_counter_bytes": [_i, _i64],
     "nf_grouped_linear_chain": [_i, _p, _i64, _p, _p],
+    "nf_linear_link_units": [_i64, _i64, _i64, _i64],
+    "nf_conv_link_units": [_i] * 9,
+    "nf_grouped_linear_linked": [_p, _i64, _i64, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                                 _i64, _i, _p, _i64, _p, ctypes.c_uint32, _p, ctypes.c_uint32,
+                                 _p, _i, _p],
+    "nf_grouped_conv_tc_linked": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _i64, _p,
+                                  ctypes.c_uint32, _p, ctypes.c_uint32, _p, _i, _p],
     "nf_grouped_linear_chain_ex": [_i, _p, _i64, _p, _i, _p, ctypes.c_uint32, _p],
     "nf_qkv_attention_after": [_p, _i64, _i64, _p, _p, _p, _i64, _i64, _i64, _i64, _f,
                                _p, _i, _p, _f, _p, ctypes.c_uint32, _p, _p],

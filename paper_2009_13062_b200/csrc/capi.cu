@@ -156,6 +156,57 @@ int nf_grouped_conv_tc(const void* x, const void* w, const float* bias, const vo
                              static_cast<cudaStream_t>(stream));
 }
 
+int nf_linear_link_units(int64_t groups, int64_t rows, int64_t k, int64_t n) {
+  if (groups < 1 || rows < 1 || k < 1 || n < 1) return 0;
+  return int(nf::linear_link_units(groups, rows, k, n));
+}
+
+int nf_conv_link_units(int N, int H, int W, int C, int Cout, int groups, int kernel, int stride,
+                       int pad) {
+  return int(nf::conv_link_units(N, H, W, C, Cout, groups, kernel, stride, pad));
+}
+
+static bool link_args(const void* dep_x, uint32_t tx, const void* dep_r, uint32_t tr,
+                      void* done, int gpi, nf::LinkSpec* l) {
+  if (gpi < 1 || (dep_x && tx < 1) || (dep_r && tr < 1)) return false;
+  *l = nf::LinkSpec{static_cast<const unsigned*>(dep_x), tx, static_cast<const unsigned*>(dep_r),
+                    tr, static_cast<unsigned*>(done), gpi};
+  return true;
+}
+
+int nf_grouped_linear_linked(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
+                             const void* bias, const void* residual, void* y, int64_t y_ld,
+                             int64_t y_gs, int64_t groups, int64_t rows, int64_t k, int64_t n,
+                             int act, void* workspace, int64_t workspace_bytes,
+                             const void* dep_x, uint32_t dep_x_target, const void* dep_r,
+                             uint32_t dep_r_target, void* done, int groups_per_instance,
+                             void* stream) {
+  if (!x || !w || !y || groups < 1 || rows < 1 || k < 1 || n < 1) return NF_ERR_SHAPE;
+  if (x_ld < k || y_ld < n || (groups > 1 && (x_gs < 1 || y_gs < 1))) return NF_ERR_SHAPE;
+  if (act < NF_ACT_NONE || act > NF_ACT_TANH) return NF_ERR_UNSUPPORTED;
+  nf::LinkSpec l;
+  if (!link_args(dep_x, dep_x_target, dep_r, dep_r_target, done, groups_per_instance, &l))
+    return NF_ERR_SHAPE;
+  return nf::grouped_linear_tc(x, x_ld, x_gs, w, static_cast<const float*>(bias), residual, y,
+                               y_ld, y_gs, groups, rows, k, n, NF_BF16, act, workspace,
+                               workspace_bytes, static_cast<cudaStream_t>(stream), nullptr, &l);
+}
+
+int nf_grouped_conv_tc_linked(const void* x, const void* w, const float* bias,
+                              const void* residual, void* y, int N, int H, int W, int C, int Cout,
+                              int groups, int kernel, int stride, int pad, int kpad, int relu,
+                              void* workspace, int64_t workspace_bytes, const void* dep_x,
+                              uint32_t dep_x_target, const void* dep_r, uint32_t dep_r_target,
+                              void* done, int groups_per_instance, void* stream) {
+  if (!x || !w || !y || N < 1 || H < 1 || W < 1 || C < 1 || Cout < 1) return NF_ERR_SHAPE;
+  nf::LinkSpec l;
+  if (!link_args(dep_x, dep_x_target, dep_r, dep_r_target, done, groups_per_instance, &l))
+    return NF_ERR_SHAPE;
+  return nf::grouped_conv_tc(x, w, bias, residual, y, N, H, W, C, Cout, groups, kernel, stride,
+                             pad, kpad, relu, workspace, workspace_bytes,
+                             static_cast<cudaStream_t>(stream), &l);
+}
+
 int nf_grouped_conv_tf32(const void* x, const void* w, const float* bias, const void* residual,
                          void* y, int N, int H, int W, int C, int Cout, int groups, int kernel,
                          int stride, int pad, int kpad, int relu, void* workspace,

@@ -540,6 +540,16 @@ NF_DEVICE void wait_counter(const unsigned* ctr, unsigned target) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Non-blocking form of wait_counter: true (and the acquire + proxy fence
+// done) when the counter has arrived.
+NF_DEVICE bool counter_ready(const unsigned* ctr, unsigned target) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  if (v < target) return false;
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  return true;
+}
+
 // Per-token (mean, rstd) of a folded LayerNorm over D features from its
 // producer's statistics of `parts` equal parts (the producer's 128-feature
 // tiles): (sum, M2 = centred sum of squares about the part's own mean).

@@ -82,9 +82,22 @@ int64_t conv_workspace_bytes(int64_t N, int64_t H, int64_t W, int64_t C, int64_t
   return kCounterBytes + tiles * s * int64_t(kGemmBM) * bn * 4;
 }
 
+int64_t conv_link_units(int64_t N, int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t G,
+                        int64_t k, int64_t stride, int64_t pad) {
+  if (G < 1 || C % G || Cout % G || stride < 1) return 0;
+  const int64_t Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+  const int64_t pix = N * Ho * Wo, coutg = Cout / G;
+  bool swap;
+  const int bn = conv_pick(pix, coutg, &swap);
+  const int64_t ta = swap ? (coutg + kGemmBM - 1) / kGemmBM : (pix + kGemmBM - 1) / kGemmBM;
+  const int64_t tb = swap ? (pix + bn - 1) / bn : (coutg + bn - 1) / bn;
+  return ta * tb;
+}
+
 int grouped_conv_tc(const void* x, const void* w, const float* bias, const void* residual,
                     void* y, int N, int H, int W, int C, int Cout, int G, int k, int stride,
-                    int pad, int Kpad, int relu, void* ws, int64_t ws_bytes, cudaStream_t stream) {
+                    int pad, int Kpad, int relu, void* ws, int64_t ws_bytes, cudaStream_t stream,
+                    const LinkSpec* link) {
   if (G < 1 || C % G || Cout % G || k < 1 || stride < 1 || pad < 0) return NF_ERR_SHAPE;
   const int cg = C / G, coutg = Cout / G;
   const int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
@@ -112,6 +125,15 @@ int grouped_conv_tc(const void* x, const void* w, const float* bias, const void*
               bn <= 64 && halo_h <= 256 && halo_w <= 256 && halo_bytes <= 48 * 1024;
 
   GemmParams p{};
+  if (link) {
+    if (link->gpi < 1 || (link->dep_x && residual && !link->dep_r)) return NF_ERR_SHAPE;
+    p.dep_x = link->dep_x;
+    p.dep_x_target = link->dep_x_target;
+    p.dep_r = link->dep_r;
+    p.dep_r_target = link->dep_r_target;
+    p.done = link->done;
+    p.link_gpi = link->gpi;
+  }
   p.act = relu ? NF_ACT_RELU : NF_ACT_NONE;
   p.bias = bias;
   p.residual = residual;

@@ -105,6 +105,11 @@ bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N) {
   return L.swap && L.bn == 128 && GemmOut<128, true>::kStaged && N % 128 == 0;
 }
 
+int64_t linear_link_units(int64_t G, int64_t T, int64_t K, int64_t N) {
+  const LinearPlan L = plan_linear(G, T, K, N, 0);
+  return (L.pair ? 2 : 1) * L.tiles_a * L.tiles_b;
+}
+
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N) {
   const LinearPlan L = plan_linear(G, T, K, N, INT64_MAX);
   if (L.splits <= 1) return 0;
@@ -175,12 +180,21 @@ int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const NormFold* fold) {
+                      const NormFold* fold, const LinkSpec* link) {
   GemmParams p;
   LinearPlan L;
   const int st = linear_setup(ws, ws_bytes, G, T, K, N, out_dtype, act, bias, residual, y, y_ld,
                               y_gs, fold, p, L);
   if (st != NF_OK) return st;
+  if (link) {
+    if (link->gpi < 1 || (link->dep_x && residual && !link->dep_r)) return NF_ERR_SHAPE;
+    p.dep_x = link->dep_x;
+    p.dep_x_target = link->dep_x_target;
+    p.dep_r = link->dep_r;
+    p.dep_r_target = link->dep_r_target;
+    p.done = link->done;
+    p.link_gpi = link->gpi;
+  }
   const bool swap = L.swap;
   const int bn = L.bn;
   const int bbox = L.pair ? bn / 2 : bn;  // B rows each CTA loads

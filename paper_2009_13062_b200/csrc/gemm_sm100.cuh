@@ -125,6 +125,17 @@ struct GemmParams {
   int nres_parts;
   float nres_inv_d, nres_eps;
   float2* nout_stats;
+  // Per-instance launch linking (CNN plans; all null = wait for the whole
+  // previous launch as usual). The instance of a unit is g / link_gpi.
+  // dep_x / dep_r: [instance] counters of stored tiles of the launches that
+  // produced the activations / the residual -- a unit starts once its
+  // instance reached the target, not once the previous launch finished.
+  // done: this launch's [instance] counter, bumped per stored output tile.
+  const unsigned* dep_x;
+  const unsigned* dep_r;
+  unsigned* done;
+  unsigned dep_x_target, dep_r_target;
+  int link_gpi;
 };
 
 
@@ -370,6 +381,14 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       int it = 0;
       int u = ubase;
       int pre = 0;
+      int ready_x = -1;  // linked launches: last instance whose inputs were acquired
+      auto wait_x = [&](const UnitCoord& c) {
+        const int inst = c.g / p.link_gpi;
+        if (inst != ready_x) {
+          wait_counter(p.dep_x + inst, p.dep_x_target);
+          ready_x = inst;
+        }
+      };
       if (u < p.units) {
         // Under programmatic dependent launch the weights do not depend on
         // the previous kernel but the activations do: request the first
@@ -380,14 +399,18 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           arm(i);
           load_w(i, c, c.kb0 + i * KPT);
         }
-        if (!GATHER) grid_dependency_wait();
+        if (!GATHER) {
+          if (p.dep_x) wait_x(c);
+          else grid_dependency_wait();
+        }
         for (int i = 0; i < pre; ++i) load_x(i, c, c.kb0 + i * KPT);
         it = pre;
-      } else if (!GATHER) {
+      } else if (!GATHER && !p.dep_x) {
         grid_dependency_wait();
       }
       for (; u < p.units; u += ustride) {
         const UnitCoord c = decode_unit(p, u, SWAP);
+        if (!GATHER && p.dep_x && pre == 0) wait_x(c);
         for (int kb = c.kb0 + pre * KPT; kb < c.kb1; kb += KPT, ++it) {
           const int stage = it % kStages;
           {
@@ -465,7 +488,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     // The residual tile and folded-LN statistics are fetched by these
     // threads ahead of the accumulator: order them after the previous launch
     // like the producer's operand loads.
-    if (kResTma || (kFold && (p.nin_stats || p.nres_stats))) grid_dependency_wait();
+    if ((kResTma || (kFold && (p.nin_stats || p.nres_stats))) && !p.dep_x)
+      grid_dependency_wait();
+    int ready_r = -1;  // linked launches: last instance whose residual was acquired
+    // linked launches: this unit's output tile is stored (the caller made the
+    // writes complete and ordered them before this thread): count it
+    auto publish = [&](int g) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      atomicAdd(p.done + g / p.link_gpi, 1u);
+    };
     const uint32_t stage_base = smem_u32(sOut);
     // Token-row staged tiles store progressively: each half of the epilogue
     // warps (4 warps = 128 rows x kColsPerThread columns) TMA-stores every
@@ -531,6 +563,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         // this half's staging blocks are free once its previous stores read them
         if (issuer) bulk_wait_read0();
         if constexpr (!kResTma) named_bar_sync(3 + half, 128);
+      }
+      if (HAS_RES && p.dep_r && c.g / p.link_gpi != ready_r) {
+        // linked: the residual's producer stored this instance's tiles
+        if (etid == 0) wait_counter(p.dep_r + c.g / p.link_gpi, p.dep_r_target);
+        named_bar_sync(1, kEpiThreads);
+        ready_r = c.g / p.link_gpi;
       }
       if constexpr (kResTma) issue_residual();
       if constexpr (kFold) {
@@ -837,6 +875,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       release_acc(acc);
       if constexpr (kProg) {
         if (p.splits > 1 && etid == 0) p.counters[wtile] = 0u;  // re-arm for the next launch
+        if (p.done) {
+          // both halves' stores complete, then one count for the tile
+          if (issuer) bulk_wait0();
+          named_bar_sync(1, kEpiThreads);
+          if (etid == 0) publish(c.g);
+        }
       } else if constexpr (C::kStaged) {
         fence_proxy_async_smem();
         named_bar_sync(1, kEpiThreads);
@@ -908,12 +952,20 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
                      make_float2(s, m2));
           }
         }
-        if (etid == 0) bulk_wait_read0();  // staging reusable
+        if (etid == 0) {
+          if (p.done) {
+            bulk_wait0();  // the tile is in global memory (and the staging free)
+            publish(c.g);
+          } else {
+            bulk_wait_read0();  // staging reusable
+          }
+        }
         named_bar_sync(1, kEpiThreads);
       } else {
-        if (p.splits > 1) {
-          named_bar_sync(1, kEpiThreads);
-          if (etid == 0) p.counters[wtile] = 0u;
+        if (p.splits > 1 || p.done) {
+          named_bar_sync(1, kEpiThreads);  // every thread's direct stores issued
+          if (etid == 0 && p.splits > 1) p.counters[wtile] = 0u;
+          if (etid == 0 && p.done) publish(c.g);
         }
       }
     }
@@ -944,14 +996,40 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       tma_load_4d(halo + hb * p.halo_bytes, &map_a, &hbar[hb], (c.g * p.cCg) & ~7, -p.cP,
                   oh_lo * p.cS - p.cP, 0, kEvictNormal);
     };
-    grid_dependency_wait();
-    if (gt == 0 && int(blockIdx.x) < p.units) issue_halo(blockIdx.x, 0);
+    // Linked launches: a halo is requested once its instance's input tiles
+    // are stored. The next unit's halo is prefetched only if that instance
+    // is already complete (non-blocking check); otherwise it is requested
+    // (blocking) when its unit starts, so a late instance never stalls the
+    // current unit's gather.
+    auto inst_ready = [&](int u, bool block) {
+      const int inst = decode_unit(p, u, false).g / p.link_gpi;
+      if (block) {
+        wait_counter(p.dep_x + inst, p.dep_x_target);
+        return true;
+      }
+      return counter_ready(p.dep_x + inst, p.dep_x_target);
+    };
+    bool halo_issued = true;  // the current unit's halo was requested (gt == 0)
+    if (!p.dep_x) grid_dependency_wait();
+    if (gt == 0 && int(blockIdx.x) < p.units) {
+      if (p.dep_x) inst_ready(blockIdx.x, true);
+      issue_halo(blockIdx.x, 0);
+    }
     int it = 0, local = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
       const int hb = local & 1;
-      if (gt == 0 && u + int(gridDim.x) < p.units) {
-        fence_proxy_async_smem();  // generic reads of that buffer (previous unit) done
-        issue_halo(u + gridDim.x, hb ^ 1);
+      if (gt == 0 && !halo_issued) {  // its prefetch was skipped: request it now
+        inst_ready(u, true);
+        fence_proxy_async_smem();  // generic reads of that buffer (two units ago) done
+        issue_halo(u, hb);
+      }
+      if (gt == 0) {
+        halo_issued = false;
+        if (u + int(gridDim.x) < p.units && (!p.dep_x || inst_ready(u + gridDim.x, false))) {
+          fence_proxy_async_smem();  // generic reads of that buffer (previous unit) done
+          issue_halo(u + gridDim.x, hb ^ 1);
+          halo_issued = true;
+        }
       }
       const UnitCoord c = decode_unit(p, u, false);
       const int p0 = c.ta * kGemmBM;
@@ -1040,10 +1118,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     const uint32_t jb = uint32_t(j * GATHER);
     const int taps = p.cK * p.cK;
     const int rows = SWAP ? p.rows_b : p.rows_a;
-    grid_dependency_wait();
-    int it = 0;
+    if (!p.dep_x) grid_dependency_wait();
+    int it = 0, ready = -1;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const UnitCoord c = decode_unit(p, u, SWAP);
+      if (p.dep_x && c.g / p.link_gpi != ready) {
+        // linked: this instance's input tiles are stored
+        if (gt == 0) wait_counter(p.dep_x + c.g / p.link_gpi, p.dep_x_target);
+        named_bar_sync(2, kGatherThreads);
+        ready = c.g / p.link_gpi;
+      }
       const int row0 = SWAP ? c.tb * BN : c.ta * kGemmBM;
       const __nv_bfloat16* xg = p.cx + int64_t(c.g) * p.cCg;
       int pix_off[PASSES], ih0[PASSES], iw0[PASSES];

@@ -23,14 +23,27 @@ struct NormFold {
   float* out_stats;
 };
 
+// Per-instance launch linking (see GemmParams::dep_x): counters are
+// [instance] tile counts; instance of group g = g / gpi.
+struct LinkSpec {
+  const unsigned* dep_x;
+  unsigned dep_x_target;
+  const unsigned* dep_r;
+  unsigned dep_r_target;
+  unsigned* done;
+  int gpi;
+};
+
 // gemm_sm100.cu — tcgen05 grouped GEMM (bf16 in, fp32 accumulate).
 bool linear_fold_supported(int64_t G, int64_t T, int64_t K, int64_t N);
 int grouped_linear_tc(const void* x, int64_t x_ld, int64_t x_gs, const void* w,
                       const float* bias, const void* residual, void* y, int64_t y_ld,
                       int64_t y_gs, int64_t G, int64_t T, int64_t K, int64_t N, int out_dtype,
                       int act, void* ws, int64_t ws_bytes, cudaStream_t stream,
-                      const NormFold* fold = nullptr);
+                      const NormFold* fold = nullptr, const LinkSpec* link = nullptr);
 int64_t linear_workspace_bytes(int64_t G, int64_t T, int64_t K, int64_t N);
+// output tiles one group publishes (a CTA pair's two halves count apart)
+int64_t linear_link_units(int64_t G, int64_t T, int64_t K, int64_t N);
 // One op of a chained launch (same operands as grouped_linear_tc).
 struct LinearOpDesc {
   const void* x;
@@ -87,7 +100,10 @@ int conv2d_simt(const void* x, const void* w, const float* bias, const float* sc
 // conv_igemm.cu — implicit-GEMM conv (tcgen05, cp.async im2col gather).
 int grouped_conv_tc(const void* x, const void* w, const float* bias, const void* residual,
                     void* y, int N, int H, int W, int C, int Cout, int G, int k, int stride,
-                    int pad, int Kpad, int relu, void* ws, int64_t ws_bytes, cudaStream_t stream);
+                    int pad, int Kpad, int relu, void* ws, int64_t ws_bytes, cudaStream_t stream,
+                    const LinkSpec* link = nullptr);
+int64_t conv_link_units(int64_t N, int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t G,
+                        int64_t k, int64_t stride, int64_t pad);
 int64_t conv_workspace_bytes(int64_t N, int64_t H, int64_t W, int64_t C, int64_t Cout, int64_t G,
                              int64_t k, int64_t stride, int64_t pad, int64_t Kpad);
 

@@ -154,6 +154,39 @@ class _QKVStep:
                       sc, st)
 
 
+class _LinkedStep:
+    """A merged conv launch (implicit GEMM, or a 1x1 conv as a grouped GEMM)
+    that :meth:`Plan._link_convs` may link per instance: its units of
+    instance m start once the launches producing its input / residual stored
+    m's tiles, and it counts its own stored tiles per instance."""
+
+    def __init__(self, kind, args, x, residual, y, groups, gpi, units, ws_need):
+        self.kind, self.args = kind, args  # "gemm" | "conv", plain-call arguments
+        self.x, self.residual, self.y = x, residual, y
+        self.groups, self.gpi, self.units = groups, gpi, units  # units: tiles per group
+        self.ws_need = ws_need
+        self.dep_x = self.dep_r = None  # (counters ptr, target)
+        self.done = None                 # counters ptr
+
+    def set_workspace(self, ptr, nbytes):
+        self.args = self.args[:-2] + (ptr, nbytes)  # both call forms end (ws, ws_bytes)
+
+    def __call__(self, st):
+        if self.dep_x is None and self.done is None:
+            name = "nf_grouped_linear_ws" if self.kind == "gemm" else "nf_grouped_conv_tc"
+            _lib.call(name, *self.args, st)
+            return
+        dx, tx = self.dep_x if self.dep_x else (None, 0)
+        dr, tr = self.dep_r if self.dep_r else (None, 0)
+        if self.kind == "gemm":
+            a = self.args  # nf_grouped_linear_ws arguments
+            _lib.call("nf_grouped_linear_linked", *a[:13], a[15], a[17], a[18], dx, tx, dr, tr,
+                      self.done, self.gpi, st)
+        else:
+            _lib.call("nf_grouped_conv_tc_linked", *self.args, dx, tx, dr, tr, self.done,
+                      self.gpi, st)
+
+
 @dataclass
 class _FoldedNorm:
     """A per-instance LayerNorm that is not launched: ``raw`` (G, T, D) holds
@@ -527,6 +560,61 @@ class Plan:
             del self._wcache[key]
         if self.fuse and self.chain and self.mcode == _lib.NF_MODE_FAST:
             self._chain_linears()
+            self._link_convs()
+
+    def _gpi(self, groups: int) -> int:
+        """Kernel groups per merged instance (0: unknown / not instance-aligned)."""
+        m = (getattr(self.graph, "metadata", None) or {}).get("merge", {}).get("num_models")
+        return groups // m if m and groups % m == 0 else 0
+
+    def _link_convs(self) -> None:
+        """Per-instance linking of merged conv launches (CNN plans): a conv
+        whose input and residual both come from linked conv launches starts
+        instance m's units once those stored m's tiles, instead of waiting for
+        the whole previous launch -- each launch's tail overlaps the next
+        launch's first instances. Linked launches with split-K get their own
+        workspace (they may overlap other launches); the counters live in one
+        buffer that a memset re-arms at the start of every forward."""
+        linked = [fn for _, fn, _ in self.steps if isinstance(fn, _LinkedStep) and fn.gpi > 0]
+        if not linked:
+            return
+        producers: dict[int, _LinkedStep] = {}
+        consumers = []
+        for fn in linked:
+            px = producers.get(fn.x)
+            pr = producers.get(fn.residual) if fn.residual else None
+            if px is not None and (fn.residual is None or pr is not None):
+                consumers.append((fn, px, pr))
+            producers[fn.y] = fn
+        if not consumers:
+            return
+        publishers = {id(p): p for _, px, pr in consumers for p in (px, pr) if p is not None}
+        m = self.graph.metadata["merge"]["num_models"]
+        buf = self._own(torch.zeros(-(-m * len(publishers) // 64) * 64, dtype=torch.int32,
+                                    device=self.device))
+        for i, p in enumerate(publishers.values()):
+            p.done = buf[i * m:].data_ptr()
+        for fn, px, pr in consumers:
+            fn.dep_x = (px.done, px.units * px.gpi)
+            if pr is not None:
+                fn.dep_r = (pr.done, pr.units * pr.gpi)
+        for fn in {id(f): f for f in [c[0] for c in consumers] + list(publishers.values())}.values():
+            if fn.ws_need > 0:
+                ws = self._own(torch.zeros(fn.ws_need, dtype=torch.uint8, device=self.device))
+                fn.set_workspace(ws.data_ptr(), ws.numel())
+        self._add_rearm(buf)
+
+    def _add_rearm(self, buf: torch.Tensor) -> None:
+        """Zero ``buf`` (per-instance counters) at the start of every forward."""
+        if getattr(self, "_rearm_bufs", None) is None:
+            self._rearm_bufs = []
+
+            def rearm(st, bufs=self._rearm_bufs):
+                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=bufs[0].device)):
+                    for b in bufs:
+                        b.zero_()
+            self.steps.insert(0, ("rearm", rearm, 0))
+        self._rearm_bufs.append(buf)
 
     def _chainable(self, ls, run) -> bool:
         if not isinstance(ls, _LinearStep) or ls.dcode != _lib.NF_BF16 \
@@ -627,13 +715,9 @@ class Plan:
             self._qkv_done = done
             linked = True
         if linked:
-            bufs = [self._chain_counters] + ([self._qkv_done] if qkv_links else [])
-
-            def rearm(st, bufs=bufs):
-                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=bufs[0].device)):
-                    for b in bufs:
-                        b.zero_()
-            self.steps.insert(0, ("chain:rearm", rearm, 0))
+            self._add_rearm(self._chain_counters)
+            if qkv_links:
+                self._add_rearm(self._qkv_done)
 
     def linear_steps(self) -> dict[str, "_LinearStep"]:
         """node id -> its merged-Linear launch description (chained or not)."""
@@ -882,9 +966,13 @@ class Plan:
             xp, wp, bp, yp = xn.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
             ws = self._workspace(groups, pix, cg, coutg)
             wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
-            self._emit(conv.id, lambda st: _lib.call(
-                "nf_grouped_linear_ws", xp, c, cg, wp, bp, rp, yp, cout, coutg, groups, pix,
-                cg, coutg, _lib.NF_BF16, _lib.NF_W_NK, act, _lib.NF_MODE_FAST, wsp, wsb, st))
+            args = (xp, c, cg, wp, bp, rp, yp, cout, coutg, groups, pix, cg, coutg, _lib.NF_BF16,
+                    _lib.NF_W_NK, act, _lib.NF_MODE_FAST, wsp, wsb)
+            lib = _lib.load()
+            self._emit(conv.id, _LinkedStep(
+                "gemm", args, xp, rp, yp, groups, self._gpi(groups),
+                int(lib.nf_linear_link_units(groups, pix, cg, coutg)),
+                int(lib.nf_linear_workspace_bytes(groups, pix, cg, coutg))))
         elif coutg % 4 == 0:
             # implicit GEMM: im2col rows gathered on chip (cp.async), never in HBM.
             # Narrow groups (ResNeXt: 4..16 channels) are densified into
@@ -922,9 +1010,12 @@ class Plan:
             ws = self._ws_buffer(need) if need > 0 else None
             wsp, wsb = (ws.data_ptr(), ws.numel()) if ws is not None else (None, 0)
             xp, wp, bp, yp = xn.data_ptr(), wg.data_ptr(), bg.data_ptr(), yn.data_ptr()
-            self._emit(conv.id, lambda st: _lib.call(
-                "nf_grouped_conv_tc", xp, wp, bp, rp, yp, n, h, wd, c_in, cout, groups, k, s,
-                pad, kpad, relu, wsp, wsb, st))
+            args = (xp, wp, bp, rp, yp, n, h, wd, c_in, cout, groups, k, s, pad, kpad, relu,
+                    wsp, wsb)
+            self._emit(conv.id, _LinkedStep(
+                "conv", args, xp, rp, yp, groups, self._gpi(groups),
+                int(_lib.load().nf_conv_link_units(n, h, wd, c_in, cout, groups, k, s, pad)),
+                need))
         else:
             wkey = key + ("direct",)
             if wkey not in self._wcache:

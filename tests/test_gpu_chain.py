@@ -113,3 +113,24 @@ def test_chain_rejects_unsupported_shapes():
     assert lib.nf_linear_chain_supported(8, 1024, 768, 3072) == 0  # token-row tiles
     assert lib.nf_linear_chain_supported(8, 128, 768, 200) == 0    # n % 128
     assert lib.nf_grouped_linear_chain(0, None, 1, None, None) == _lib.NF_ERR_SHAPE
+
+
+@pytest.mark.parametrize("name,m", [("resnext50_32x4d", 4), ("resnet50", 2)])
+def test_linked_conv_launches_bit_identical(name, m):
+    """Merged CNN plans link conv launches per instance (a conv starts
+    instance k once its input / residual producers stored k's tiles): the
+    outputs are bit-identical to the unlinked plan, on every replay."""
+    graph, stores = W.build_zoo(name, num_models=m, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    bound = merged.bind_inputs([model_inputs(graph, seed=2, model=j) for j in range(m)])
+    linked = compile_plan(merged.graph, mstore)
+    kinds = [type(fn).__name__ for _, fn, _ in linked.steps]
+    assert sum(getattr(fn, "dep_x", None) is not None for _, fn, _ in linked.steps) >= 40
+    ref = compile_plan(merged.graph, mstore, chain=False)
+    assert not any(getattr(fn, "dep_x", None) for _, fn, _ in ref.steps)
+    got = _run(linked, bound, replays=3)
+    want = _run(ref, bound)[0]
+    for rep in got:
+        for a, b in zip(rep, want):
+            assert torch.equal(a, b)
+    assert "rearm" == linked.steps[0][0] and "_LinkedStep" in kinds

@@ -33,7 +33,7 @@ def test_bert_glue_is_zero_copy():
     assert "chain:merged::l00.proj+merged::l00.ff1+merged::l00.ff2" in ids
     # the chains' counters are re-armed by one memset at the start (layer 1's
     # attention waits on layer 0's chain per instance)
-    assert ids[0] == "chain:rearm"
+    assert ids[0] == "rearm"
     unchained = Plan(merged.graph, mstore, device="cpu", chain=False)
     assert len(unchained.steps) == unchained.kernel_launches == 2 * 4 + 1
     assert not any("res" in nid for nid, _, _ in plan.steps)
