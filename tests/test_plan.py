@@ -142,3 +142,33 @@ def test_sibling_heads_batch_into_grouped_launches():
     # pooler (tanh fused) and classifier: one launch each for all 3 models
     assert head_steps == ["head0::pool", "head0::logits"]
     assert [plan.vals[f"head{j}::logits"].dims for j in range(3)] == [(1, 2), (1, 3), (1, 5)]
+
+
+def test_cnn_conv_launches_link_per_instance():
+    """Merged CNN plans: every conv whose input and residual come from conv
+    launches waits on those launches' per-instance tile counters (targets =
+    producer tiles per group x groups per instance); linked launches with
+    split-K own their workspace; one memset step re-arms the counters."""
+    graph, stores = W.build_zoo("resnext50_32x4d", num_models=4, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    plan = Plan(merged.graph, mstore, device="cpu")
+    steps = [fn for _, fn, _ in plan.steps if type(fn).__name__ == "_LinkedStep"]
+    assert plan.steps[0][0] == "rearm" and plan.steps[0][2] == 0  # a memset, not a kernel
+    by_y = {fn.y: fn for fn in steps}
+    consumers = [fn for fn in steps if fn.dep_x is not None]
+    assert len(consumers) >= 48
+    for fn in consumers:
+        px = by_y[fn.x]
+        assert px.done is not None and fn.dep_x == (px.done, px.units * px.gpi)
+        assert (fn.residual is None) == (fn.dep_r is None)
+        if fn.residual is not None:
+            pr = by_y[fn.residual]
+            assert fn.dep_r == (pr.done, pr.units * pr.gpi)
+        assert fn.gpi * 4 == fn.groups
+    shared = getattr(plan, "_ws", None)
+    for fn in steps:
+        if (fn.dep_x is not None or fn.done is not None) and fn.ws_need > 0:
+            assert shared is None or fn.args[-2] != shared.data_ptr()
+    # without chaining / linking nothing waits per instance
+    ref = Plan(merged.graph, mstore, device="cpu", chain=False)
+    assert not any(getattr(fn, "dep_x", None) for _, fn, _ in ref.steps)
