@@ -312,11 +312,15 @@ def run_ours(args) -> dict | None:
     import torch.distributed as dist
 
     world, rank, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
+    # one rank per GPU; --dist-backend gloo lets several ranks share a GPU
+    # (a functional check of the multi-rank path on a one-GPU box)
+    dev = torch.device("cuda", local % max(torch.cuda.device_count(), 1) if world > 1 else 0)
     torch.cuda.set_device(dev)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     from paper_2009_13062_b200 import PipelinedRunner, compile_plan
 
@@ -377,7 +381,8 @@ def run_ours(args) -> dict | None:
         gms = ge0.elapsed_time(ge1)
         t = torch.tensor([gms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gather = {"collective": "all_gather (NCCL) of per-instance logits, after timing",
+        gather = {"collective": f"all_gather ({args.dist_backend}) of per-instance logits, "
+                                "after timing",
                   "ms": round(float(t.item()), 4),
                   "bytes_per_rank": sum(x.numel() * x.element_size() for x in logits),
                   "instances_gathered": len(got) if got is not None else None}
@@ -463,7 +468,8 @@ def run_ours(args) -> dict | None:
             "batch": args.batch,
             "seq_len": 128 if "bert" in args.model or "xlnet" in args.model else None,
             "image": 224 if "res" in args.model else None,
-            "parallelism": f"instance-shard x{world} (no collective on the hot path)",
+            "parallelism": f"instance-shard x{world} (no collective on the hot path)"
+                           + (f", {args.dist_backend}" if world > 1 else ""),
             "l2": "flushed between timed steps (256 MiB write outside the events)",
             "timing": "CUDA events around each CUDA-graph replay; max over ranks",
         },
@@ -793,6 +799,8 @@ def main(argv=None) -> int:
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--dtype", default=None)
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend under torchrun (gloo: ranks may share a GPU)")
     ap.add_argument("--no-heads", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-unmerged", action="store_true",
