@@ -563,7 +563,6 @@ __global__ void k_rel_attention_simt(const T* __restrict__ qkv, const T* __restr
 // reuses TMEM cols [0,64). 256 TMEM cols + ~86 KB smem -> 2 CTAs per SM.
 // ---------------------------------------------------------------------------
 constexpr int kRelPitch = 68;                           // words per staged row
-constexpr int kRelStageBytes = 4 * 32 * kRelPitch * 4;  // 34816 B (4 warps)
 
 // positional keys r viewed as 4-D (dh, H, 2S, Bt); box (64, 1, 128, 1).
 bool make_r_map(CUtensorMap* map, const void* r, int64_t Bt, int64_t S, int64_t H) {

@@ -1055,15 +1055,22 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           const int kh = tap / p.cK;
           const int tap_off = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp + ch;
           const bool tap_ok = tap < taps;
+          // all eight 16-byte reads first, then the eight writes: one
+          // shared-memory latency per k-block instead of eight in series
+          uint32_t v[8][4];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0;
+            if (tap_ok && hoff[i] >= 0)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v[i][0]), "=r"(v[i][1]), "=r"(v[i][2]), "=r"(v[i][3])
+                           : "r"(hsrc + uint32_t((hoff[i] * p.halo_cpp + tap_off) * 2)));
+          }
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = rb + 16 * i;
-            uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-            if (tap_ok && hoff[i] >= 0)
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                           : "r"(hsrc + uint32_t((hoff[i] * p.halo_cpp + tap_off) * 2)));
-            st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v0, v1, v2, v3);
+            st_shared_v4(sbase + uint32_t(r * 128) + (uint32_t(j ^ (r & 7)) << 4), v[i][0],
+                         v[i][1], v[i][2], v[i][3]);
           }
         } else {
           // 4-channel groups (padded stem): two taps per 16-byte chunk
