@@ -330,15 +330,20 @@ __global__ void __launch_bounds__(kTThreads, 1)
     // split pass of a landed stage: hi in place, lo into the A-lo slot
     auto split_stage = [&](int s) {
       const uint32_t h0 = smem_u32(a_hi(s)), l0 = smem_u32(a_lo(s));
+      // the eight 16-byte reads first, then split + write back: one
+      // shared-memory latency per stage instead of eight in series
+      uint32_t w[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                     : "r"(h0 + chunk_off(i)));
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint32_t o = chunk_off(i);
-        uint32_t w[4], hi[4], lo[4];
-        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-                     : "r"(h0 + o));
+        uint32_t hi[4], lo[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) split_tf32(w[e], hi[e], lo[e]);
+        for (int e = 0; e < 4; ++e) split_tf32(w[i][e], hi[e], lo[e]);
         st_shared_v4(h0 + o, hi[0], hi[1], hi[2], hi[3]);
         st_shared_v4(l0 + o, lo[0], lo[1], lo[2], lo[3]);
       }
