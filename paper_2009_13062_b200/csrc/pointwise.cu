@@ -400,17 +400,46 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
   fence_barrier_init();
   __syncwarp();
   grid_dependents_launch();
-  auto base_of = [&](int u) {
-    const int row = u / G, grp = u - (u / G) * G;
-    const int r1 = row / R2, r2 = row - r1 * R2;
-    return int64_t(r1) * g.s1 + int64_t(r2) * g.s2 + int64_t(grp) * g.sg;
+  // A warp walks a contiguous unit range: (group, r2, r1) and the affine
+  // block advance incrementally (one set of divisions per warp, not per row;
+  // the kernel is issue-bound). Two cursors: the TMA issue (lane 0) runs
+  // kNormDepth units ahead of the one being normalised.
+  struct Cursor {
+    int grp, r2, r1, arow, ablk;
+    int64_t base;
   };
-  auto aff_of = [&](int u) {
-    const int row = u / G, grp = u - (u / G) * G;
-    return (g.rows_per_affine > 0 ? int64_t(row / int(g.rows_per_affine)) : 0) * g.G * g.Cg +
-           int64_t(grp) * Cg;
+  const int rpa = g.rows_per_affine > 0 ? int(g.rows_per_affine) : 0;
+  auto cursor_at = [&](int u) {
+    Cursor k;
+    const int row = u / G;
+    k.grp = u - row * G;
+    k.r1 = row / R2;
+    k.r2 = row - k.r1 * R2;
+    k.ablk = rpa ? row / rpa : 0;
+    k.arow = rpa ? row - k.ablk * rpa : 0;
+    k.base = int64_t(k.r1) * g.s1 + int64_t(k.r2) * g.s2 + int64_t(k.grp) * g.sg;
+    return k;
   };
-  float ga[Q * V], be[Q * V];
+  auto advance = [&](Cursor& k) {
+    if (++k.grp < G) {
+      k.base += g.sg;
+      return;
+    }
+    k.grp = 0;
+    if (rpa && ++k.arow == rpa) {
+      k.arow = 0;
+      ++k.ablk;
+    }
+    if (++k.r2 == R2) {
+      k.r2 = 0;
+      ++k.r1;
+    }
+    k.base = int64_t(k.r1) * g.s1 + int64_t(k.r2) * g.s2;
+  };
+  auto aff_of = [&](const Cursor& k) {
+    return int64_t(k.ablk) * g.G * g.Cg + int64_t(k.grp) * Cg;
+  };
+  float2 ga[Q * V / 2], be[Q * V / 2];
   int64_t aff_cur = -1;
   auto load_affine = [&](int64_t aff) {
 #pragma unroll
@@ -421,28 +450,33 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
         for (int e = 0; e < V; e += 4) {
           const float4 a4 = __ldg(reinterpret_cast<const float4*>(gamma + aff + ch * V + e));
           const float4 b4 = __ldg(reinterpret_cast<const float4*>(beta + aff + ch * V + e));
-          ga[q * V + e] = a4.x; ga[q * V + e + 1] = a4.y; ga[q * V + e + 2] = a4.z;
-          ga[q * V + e + 3] = a4.w;
-          be[q * V + e] = b4.x; be[q * V + e + 1] = b4.y; be[q * V + e + 2] = b4.z;
-          be[q * V + e + 3] = b4.w;
+          ga[(q * V + e) / 2] = make_float2(a4.x, a4.y);
+          ga[(q * V + e) / 2 + 1] = make_float2(a4.z, a4.w);
+          be[(q * V + e) / 2] = make_float2(b4.x, b4.y);
+          be[(q * V + e) / 2 + 1] = make_float2(b4.z, b4.w);
         }
       }
     }
     aff_cur = aff;
   };
-  if (u0 < u1) load_affine(aff_of(u0));  // a weight: before the dependency wait
+  Cursor cur = cursor_at(u0 < u1 ? u0 : 0);
+  if (u0 < u1) load_affine(aff_of(cur));  // a weight: before the dependency wait
   grid_dependency_wait();
   if (u0 >= u1) return;
-  auto issue = [&](int u) {
+  Cursor nxt = cur;
+  auto issue = [&](int u, const Cursor& k) {
     const int slot = (u - u0) % kNormDepth;
-    const int64_t b = base_of(u);
     uint8_t* dst = ring + size_t(slot) * 2 * kNormRowBytes;
     mbar_arrive_expect_tx(&bars[slot], has_res ? 2 * row_bytes : row_bytes);
-    bulk_load_1d(dst, x + b, row_bytes, &bars[slot]);
-    if (has_res) bulk_load_1d(dst + kNormRowBytes, res + b, row_bytes, &bars[slot]);
+    bulk_load_1d(dst, x + k.base, row_bytes, &bars[slot]);
+    if (has_res) bulk_load_1d(dst + kNormRowBytes, res + k.base, row_bytes, &bars[slot]);
   };
+  int un = u0;  // next unit to issue (lane 0's cursor `nxt`)
   if (lane == 0)
-    for (int u = u0; u < min(u1, u0 + kNormDepth); ++u) issue(u);
+    for (; un < min(u1, u0 + kNormDepth); ++un) {
+      issue(un, nxt);
+      advance(nxt);
+    }
   for (int u = u0; u < u1; ++u) {
     const int k = u - u0;
     const int slot = k % kNormDepth;
@@ -458,16 +492,19 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
       }
     }
     __syncwarp();  // every lane has its chunks: the slot can be refilled
-    if (lane == 0 && u + kNormDepth < u1) {
+    if (lane == 0 && un < u1) {
       fence_proxy_async_smem();  // generic reads of the slot before the async refill
-      issue(u + kNormDepth);
+      issue(un, nxt);
+      advance(nxt);
+      ++un;
     }
-    const int64_t aff = aff_of(u);
+    const int64_t aff = aff_of(cur);
     if (aff != aff_cur) load_affine(aff);
     // two passes over the registers: mean, then the centred sum of squares
-    // (no E[x^2] - mean^2 cancellation when |mean| >> std)
-    float v[Q * V];
-    float sum = 0.f;
+    // (no E[x^2] - mean^2 cancellation when |mean| >> std); element pairs in
+    // packed fp32x2 arithmetic (FADD2 / FFMA2: half the FP instructions)
+    float2 v[Q * V / 2];
+    float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       if (lane + 32 * q < nchunks) {
@@ -476,29 +513,26 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
 #pragma unroll
         for (int e = 0; e < V / 2; ++e) {
           float2 t = __bfloat1622float2(px[e]);
-          if (has_res) {
-            const float2 r2 = __bfloat1622float2(pr[e]);
-            t.x = __fadd_rn(t.x, r2.x);
-            t.y = __fadd_rn(t.y, r2.y);
-          }
-          v[q * V + 2 * e] = t.x;
-          v[q * V + 2 * e + 1] = t.y;
-          sum += t.x + t.y;
+          if (has_res) t = __fadd2_rn(t, __bfloat1622float2(pr[e]));
+          v[q * V / 2 + e] = t;
+          sum2 = __fadd2_rn(sum2, t);
         }
       }
     const float inv_c = 1.0f / float(Cg);
-    const float mean = warp_sum(sum) * inv_c;
-    float sq = 0.f;
+    const float mean = warp_sum(sum2.x + sum2.y) * inv_c;
+    const float2 nmean = make_float2(-mean, -mean);
+    float2 sq2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       if (lane + 32 * q < nchunks)
 #pragma unroll
-        for (int e = 0; e < V; ++e) {
-          const float d = v[q * V + e] - mean;
-          sq = fmaf(d, d, sq);
+        for (int e = 0; e < V / 2; ++e) {
+          const float2 d = __fadd2_rn(v[q * V / 2 + e], nmean);
+          v[q * V / 2 + e] = d;
+          sq2 = __ffma2_rn(d, d, sq2);
         }
-    const float rstd = rsqrtf(warp_sum(sq) * inv_c + g.eps);
-    const int64_t b = base_of(u);
+    const float rstd = rsqrtf(warp_sum(sq2.x + sq2.y) * inv_c + g.eps);
+    const float2 rstd2 = make_float2(rstd, rstd);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int ch = lane + 32 * q;
@@ -507,13 +541,14 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
         uint32_t* po = reinterpret_cast<uint32_t*>(&uo);
 #pragma unroll
         for (int e = 0; e < V / 2; ++e) {
-          const int i0 = q * V + 2 * e;
-          const float a0 = ga[i0] * rstd, a1 = ga[i0 + 1] * rstd;
-          po[e] = pack_bf16x2(fmaf(v[i0] - mean, a0, be[i0]), fmaf(v[i0 + 1] - mean, a1, be[i0 + 1]));
+          const int i = q * V / 2 + e;
+          const float2 o = __ffma2_rn(v[i], __fmul2_rn(ga[i], rstd2), be[i]);
+          po[e] = pack_bf16x2(o.x, o.y);
         }
-        *reinterpret_cast<uint4*>(y + b + int64_t(ch) * V) = uo;
+        *reinterpret_cast<uint4*>(y + cur.base + int64_t(ch) * V) = uo;
       }
     }
+    advance(cur);
   }
 }
 constexpr size_t kNormTmaSmem =
