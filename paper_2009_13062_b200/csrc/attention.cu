@@ -261,9 +261,10 @@ constexpr size_t kAttnSmem = 1024 + 5 * kTileBytes + 64;
 // two 4-warp CTAs per SM already overlap their softmax phases.)
 
 // Persistent variant for many (sequence, head) units: each CTA walks units
-// u = blockIdx.x, += gridDim.x with the next unit's Q/K/V tiles loading into
-// the other half of a double buffer while the current unit runs; P (bf16
-// 128 x 128) reuses the current unit's Q|K slots once S = Q K^T retired.
+// u = blockIdx.x, += gridDim.x over a double buffer of Q/K/V tiles; a
+// buffer is refilled with the unit two ahead as soon as its unit's PV MMA
+// retired; P (bf16 128 x 128) reuses the current unit's Q|K slots once
+// S = Q K^T retired.
 // 2 x 48 KB of tiles + barriers -> two CTAs per SM (256 TMEM cols each).
 constexpr size_t kAttnPSmem = 1024 + 6 * kTileBytes + 128;
 
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(128, 2)
   if (tid == 0) {
     grid_dependency_wait();
     if (int(blockIdx.x) < units) issue(blockIdx.x, 0);
+    if (int(blockIdx.x + gridDim.x) < units) issue(blockIdx.x + gridDim.x, 1);
   }
   grid_dependents_launch();
 
@@ -320,9 +322,6 @@ __global__ void __launch_bounds__(128, 2)
     uint8_t* sV = sK + kTileBytes;
     uint8_t* sP = sQ;  // Q|K, free once S is in TMEM
     const int bt = u / H, h = u % H;
-    // next unit's tiles into the other buffer (its last reader, the previous
-    // unit's PV MMA, retired before that unit's epilogue)
-    if (tid == 0 && u + int(gridDim.x) < units) issue(u + gridDim.x, buf ^ 1);
     mbar_wait(&bar_load[buf], uint32_t(i >> 1) & 1u);
     if (tid == 0) {
       tc_fence_after();
@@ -392,6 +391,10 @@ __global__ void __launch_bounds__(128, 2)
       umma_commit(bar_o);
     }
     mbar_wait(bar_o, uint32_t(i) & 1u);
+    // this unit's Q | K (P) and V are consumed: the unit after next streams
+    // into them during this epilogue and the next unit's work (two units'
+    // tiles in flight instead of one)
+    if (tid == 0 && u + 2 * int(gridDim.x) < units) issue(u + 2 * gridDim.x, buf);
     tc_fence_after();
     {
       uint32_t o[2][32];
