@@ -56,6 +56,7 @@ constexpr int kMaxSplits = 8;
 #define NF_GEMM_BUDGET_KB 220  // smem for the operand ring + output staging
 #endif
 constexpr int64_t kCounterBytes = 64 * 1024;  // semaphores at the workspace head
+static __device__ float g_zero_bias[1];  // bias operand of bias-free launches
 
 #ifdef NF_GEMM_TRACE
 // Per-CTA pipeline timestamps (globaltimer ns), 8 slots per CTA:
@@ -600,9 +601,14 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       // per lane fits where a float4 x 8 per thread would spill.
       constexpr bool kBiasAhead = !SWAP && EC == 32;
       float bpre = 0.f;
+      // an unconditional load (clamped index, a zero word when there is no
+      // bias): a select on the loaded value made the prefetch wait for it
+      // right away (the FF1 epilogue's top stall in ncu)
+      const float* bsrc = p.bias ? p.bias + int64_t(c.g) * p.features : g_zero_bias;
+      const int blast = p.bias ? p.rows_b - 1 : 0;
       auto bias_chunk = [&](int cc_) {
         const int f = c.tb * BN + cc_ + lane;
-        bpre = (p.bias && f < p.rows_b) ? __ldg(p.bias + int64_t(c.g) * p.features + f) : 0.f;
+        bpre = __ldg(bsrc + (f < blast ? f : blast));  // columns past N are not stored
       };
       if constexpr (kBiasAhead) bias_chunk(((warp - 2) >> 2) * kColsPerThread);
       // swapped tiles: this thread's feature row constants, loaded ahead too
