@@ -161,6 +161,9 @@ struct GemmOut {
   static constexpr bool kStaged = BN >= 64;
 };
 
+#ifndef NF_GEMM_PAIR_KB
+#define NF_GEMM_PAIR_KB 225  // CTA-pair 128 x 256 tiles: 5 stages of 32 KB + 64 KB staging
+#endif
 #ifndef NF_GEMM_GATHER_KB
 #define NF_GEMM_GATHER_KB NF_GEMM_BUDGET_KB
 #endif
@@ -190,7 +193,7 @@ struct GemmCfg {
       GATHER == 1 ? (NF_GEMM_HALO_KB > kMinKB ? NF_GEMM_HALO_KB : kMinKB)
       : GATHER ? (NF_GEMM_GATHER_KB > kMinKB ? NF_GEMM_GATHER_KB : kMinKB)
       : KPT > 1 ? 225
-      : BN >= 256 ? (PAIR ? 225 : 220)
+      : BN >= 256 ? (PAIR ? NF_GEMM_PAIR_KB : 220)
                   : (SWAP ? (kStaged ? NF_GEMM_SWAP_KB : NF_GEMM_LITE_KB) : NF_GEMM_BUDGET_KB);
   static constexpr int kStages = (kBudgetKB * 1024 - kOutBytes) / kStageBytes;
   // two accumulator buffers; tcgen05.alloc takes a power of two >= 32
