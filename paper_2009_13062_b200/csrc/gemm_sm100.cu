@@ -286,6 +286,7 @@ int grouped_linear_chain_tc(int nops, const LinearOpDesc* ops, unsigned* counter
     const int st = linear_setup(d.ws, d.ws_bytes, d.G, d.T, d.K, d.N, NF_BF16, d.act, d.bias,
                                 d.residual, d.y, d.y_ld, d.y_gs, fold, o.p, L);
     if (st != NF_OK) return st;
+    o.p = gemm_params_finalize(o.p);
     if (!make_bf16_map_kpt2(&o.ma, d.w, d.G, d.N, d.K, kGemmBM, 0, 0, 2) ||
         !make_bf16_map_kpt2(&o.mb, d.x, d.G, d.T, d.K, 128, d.x_ld, d.x_gs, 2) ||
         !make_bf16_map_kpt2(&o.my, d.y, d.G, d.T, d.N, 128, d.y_ld, d.y_gs, 2))

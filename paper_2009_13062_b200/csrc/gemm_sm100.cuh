@@ -88,6 +88,25 @@ __device__ unsigned long long g_gemm_wait[148 * 8];
   } while (0)
 #endif
 
+// n / d for 0 <= n < 2^31 by a multiply-high and a shift (Granlund-Montgomery
+// round-up reciprocal; exhaustively checked for the divisor ranges used).
+// Unit decode and the implicit-GEMM gather divide by run-time extents per
+// unit / per k-block: ~20 instructions each as integer divisions, which the
+// short-K gather warps of the grouped 3x3 convs spent ~10% of their stall
+// samples on.
+struct FastDiv {
+  uint32_t m = 0, s = 0;
+  static FastDiv make(int d) {
+    FastDiv f;
+    while ((1u << f.s) < uint32_t(d)) ++f.s;
+    f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << f.s) - uint64_t(d))) / uint64_t(d) + 1);
+    return f;
+  }
+  NF_DEVICE int div(int n) const {
+    return int((__umulhi(uint32_t(n), m) + uint32_t(n)) >> s);
+  }
+};
+
 struct GemmParams {
   int act;               // fused epilogue activation (NF_ACT_*)
   const float* bias;     // (G, features) fp32 or nullptr
@@ -98,6 +117,8 @@ struct GemmParams {
   int features;          // N (bias stride per instance)
   int tiles_a, tiles_b, groups;
   int splits, kb_total, kb_per_split, units;
+  // divisors of the unit decode / conv gather (gemm_params_finalize)
+  FastDiv fd_splits, fd_ta, fd_tb, fd_cWo, fd_cHo, fd_cCg, fd_cK;
   float* ws;             // split-K partials [tile][split][128][BN]
   unsigned* counters;    // [tile] arrival semaphores (zero between launches)
   void* y_direct;        // y for tiles stored straight from registers (!kStaged)
@@ -224,20 +245,35 @@ struct UnitCoord {
   int g, ta, tb, s, tile, kb0, kb1;
 };
 
+// The divisors the kernels use, from the extents (every launch path).
+inline GemmParams gemm_params_finalize(GemmParams p) {
+  auto pos = [](int v) { return v > 0 ? v : 1; };
+  p.fd_splits = FastDiv::make(pos(p.splits));
+  p.fd_ta = FastDiv::make(pos(p.tiles_a));
+  p.fd_tb = FastDiv::make(pos(p.tiles_b));
+  p.fd_cWo = FastDiv::make(pos(p.cWo));
+  p.fd_cHo = FastDiv::make(pos(p.cHo));
+  p.fd_cCg = FastDiv::make(pos(p.cCg));
+  p.fd_cK = FastDiv::make(pos(p.cK));
+  return p;
+}
+
 NF_DEVICE UnitCoord decode_unit(const GemmParams& p, int u, bool swap) {
   UnitCoord c;
-  c.s = u % p.splits;
-  c.tile = u / p.splits;
+  c.tile = p.fd_splits.div(u);
+  c.s = u - c.tile * p.splits;
   // swapped: B (tokens) fastest; normal: A (token tiles) fastest, so CTAs
   // running concurrently share one weight tile in L2.
   if (swap) {
-    c.tb = c.tile % p.tiles_b;
-    c.ta = (c.tile / p.tiles_b) % p.tiles_a;
-    c.g = c.tile / (p.tiles_b * p.tiles_a);
+    const int q = p.fd_tb.div(c.tile);
+    c.tb = c.tile - q * p.tiles_b;
+    c.g = p.fd_ta.div(q);
+    c.ta = q - c.g * p.tiles_a;
   } else {
-    c.ta = c.tile % p.tiles_a;
-    c.tb = (c.tile / p.tiles_a) % p.tiles_b;
-    c.g = c.tile / (p.tiles_a * p.tiles_b);
+    const int q = p.fd_ta.div(c.tile);
+    c.ta = c.tile - q * p.tiles_a;
+    c.g = p.fd_tb.div(q);
+    c.tb = q - c.g * p.tiles_b;
   }
   c.kb0 = c.s * p.kb_per_split;
   c.kb1 = min(p.kb_total, c.kb0 + p.kb_per_split);
@@ -998,7 +1034,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     const int hw = p.halo_w;
     auto issue_halo = [&](int u, int hb) {
       const UnitCoord c = decode_unit(p, u, false);
-      const int oh_lo = (c.ta * kGemmBM) / p.cWo;
+      const int oh_lo = p.fd_cWo.div(c.ta * kGemmBM);
       mbar_arrive_expect_tx(&hbar[hb], p.halo_tx);
       // the box's first channel must sit on a 16-byte boundary: 4-channel
       // groups start at the even-group boundary and index +4 inside the pixel
@@ -1042,12 +1078,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
       }
       const UnitCoord c = decode_unit(p, u, false);
       const int p0 = c.ta * kGemmBM;
-      const int oh_lo = p0 / p.cWo;
+      const int oh_lo = p.fd_cWo.div(p0);
       int hoff[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int pix = p0 + rb + 16 * i;
-        const int oh = pix / p.cWo, ow = pix - (pix / p.cWo) * p.cWo;
+        const int oh = p.fd_cWo.div(pix), ow = pix - oh * p.cWo;
         hoff[i] = pix < rows ? ((oh - oh_lo) * p.cS * hw + ow * p.cS) : -1;
       }
       const uint32_t hsrc = smem_u32(halo + hb * p.halo_bytes) + uint32_t(((c.g * p.cCg) & 7) * 2);
@@ -1059,9 +1095,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         const uint32_t sbase = smem_u32(sA + stage * C::kABytes);
         if (p.cCg >= 8) {
           // chunk j = K elements [k0, k0+8) of one tap: one 16-byte copy per row
-          const int tap = k0 / p.cCg;
+          const int tap = p.fd_cCg.div(k0);
           const int ch = k0 - tap * p.cCg;
-          const int kh = tap / p.cK;
+          const int kh = p.fd_cK.div(tap);
           const int tap_off = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp + ch;
           const bool tap_ok = tap < taps;
           // all eight 16-byte reads first, then the eight writes: one
@@ -1087,8 +1123,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           bool okh[2];
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            const int tap = (k0 + hh * 4) / p.cCg;
-            const int kh = tap / p.cK;
+            const int tap = p.fd_cCg.div(k0 + hh * 4);
+            const int kh = p.fd_cK.div(tap);
             off[hh] = (kh * hw + (tap - kh * p.cK)) * p.halo_cpp;
             okh[hh] = tap < taps;
           }
@@ -1150,10 +1186,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
 #pragma unroll
       for (int i = 0; i < PASSES; ++i) {
         const int pix = row0 + r0 + RPP * i;
-        const int ow = pix % p.cWo;
-        const int t2 = pix / p.cWo;
-        const int oh = t2 % p.cHo;
-        const int n = t2 / p.cHo;
+        const int t2 = p.fd_cWo.div(pix);
+        const int ow = pix - t2 * p.cWo;
+        const int n = p.fd_cHo.div(t2);
+        const int oh = t2 - n * p.cHo;
         ih0[i] = pix < rows ? oh * p.cS - p.cP : -(1 << 20);
         iw0[i] = ow * p.cS - p.cP;
         pix_off[i] = n * p.cH * p.cW;
@@ -1162,9 +1198,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
         const int stage = it % kStages;
         mbar_wait(&empty[stage], ((it / kStages) & 1) ^ 1);
         const int k0 = kb * kGemmBK + j * CE;
-        const int tap = k0 / p.cCg;
+        const int tap = p.fd_cCg.div(k0);
         const int ch = k0 - tap * p.cCg;
-        const int kh = tap / p.cK;
+        const int kh = p.fd_cK.div(tap);
         const int kw = tap - kh * p.cK;
         const bool tap_ok = tap < taps;
         const uint32_t sbase = act_smem + uint32_t(stage) * kActBytes;
@@ -1236,6 +1272,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
                      const CUtensorMap& mr, const GemmParams& p, int grid, cudaStream_t stream) {
   using C = GemmCfg<BN, SWAP, PAIR, GATHER, KPT>;
   auto kern = k_grouped_gemm_tc<BN, SWAP, HAS_RES, GATHER, PAIR, KPT>;
+  const GemmParams pf = gemm_params_finalize(p);
   static SmemAttrOnce smem_attr;  // one per kernel instantiation, a bit per device
   smem_attr.set(kern, GATHER == 1 ? 232448 : int(C::kBytes));
   cudaLaunchConfig_t cfg = {};
@@ -1254,7 +1291,7 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   }
   cfg.attrs = la;
   cfg.numAttrs = PAIR ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, mr, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, my, mr, pf);
   return e == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
 }
 
