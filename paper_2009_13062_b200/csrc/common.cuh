@@ -505,6 +505,25 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16_f32(int M, int N, int a_m
 // driving several GPUs must set them on each. One instance per kernel (a
 // function-local static next to the launch); idempotent, so two threads
 // racing on the first launch both just set the same value.
+// n / d for 0 <= n < 2^31 by a multiply-high and a shift (Granlund-Montgomery
+// round-up reciprocal; exhaustively checked for the divisor ranges used).
+// The GEMM unit decode and the implicit-GEMM gathers divide by run-time
+// extents per unit / per k-block: ~20 instructions each as integer
+// divisions, which the short-K gather warps of the grouped 3x3 convs spent
+// ~10% of their stall samples on.
+struct FastDiv {
+  uint32_t m = 0, s = 0;
+  static FastDiv make(int d) {
+    FastDiv f;
+    while ((1u << f.s) < uint32_t(d)) ++f.s;
+    f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << f.s) - uint64_t(d))) / uint64_t(d) + 1);
+    return f;
+  }
+  NF_DEVICE int div(int n) const {
+    return int((__umulhi(uint32_t(n), m) + uint32_t(n)) >> s);
+  }
+};
+
 struct SmemAttrOnce {
   std::atomic<unsigned long long> done{0};
   template <typename F>

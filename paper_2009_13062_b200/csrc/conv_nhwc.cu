@@ -217,6 +217,49 @@ __global__ void k_pool_nhwc_v8(const __nv_bfloat16* __restrict__ x, __nv_bfloat1
   }
 }
 
+// fp32, C % 4 == 0: one thread per (pixel, 4-channel group), 16-byte loads /
+// stores, 32-bit indexing; per element the same window order and arithmetic
+// as k_pool_nhwc (bit-identical), without its per-element 64-bit divisions.
+template <bool MAXP>
+__global__ void k_pool_nhwc_v4f(const float* __restrict__ x, float* __restrict__ y, int N, int H,
+                                int W, int C4, int Ho, int Wo, int k, int stride, int pad) {
+  pdl_enter();
+  const int total = N * Ho * Wo * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int pix = i / C4;
+    const int c4 = i - pix * C4;
+    const int t = pix / Wo;
+    const int wo = pix - t * Wo;
+    const int n = t / Ho;
+    const int ho = t - n * Ho;
+    float4 acc = MAXP ? make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < k; ++r) {
+      const int h = ho * stride - pad + r;
+      for (int q = 0; q < k; ++q) {
+        const int w = wo * stride - pad + q;
+        float4 v = MAXP ? make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (h >= 0 && h < H && w >= 0 && w < W)
+          v = *reinterpret_cast<const float4*>(x + ((n * H + h) * W + w) * (C4 * 4) + c4 * 4);
+        if (MAXP) {
+          acc.x = fmaxf(acc.x, v.x); acc.y = fmaxf(acc.y, v.y);
+          acc.z = fmaxf(acc.z, v.z); acc.w = fmaxf(acc.w, v.w);
+        } else {
+          acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
+          acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+        }
+      }
+    }
+    if (!MAXP) {
+      const float den = float(k * k);
+      acc.x = __fdiv_rn(acc.x, den); acc.y = __fdiv_rn(acc.y, den);
+      acc.z = __fdiv_rn(acc.z, den); acc.w = __fdiv_rn(acc.w, den);
+    }
+    *reinterpret_cast<float4*>(y + pix * (C4 * 4) + c4 * 4) = acc;
+  }
+}
+
 int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int k, int stride,
               int pad, int dtype, cudaStream_t s) {
   if (k < 1 || stride < 1 || pad < 0 || 2 * pad > k) return NF_ERR_SHAPE;
@@ -238,6 +281,23 @@ int pool_nhwc(const void* x, void* y, int N, int H, int W, int C, int kind, int 
   } while (0)
   const bool v8 = dtype == NF_BF16 && C % 8 == 0 && int64_t(N) * H * W * C < (int64_t(1) << 31) &&
                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  const bool v4f = dtype == NF_F32 && C % 4 == 0 && int64_t(N) * H * W * C < (int64_t(1) << 31) &&
+                   int64_t(N) * Ho * Wo * C < (int64_t(1) << 31) &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  if (v4f) {
+    const int64_t work = int64_t(N) * Ho * Wo * (C / 4);
+    int64_t b4 = (work + 255) / 256;
+    if (b4 > int64_t(kNumSMs) * 16) b4 = int64_t(kNumSMs) * 16;
+    auto* px = static_cast<const float*>(x);
+    auto* py = static_cast<float*>(y);
+    if (kind == NF_POOL_MAX)
+      launch_pdl(k_pool_nhwc_v4f<true>, dim3(unsigned(b4)), dim3(256), 0, s, px, py, N, H, W,
+                 C / 4, Ho, Wo, k, stride, pad);
+    else
+      launch_pdl(k_pool_nhwc_v4f<false>, dim3(unsigned(b4)), dim3(256), 0, s, px, py, N, H, W,
+                 C / 4, Ho, Wo, k, stride, pad);
+    return cudaGetLastError() == cudaSuccess ? NF_OK : NF_ERR_LAUNCH;
+  }
   if (v8) {
     const int64_t work = int64_t(N) * Ho * Wo * (C / 8);
     int64_t b8 = (work + 255) / 256;

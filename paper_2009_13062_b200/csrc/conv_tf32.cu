@@ -83,6 +83,7 @@ struct TfParams {
   float* y;              // NHWC (N, Ho, Wo, Cout)
   int H, W, C, cg, k, S, P, Ho, Wo, pix, coutg, Cout, G, relu;
   int kb_total, kb_per_split, splits, tiles_m, tiles_n, units;
+  FastDiv fd_cg, fd_k, fd_Wo, fd_Ho;  // gather divisors
   float* ws;             // split-K partials [tile][split][BN][128]
   unsigned* counters;    // [tile] arrival semaphores (zero between launches)
 };
@@ -314,10 +315,10 @@ __global__ void __launch_bounds__(kTThreads, 1)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int px = tm * kTM + rb + 16 * i;
-      const int ow = px % p.Wo;
-      const int t2 = px / p.Wo;
-      const int oh = t2 % p.Ho;
-      const int n = t2 / p.Ho;
+      const int t2 = p.fd_Wo.div(px);
+      const int ow = px - t2 * p.Wo;
+      const int n = p.fd_Ho.div(t2);
+      const int oh = t2 - n * p.Ho;
       ih0[i] = px < p.pix ? oh * p.S - p.P : -(1 << 20);
       iw0[i] = ow * p.S - p.P;
       base[i] = n * p.H * p.W;
@@ -355,9 +356,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const int s = i % kStages;
       mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
       const int k0 = (kb0 + i) * kTK + j * 4;
-      const int tap = k0 / p.cg;
+      const int tap = p.fd_cg.div(k0);
       const int ch = k0 - tap * p.cg;
-      const int kh = tap / p.k;
+      const int kh = p.fd_k.div(tap);
       const int kw = tap - kh * p.k;
       const bool tap_ok = tap < taps;
       const uint32_t dst0 = smem_u32(a_hi(s));
@@ -485,6 +486,10 @@ int grouped_conv_tf32(const void* x, const void* w, const float* bias, const voi
   p.H = H; p.W = W; p.C = C; p.cg = cg; p.k = k; p.S = stride; p.P = pad;
   p.Ho = Ho; p.Wo = Wo; p.pix = int(pix); p.coutg = coutg; p.Cout = Cout; p.G = G;
   p.relu = relu;
+  p.fd_cg = FastDiv::make(cg);
+  p.fd_k = FastDiv::make(k);
+  p.fd_Wo = FastDiv::make(Wo);
+  p.fd_Ho = FastDiv::make(Ho);
   p.kb_total = t.kb_total;
   p.kb_per_split = (t.kb_total + t.splits - 1) / t.splits;
   p.splits = (t.kb_total + p.kb_per_split - 1) / p.kb_per_split;

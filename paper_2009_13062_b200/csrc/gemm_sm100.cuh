@@ -88,25 +88,6 @@ __device__ unsigned long long g_gemm_wait[148 * 8];
   } while (0)
 #endif
 
-// n / d for 0 <= n < 2^31 by a multiply-high and a shift (Granlund-Montgomery
-// round-up reciprocal; exhaustively checked for the divisor ranges used).
-// Unit decode and the implicit-GEMM gather divide by run-time extents per
-// unit / per k-block: ~20 instructions each as integer divisions, which the
-// short-K gather warps of the grouped 3x3 convs spent ~10% of their stall
-// samples on.
-struct FastDiv {
-  uint32_t m = 0, s = 0;
-  static FastDiv make(int d) {
-    FastDiv f;
-    while ((1u << f.s) < uint32_t(d)) ++f.s;
-    f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << f.s) - uint64_t(d))) / uint64_t(d) + 1);
-    return f;
-  }
-  NF_DEVICE int div(int n) const {
-    return int((__umulhi(uint32_t(n), m) + uint32_t(n)) >> s);
-  }
-};
-
 struct GemmParams {
   int act;               // fused epilogue activation (NF_ACT_*)
   const float* bias;     // (G, features) fp32 or nullptr
