@@ -576,6 +576,15 @@ NF_DEVICE void wait_counter(const unsigned* ctr, unsigned target) {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Producer side of wait_counter: one release reduction (the writes ordered
+// before it -- this thread's and, through the barrier the caller passed,
+// its CTA's -- are visible to an acquire that sees the count). Replaces a
+// sequentially consistent __threadfence() + atomicAdd (MEMBAR.SC + L1
+// invalidate on the publishing thread).
+NF_DEVICE void publish_count(unsigned* ctr) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+
 // Non-blocking form of wait_counter: true (and the acquire + proxy fence
 // done) when the counter has arrived.
 NF_DEVICE bool counter_ready(const unsigned* ctr, unsigned target) {

@@ -524,8 +524,7 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
         NF_CT(local, 11, chain_clock());
 #endif
         fence_proxy_async_global();
-        __threadfence();
-        atomicAdd(cp.done_tiles + op * cp.groups + c.g, 1u);
+        publish_count(cp.done_tiles + op * cp.groups + c.g);
 #ifdef NF_CHAIN_TRACE
         NF_CT(local, 5, chain_clock());
 #endif

@@ -516,8 +516,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
     // writes complete and ordered them before this thread): count it
     auto publish = [&](int g) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      __threadfence();
-      atomicAdd(p.done + g / p.link_gpi, 1u);
+      publish_count(p.done + g / p.link_gpi);
     };
     const uint32_t stage_base = smem_u32(sOut);
     // Token-row staged tiles store progressively: each half of the epilogue

@@ -294,10 +294,7 @@ __global__ void __launch_bounds__(192, 1)
       // this head's context is stored: count it for instance g (a chained
       // launch's first op starts g's units at H heads)
       named_bar_sync(1, 128);
-      if (etid == 0) {
-        __threadfence();
-        atomicAdd(done + g, 1u);
-      }
+      if (etid == 0) publish_count(done + g);
     }
   }
   tc_fence_before();
