@@ -585,6 +585,15 @@ NF_DEVICE void publish_count(unsigned* ctr) {
   asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
 }
 
+// Split-K arrival: one acq_rel increment by one thread after a CTA barrier
+// (the CUTLASS semaphore pattern): releases the CTA's partials written
+// before the barrier, and the last arriver acquires the other splits'.
+NF_DEVICE unsigned arrive_acq_rel(unsigned* ctr) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+  return old;
+}
+
 // Non-blocking form of wait_counter: true (and the acquire + proxy fence
 // done) when the counter has arrived.
 NF_DEVICE bool counter_ready(const unsigned* ctr, unsigned target) {

@@ -355,9 +355,8 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
 #pragma unroll
           for (int j = 0; j < EC; ++j) __stcg(mine + (cc + j) * kGemmBM, __uint_as_float(r[j]));
         }
-        __threadfence();
         named_bar_sync(1, kEpiThreads);
-        if (etid == 0) *last_flag = (atomicAdd(p.counters + c.tile, 1u) == unsigned(p.splits - 1));
+        if (etid == 0) *last_flag = (arrive_acq_rel(p.counters + c.tile) == unsigned(p.splits - 1));
         named_bar_sync(1, kEpiThreads);
         if (!*last_flag) {
           tc_fence_before();
@@ -368,7 +367,6 @@ __global__ void __launch_bounds__(64 + 32 * epi_warps<128>(), 1)
           }
           continue;
         }
-        __threadfence();
       }
       if (has_res) {
         mbar_wait(rbar, res_phase);

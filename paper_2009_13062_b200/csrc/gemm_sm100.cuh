@@ -670,9 +670,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
 #pragma unroll
           for (int j = 0; j < EC; ++j) __stcg(mine + (cc + j) * kGemmBM, __uint_as_float(r[j]));
         }
-        __threadfence();
         named_bar_sync(1, kEpiThreads);
-        if (etid == 0) *last_flag = (atomicAdd(p.counters + wtile, 1u) == unsigned(p.splits - 1));
+        if (etid == 0) *last_flag = (arrive_acq_rel(p.counters + wtile) == unsigned(p.splits - 1));
         named_bar_sync(1, kEpiThreads);
         if (!*last_flag) {
           release_acc(acc);
@@ -682,7 +681,6 @@ __global__ void __launch_bounds__(gemm_threads<BN, GATHER>(), 1)
           }
           continue;
         }
-        __threadfence();
       }
       const __nv_bfloat16* res =
           HAS_RES ? reinterpret_cast<const __nv_bfloat16*>(p.residual) +
