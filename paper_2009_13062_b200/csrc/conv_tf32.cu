@@ -267,13 +267,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) __stcg(mine + (cc + j) * kTM, __uint_as_float(r[j]));
       }
-      __threadfence();
       named_bar_sync(1, kTEpi);
       unsigned* arrive = p.counters + tile;
       unsigned* leave = p.counters + kTLeaveOff + tile;
       if (etid == 0) {
         NF_TT(5);
-        atomicAdd(arrive, 1u);
+        publish_count(arrive);  // releases the CTA's partials (after the barrier)
         unsigned seen;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
