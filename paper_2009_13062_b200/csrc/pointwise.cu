@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
   const int units = int(g.R1) * R2 * G;
   const int Cg = int(g.Cg);
   const int nchunks = Cg / V;
+  const bool uniform = nchunks == 32 * Q;  // every lane holds Q chunks of each row
   const uint32_t row_bytes = uint32_t(Cg) * 2u;
   const int u0 = warp_id * units_per_warp;
   const int u1 = min(units, u0 + units_per_warp);
@@ -500,11 +501,16 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
     }
     const int64_t aff = aff_of(cur);
     if (aff != aff_cur) load_affine(aff);
-    // two passes over the registers: mean, then the centred sum of squares
-    // (no E[x^2] - mean^2 cancellation when |mean| >> std); element pairs in
-    // packed fp32x2 arithmetic (FADD2 / FFMA2: half the FP instructions)
+    // Centred statistics, no E[x^2] - mean^2 anywhere (|mean| >> std stays
+    // exact); element pairs in packed fp32x2 arithmetic (FADD2 / FFMA2) over
+    // four independent accumulators. When every lane holds Q chunks, each
+    // lane reduces its own elements (mean, then centred M2) and the lanes merge
+    // pairwise (Chan et al.: equal counts n, m = (ma + mb) / 2, M2 = M2a + M2b
+    // + (mb - ma)^2 n / 2): one butterfly of two independent shuffles instead
+    // of two dependent warp sums (the kernel is bound by that per-row chain).
     float2 v[Q * V / 2];
-    float2 sum2 = make_float2(0.f, 0.f);
+    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                     make_float2(0.f, 0.f)};
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       if (lane + 32 * q < nchunks) {
@@ -515,23 +521,55 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
           float2 t = __bfloat1622float2(px[e]);
           if (has_res) t = __fadd2_rn(t, __bfloat1622float2(pr[e]));
           v[q * V / 2 + e] = t;
-          sum2 = __fadd2_rn(sum2, t);
+          acc[e & 3] = __fadd2_rn(acc[e & 3], t);
         }
       }
     const float inv_c = 1.0f / float(Cg);
-    const float mean = warp_sum(sum2.x + sum2.y) * inv_c;
-    const float2 nmean = make_float2(-mean, -mean);
-    float2 sq2 = make_float2(0.f, 0.f);
+    float rstd;
+    if (uniform) {
+      constexpr float kLocal = float(Q * V);
+      const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+      float m = ((s01.x + s01.y) + (s23.x + s23.y)) * (1.0f / kLocal);
+      const float2 nm = make_float2(-m, -m);
+      float2 q4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                      make_float2(0.f, 0.f)};
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
-      if (lane + 32 * q < nchunks)
+      for (int i = 0; i < Q * V / 2; ++i) {
+        const float2 d = __fadd2_rn(v[i], nm);
+        q4[i & 3] = __ffma2_rn(d, d, q4[i & 3]);
+      }
+      const float2 q01 = __fadd2_rn(q4[0], q4[1]), q23 = __fadd2_rn(q4[2], q4[3]);
+      float m2 = (q01.x + q01.y) + (q23.x + q23.y);
+      float half_n = 0.5f * kLocal;
 #pragma unroll
-        for (int e = 0; e < V / 2; ++e) {
-          const float2 d = __fadd2_rn(v[q * V / 2 + e], nmean);
-          v[q * V / 2 + e] = d;
-          sq2 = __ffma2_rn(d, d, sq2);
-        }
-    const float rstd = rsqrtf(warp_sum(sq2.x + sq2.y) * inv_c + g.eps);
+      for (int o = 1; o < 32; o <<= 1) {
+        const float mb = __shfl_xor_sync(0xffffffffu, m, o);
+        const float m2b = __shfl_xor_sync(0xffffffffu, m2, o);
+        const float d = mb - m;
+        m2 = fmaf(d * d, half_n, m2 + m2b);
+        m = 0.5f * (m + mb);
+        half_n *= 2.f;
+      }
+      const float2 nmean = make_float2(-m, -m);
+#pragma unroll
+      for (int i = 0; i < Q * V / 2; ++i) v[i] = __fadd2_rn(v[i], nmean);
+      rstd = rsqrtf(m2 * inv_c + g.eps);
+    } else {
+      const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+      const float mean = warp_sum((s01.x + s01.y) + (s23.x + s23.y)) * inv_c;
+      const float2 nmean = make_float2(-mean, -mean);
+      float2 sq2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (lane + 32 * q < nchunks)
+#pragma unroll
+          for (int e = 0; e < V / 2; ++e) {
+            const float2 d = __fadd2_rn(v[q * V / 2 + e], nmean);
+            v[q * V / 2 + e] = d;
+            sq2 = __ffma2_rn(d, d, sq2);
+          }
+      rstd = rsqrtf(warp_sum(sq2.x + sq2.y) * inv_c + g.eps);
+    }
     const float2 rstd2 = make_float2(rstd, rstd);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -554,6 +592,171 @@ __global__ void __launch_bounds__(kNormWarps * 32, 2 * 8 / kNormWarps)
 constexpr size_t kNormTmaSmem =
     size_t(kNormWarps) * kNormDepth * 2 * kNormRowBytes + kNormWarps * kNormDepth * 8;
 
+// Lean streaming variant for the merged encoders' LayerNorm layout (C4 / C5):
+// one group per row, rows back to back (model-major instances, per-instance
+// affine blocks of rows_per_affine rows), Cg = 256 Q. Every lane owns Q
+// 16-byte chunks of each row (no per-chunk predicates), a warp walks a
+// contiguous row range with 32-bit shared-memory offsets and pointer
+// increments (no per-row 64-bit cursor arithmetic), and the row statistics
+// are merged across lanes in one butterfly (Chan et al.). ncu on the general
+// kernel: ~480 issued instructions per row at 6 cycles per issue, i.e. bound
+// by per-warp issue latency, not by bytes in flight; this kernel issues about
+// half as many and fits three 8-warp blocks per SM.
+#ifndef NF_LN_DEPTH
+#define NF_LN_DEPTH 4
+#endif
+#ifndef NF_LN_BLOCKS
+#define NF_LN_BLOCKS 2
+#endif
+constexpr int kLnDepth = NF_LN_DEPTH;
+constexpr int kLnBlocks = NF_LN_BLOCKS;  // resident 8-warp blocks per SM
+constexpr int kLnWarps = 8;
+constexpr size_t kLnSmem = size_t(kLnWarps) * kLnDepth * 2 * kNormRowBytes + kLnWarps * kLnDepth * 8;
+
+template <int Q>
+__global__ void __launch_bounds__(kLnWarps * 32, kLnBlocks)
+    k_layer_norm_rows(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
+                      const float* __restrict__ gamma, const float* __restrict__ beta,
+                      __nv_bfloat16* __restrict__ y, int rows, int rpa, float eps,
+                      int rows_per_warp) {
+  constexpr int C = 256 * Q;
+  constexpr uint32_t kRow = uint32_t(C) * 2u;  // bytes of one row
+  extern __shared__ __align__(128) uint8_t nsm[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int r0 = (int(blockIdx.x) * kLnWarps + wib) * rows_per_warp;
+  const int n = min(rows, r0 + rows_per_warp) - r0;
+  uint8_t* ring = nsm + size_t(wib) * kLnDepth * 2 * kNormRowBytes;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(nsm + size_t(kLnWarps) * kLnDepth * 2 * kNormRowBytes) +
+      wib * kLnDepth;
+  if (lane == 0)
+    for (int d = 0; d < kLnDepth; ++d) mbar_init(&bars[d], 1);
+  fence_barrier_init();
+  __syncwarp();
+  grid_dependents_launch();
+  const bool has_res = res != nullptr;
+  float2 ga[Q * 4], be[Q * 4];
+  auto load_affine = [&](int blk) {
+    const float* gp = gamma + int64_t(blk) * C + lane * 8;
+    const float* bp = beta + int64_t(blk) * C + lane * 8;
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int e = 0; e < 8; e += 4) {
+        const float4 a4 = __ldg(reinterpret_cast<const float4*>(gp + q * 256 + e));
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp + q * 256 + e));
+        ga[(q * 8 + e) / 2] = make_float2(a4.x, a4.y);
+        ga[(q * 8 + e) / 2 + 1] = make_float2(a4.z, a4.w);
+        be[(q * 8 + e) / 2] = make_float2(b4.x, b4.y);
+        be[(q * 8 + e) / 2 + 1] = make_float2(b4.z, b4.w);
+      }
+  };
+  int blk = n > 0 ? r0 / rpa : 0;
+  int next_blk_row = (blk + 1) * rpa;  // first row of the next affine block
+  if (n > 0) load_affine(blk);         // a weight: before the dependency wait
+  grid_dependency_wait();
+  if (n <= 0) return;
+  const __nv_bfloat16* xi = x + int64_t(r0) * C;  // next row lane 0 issues
+  const __nv_bfloat16* ri = has_res ? res + int64_t(r0) * C : nullptr;
+  auto issue = [&](int slot) {
+    uint8_t* dst = ring + size_t(slot) * 2 * kNormRowBytes;
+    mbar_arrive_expect_tx(&bars[slot], has_res ? 2 * kRow : kRow);
+    bulk_load_1d(dst, xi, kRow, &bars[slot]);
+    xi += C;
+    if (has_res) {
+      bulk_load_1d(dst + kNormRowBytes, ri, kRow, &bars[slot]);
+      ri += C;
+    }
+  };
+  if (lane == 0)
+    for (int k = 0; k < min(n, kLnDepth); ++k) issue(k);
+  const uint32_t sl0 = smem_u32(ring) + uint32_t(lane) * 16u;
+  __nv_bfloat16* yo = y + int64_t(r0) * C + lane * 8;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int k = 0; k < n; ++k) {
+    mbar_wait(&bars[slot], phase);
+    const uint32_t sa = sl0 + uint32_t(slot) * (2u * kNormRowBytes);
+    uint4 ux[Q], ur[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      ux[q] = ld_shared_v4(sa + q * 512);
+      if (has_res) ur[q] = ld_shared_v4(sa + kNormRowBytes + q * 512);
+    }
+    __syncwarp();  // every lane has its chunks: the slot can be refilled
+    if (lane == 0 && k + kLnDepth < n) {
+      fence_proxy_async_smem();  // generic reads of the slot before the async refill
+      issue(slot);
+    }
+    if (r0 + k == next_blk_row) {
+      ++blk;
+      next_blk_row += rpa;
+      load_affine(blk);
+    }
+    float2 v[Q * 4];
+    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                     make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const __nv_bfloat162* px = reinterpret_cast<const __nv_bfloat162*>(&ux[q]);
+      const __nv_bfloat162* pr = reinterpret_cast<const __nv_bfloat162*>(&ur[q]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 t = __bfloat1622float2(px[e]);
+        if (has_res) t = __fadd2_rn(t, __bfloat1622float2(pr[e]));
+        v[q * 4 + e] = t;
+        acc[e] = __fadd2_rn(acc[e], t);
+      }
+    }
+    // per-lane mean and centred M2, merged pairwise across lanes (equal counts)
+    const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+    float m = ((s01.x + s01.y) + (s23.x + s23.y)) * (1.0f / float(Q * 8));
+    float2 q4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                    make_float2(0.f, 0.f)};
+    {
+      const float2 nm = make_float2(-m, -m);
+#pragma unroll
+      for (int i = 0; i < Q * 4; ++i) {
+        const float2 d = __fadd2_rn(v[i], nm);
+        q4[i & 3] = __ffma2_rn(d, d, q4[i & 3]);
+      }
+    }
+    const float2 q01 = __fadd2_rn(q4[0], q4[1]), q23 = __fadd2_rn(q4[2], q4[3]);
+    float m2 = (q01.x + q01.y) + (q23.x + q23.y);
+    float half_n = 0.5f * float(Q * 8);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float mb = __shfl_xor_sync(0xffffffffu, m, o);
+      const float m2b = __shfl_xor_sync(0xffffffffu, m2, o);
+      const float d = mb - m;
+      m2 = fmaf(d * d, half_n, m2 + m2b);
+      m = 0.5f * (m + mb);
+      half_n *= 2.f;
+    }
+    const float rstd = rsqrtf(m2 * (1.0f / float(C)) + eps);
+    const float2 nmean = make_float2(-m, -m), rstd2 = make_float2(rstd, rstd);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      uint4 uo;
+      uint32_t* po = reinterpret_cast<uint32_t*>(&uo);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = q * 4 + e;
+        const float2 o = __ffma2_rn(__fadd2_rn(v[i], nmean), __fmul2_rn(ga[i], rstd2), be[i]);
+        po[e] = pack_bf16x2(o.x, o.y);
+      }
+      *reinterpret_cast<uint4*>(yo + q * 256) = uo;
+    }
+    yo += C;
+    if (++slot == kLnDepth) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
+
 int group_norm(const void* x, const void* residual, const float* gamma, const float* beta,
                void* y, const NormGeomC& gc, int dtype, cudaStream_t s) {
   NormGeom g{gc.R1, gc.R2, gc.s1, gc.s2, gc.G, gc.Cg, gc.sg, gc.sc, gc.rows_per_affine, gc.eps};
@@ -575,7 +778,28 @@ int group_norm(const void* x, const void* residual, const float* gamma, const fl
 #ifndef NF_NORM_TMA_MIN
 #define NF_NORM_TMA_MIN (4 * 148 * 16)
 #endif
-    if (vec && q <= 3 && units >= NF_NORM_TMA_MIN) {
+    // back-to-back rows of one group, Cg = 256 q (the merged encoders' LayerNorm)
+    const bool rows_lean = vec && g.G == 1 && g.Cg % 256 == 0 && g.Cg <= 768 &&
+                           g.s2 == g.Cg && (g.R1 == 1 || g.s1 == g.R2 * g.s2) &&
+                           (g.rows_per_affine <= 0 || g.rows_per_affine <= g.R1 * g.R2);
+    if (rows_lean && units >= NF_NORM_TMA_MIN) {
+      static SmemAttrOnce la1, la2, la3;
+      const int rows = int(units);
+      const int rpa = g.rows_per_affine > 0 ? int(g.rows_per_affine) : rows;
+      const int warps = 148 * kLnBlocks * kLnWarps;
+      const int per = (rows + warps - 1) / warps;
+      const int nw = (rows + per - 1) / per;
+      const int lgrid = (nw + kLnWarps - 1) / kLnWarps;
+      auto go = [&](auto kern, SmemAttrOnce& a) {
+        a.set(kern, int(kLnSmem));
+        launch_pdl(kern, dim3(lgrid), dim3(kLnWarps * 32), kLnSmem, s, px, pr, gamma, beta, py,
+                   rows, rpa, g.eps, per);
+      };
+      const int cq = int(g.Cg / 256);
+      if (cq == 1) go(k_layer_norm_rows<1>, la1);
+      else if (cq == 2) go(k_layer_norm_rows<2>, la2);
+      else go(k_layer_norm_rows<3>, la3);
+    } else if (vec && q <= 3 && units >= NF_NORM_TMA_MIN) {
       // enough rows for each warp of 2 resident blocks per SM to stream several
       static SmemAttrOnce attr1, attr2, attr3;
       attr1.set(k_group_norm_tma<1>, int(kNormTmaSmem));

@@ -313,3 +313,29 @@ def test_space_to_depth_stem_is_an_exact_repack(n, g, cg, h, w):
     body[..., :cg] = blk
     want[:, 1:, 1:] = body.reshape(n, h // 2, w // 2, g * 16)
     assert torch.equal(y, want)
+
+
+@pytest.mark.parametrize("m,rows", [(3, 4001), (32, 1024)])
+def test_group_norm_model_major_contiguous_rows(m, rows):
+    """The C4 / C5 merged LayerNorm layout: x (m, rows, 768) model-major, one
+    group, per-instance affine blocks (rows_per_affine = rows), on the
+    TMA-ring kernel with lane-merged (Chan) statistics; a ragged row count
+    leaves warps with a short unit range that crosses an instance boundary.
+    Reference: fp32 LayerNorm of the same bf16 inputs per instance."""
+    from paper_2009_13062_b200 import _lib
+    gen = torch.Generator().manual_seed(rows)
+    d = 768
+    x = (torch.rand(m, rows, d, generator=gen) * 2 - 1).bfloat16().cuda()
+    r = (torch.rand(m, rows, d, generator=gen) - 0.5).bfloat16().cuda()
+    gam = (torch.rand(m, d, generator=gen) + 0.5).cuda()
+    bet = (torch.rand(m, d, generator=gen) - 0.5).cuda()
+    y = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("nf_group_norm", x.data_ptr(), r.data_ptr(), gam.data_ptr(), bet.data_ptr(),
+              y.data_ptr(), m, rows, rows * d, d, 1, d, d, 1, rows, 1e-12, _lib.NF_BF16, st)
+    torch.cuda.synchronize()
+    for j in range(m):
+        ref = torch.nn.functional.layer_norm(x[j].float() + r[j].float(), (d,), gam[j], bet[j],
+                                             eps=1e-12)
+        err = ((y[j].float() - ref).abs().max() / ref.abs().max()).item()
+        assert err < 1e-2, (j, err)
