@@ -15,6 +15,9 @@ def main():
     ap.add_argument("--rows", type=int, default=1024)
     ap.add_argument("--d", type=int, default=768)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--add", action="store_true",
+                    help="time torch.add(x, r, out=y) instead: the same 2-read + 1-write streams")
+    ap.add_argument("--copy", action="store_true", help="time y.copy_(x) (1 read + 1 write)")
     a = ap.parse_args()
     x = torch.randn(a.m, a.rows, a.d, device="cuda").bfloat16()
     r = torch.randn_like(x)
@@ -25,20 +28,28 @@ def main():
     st = torch.cuda.current_stream().cuda_stream
     args = (x.data_ptr(), r.data_ptr(), g.data_ptr(), b.data_ptr(), y.data_ptr(), a.m, a.rows,
             a.rows * a.d, a.d, 1, a.d, a.d, 1, a.rows, 1e-12, _lib.NF_BF16, st)
+    def run():
+        if a.copy:
+            y.copy_(x)
+        elif a.add:
+            torch.add(x, r, out=y)
+        else:
+            _lib.call("nf_group_norm", *args)
+
     for _ in range(3):
-        _lib.call("nf_group_norm", *args)
+        run()
     ts = []
     for _ in range(a.reps):
         flush.zero_()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        _lib.call("nf_group_norm", *args)
+        run()
         e.record()
         ts.append((s, e))
     torch.cuda.synchronize()
     us = sum(s.elapsed_time(e) for s, e in ts) / len(ts) * 1e3
-    nbytes = 3 * x.numel() * 2
-    print(json.dumps({"rows": a.m * a.rows, "d": a.d, "us": round(us, 2),
+    nbytes = (2 if a.copy else 3) * x.numel() * 2
+    print(json.dumps({"op": "copy" if a.copy else ("torch.add" if a.add else "nf_group_norm"), "rows": a.m * a.rows, "d": a.d, "us": round(us, 2),
                       "GBps": round(nbytes / us / 1e3, 1)}))
 
 
