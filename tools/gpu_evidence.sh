@@ -31,7 +31,7 @@ full)  # one --set full capture of each config's top kernels
       -k regex:"$2" -c $3 -o gpurun_out/ev_full_$4 python tools/ncu_forward.py --config $1 \
       > gpurun_out/ev_full_$4.log 2>&1; echo "full $4 rc=$?"
   }
-  full C5 "k_grouped_gemm_tc|k_attention_tc|k_group_norm" 5 c5
+  full C5 "k_grouped_gemm_tc|k_attention_tc|k_layer_norm_rows|k_group_norm" 5 c5
   full C4 "k_rel_attention|k_grouped_gemm_tc" 5 c4
   full C3 k_grouped_gemm_tc 6 c3
   full C2 "k_linear_chain_tc|k_qkv" 2 c2
