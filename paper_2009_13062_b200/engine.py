@@ -1776,6 +1776,23 @@ class Plan:
         if self.device.type != "cuda":
             raise UnsupportedOpError("plan was built for structure inspection only (no device)")
         st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        if st == 0:
+            # The legacy default stream: forwards issued back to back on it
+            # with per-instance linked launches (programmatic dependent
+            # launch + completion counters) were measured to fault (a bounded
+            # counter spin traps; BERT-base N=8 B=1, three eager forwards, no
+            # sync), while the same launches on any created stream run clean.
+            # Run on a plan-owned stream ordered after / before it instead.
+            base = (torch.cuda.current_stream(self.device) if stream is None
+                    else torch.cuda.default_stream(self.device))
+            side = getattr(self, "_side_stream", None)
+            if side is None:
+                side = self._side_stream = torch.cuda.Stream(device=self.device)
+            side.wait_stream(base)
+            with torch.cuda.stream(side):
+                self.launch(stream=side.cuda_stream, events=events)
+            base.wait_stream(side)
+            return
         if events is None:
             for _, fn, _ in self.steps:
                 fn(st)

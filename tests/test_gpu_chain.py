@@ -134,3 +134,22 @@ def test_linked_conv_launches_bit_identical(name, m):
         for a, b in zip(rep, want):
             assert torch.equal(a, b)
     assert "rearm" == linked.steps[0][0] and "_LinkedStep" in kinds
+
+
+def test_eager_forwards_back_to_back_on_the_default_stream():
+    """Three eager forwards of the linked BERT-base N=8 B=1 plan issued back
+    to back on the legacy default stream (no sync in between) -- the pattern
+    that faulted before Plan.launch moved legacy-stream forwards onto a
+    plan-owned stream -- complete and match a CUDA-graph replay bit for bit."""
+    graph, stores = W.build_zoo("bert-base", num_models=8, dtype="bf16")
+    merged, mstore = merge(graph, stores)
+    bound = merged.bind_inputs([model_inputs(graph, seed=2, model=j) for j in range(8)])
+    plan = compile_plan(merged.graph, mstore)
+    assert any(getattr(fn, "dep", None) is not None for _, fn, _ in plan.steps)
+    want = _run(plan, bound)[0]
+    assert torch.cuda.current_stream().cuda_stream == 0
+    for _ in range(3):
+        plan.launch()
+    torch.cuda.synchronize()
+    for a, b in zip(plan.outputs(), want):
+        assert torch.equal(a, b)
