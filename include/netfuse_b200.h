@@ -356,6 +356,14 @@ int nf_space_to_depth_stem(const void* x, void* y, int N, int groups, int cg, in
                            void* stream);
 
 /*
+ * Re-arm per-instance completion counters (linked launches) for the next
+ * forward: zeroes `bytes` at `counters` with a memset on `stream`, ordered
+ * with the stream's kernels (capturable into a CUDA graph). Replaces no
+ * reference interface: the linked launches are this port's own schedule.
+ */
+int nf_counters_rearm(void* counters, int64_t bytes, void* stream);
+
+/*
  * Layout glue: y[i0..] = x[i0..] over an up-to-8-D index space with
  * arbitrary element strides on both sides. Realises the merger's
  * Transpose/Reshape junctions (merger.py:237-301) and Pack/Unpack

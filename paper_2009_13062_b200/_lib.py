@@ -74,6 +74,7 @@ SIGNATURES: dict[str, list] = {
     "nf_grouped_conv2d": [_p, _p, _p, _p, _p, _p] + [_i64] * 5 + [_i] * 7 + [_p],
     "nf_elementwise": [_i, _p, _p, _p, _i64, _i, _p],
     "nf_copy_strided": [_p, _p, _i, _p, _p, _p, _i, _p],
+    "nf_counters_rearm": [_p, _i64, _p],
     "nf_group_norm": [_p, _p, _p, _p, _p] + [_i64] * 9 + [_f, _i, _p],
     "nf_softmax": [_p, _p] + [_i64] * 6 + [_i, _p],
     "nf_attention": [_p, _p, _i64, _i64, _i64, _i64, _f, _i, _i, _p],

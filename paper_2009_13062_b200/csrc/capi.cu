@@ -76,6 +76,14 @@ int nf_elementwise(int op, const void* a, const void* b, void* y, int64_t n, int
   return nf::elementwise(op, a, b, y, n, dtype, static_cast<cudaStream_t>(stream));
 }
 
+int nf_counters_rearm(void* counters, int64_t bytes, void* stream) {
+  if (!counters || bytes < 0) return NF_ERR_SHAPE;
+  return cudaMemsetAsync(counters, 0, size_t(bytes), static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? NF_OK
+             : NF_ERR_LAUNCH;
+}
+
 int nf_copy_strided(const void* x, void* y, int rank, const int64_t* dims,
                     const int64_t* x_strides, const int64_t* y_strides, int elem_bytes,
                     void* stream) {

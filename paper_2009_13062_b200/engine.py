@@ -609,10 +609,13 @@ class Plan:
         if getattr(self, "_rearm_bufs", None) is None:
             self._rearm_bufs = []
 
+            # A memset on the launch stream itself (nf_counters_rearm), not a
+            # torch fill under an ExternalStream context: on the legacy default
+            # stream (handle 0) that fill was measured racing the next
+            # forward's linked launches (a counter spin trapped).
             def rearm(st, bufs=self._rearm_bufs):
-                with torch.cuda.stream(torch.cuda.ExternalStream(st, device=bufs[0].device)):
-                    for b in bufs:
-                        b.zero_()
+                for b in bufs:
+                    _lib.call("nf_counters_rearm", b.data_ptr(), b.numel() * b.element_size(), st)
             self.steps.insert(0, ("rearm", rearm, 0))
         self._rearm_bufs.append(buf)
 
@@ -1776,23 +1779,6 @@ class Plan:
         if self.device.type != "cuda":
             raise UnsupportedOpError("plan was built for structure inspection only (no device)")
         st = torch.cuda.current_stream().cuda_stream if stream is None else stream
-        if st == 0:
-            # The legacy default stream: forwards issued back to back on it
-            # with per-instance linked launches (programmatic dependent
-            # launch + completion counters) were measured to fault (a bounded
-            # counter spin traps; BERT-base N=8 B=1, three eager forwards, no
-            # sync), while the same launches on any created stream run clean.
-            # Run on a plan-owned stream ordered after / before it instead.
-            base = (torch.cuda.current_stream(self.device) if stream is None
-                    else torch.cuda.default_stream(self.device))
-            side = getattr(self, "_side_stream", None)
-            if side is None:
-                side = self._side_stream = torch.cuda.Stream(device=self.device)
-            side.wait_stream(base)
-            with torch.cuda.stream(side):
-                self.launch(stream=side.cuda_stream, events=events)
-            base.wait_stream(side)
-            return
         if events is None:
             for _, fn, _ in self.steps:
                 fn(st)

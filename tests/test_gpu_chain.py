@@ -139,8 +139,9 @@ def test_linked_conv_launches_bit_identical(name, m):
 def test_eager_forwards_back_to_back_on_the_default_stream():
     """Three eager forwards of the linked BERT-base N=8 B=1 plan issued back
     to back on the legacy default stream (no sync in between) -- the pattern
-    that faulted before Plan.launch moved legacy-stream forwards onto a
-    plan-owned stream -- complete and match a CUDA-graph replay bit for bit."""
+    that faulted while the per-forward counter re-arm was a torch fill under
+    an ExternalStream(0) context (now a memset on the launch stream,
+    nf_counters_rearm) -- complete and match a CUDA-graph replay bit for bit."""
     graph, stores = W.build_zoo("bert-base", num_models=8, dtype="bf16")
     merged, mstore = merge(graph, stores)
     bound = merged.bind_inputs([model_inputs(graph, seed=2, model=j) for j in range(8)])
